@@ -1,0 +1,179 @@
+/*
+ * quantspec_b200.h -- C ABI of the B200 (sm_100a) QuantSpec decode hot path.
+ *
+ * The reference (arXiv 2502.10424, /root/reference/pkg/src/quantspec) has no
+ * FFI: its boundary is a duck-typed Python protocol.  Each entry point below
+ * names the reference function / method whose work it replaces (Q/ =
+ * pkg/src/quantspec/).  INTEGRATION.md shows the ctypes binding.
+ *
+ * Conventions
+ *   - every call returns qs_status (0 = OK); qs_last_error() gives the text.
+ *   - every call is stream-ordered on the caller's cudaStream_t (passed as
+ *     void*), performs no allocation and no host synchronisation.
+ *   - all buffers are caller-owned device pointers; sizes are element counts.
+ *   - status codes map onto the reference exception taxonomy Q/errors.py:4-33.
+ */
+#ifndef QUANTSPEC_B200_H
+#define QUANTSPEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QS_OK = 0,
+  QS_ERR_DIMENSION = 1, /* DimensionError        Q/errors.py:8  */
+  QS_ERR_CONFIG = 2,    /* ConfigError           Q/errors.py:12 */
+  QS_ERR_DATA = 3,      /* DataError             Q/errors.py:16 */
+  QS_ERR_INTEGRITY = 4, /* CacheIntegrityError   Q/errors.py:24 */
+  QS_ERR_OVERFLOW = 5,  /* BufferOverflowError   Q/errors.py:28 */
+  QS_ERR_CUDA = 6       /* CUDA launch / runtime failure          */
+} qs_status;
+
+/* attention modes (view kinds of Q/model.py:351-356) */
+enum { QS_VIEW_DRAFT = 0, QS_VIEW_TARGET = 1, QS_VIEW_FP16 = 2 };
+
+/* linear-layer epilogues (the per-layer dataflow of Q/model.py:377-397) */
+enum {
+  QS_EPI_STORE = 0,    /* y = x @ W                                  */
+  QS_EPI_ADD = 1,      /* out += x @ W    (residual add)             */
+  QS_EPI_QKV = 2,      /* q/k RoPE (Q/tensor.py:65-82), q store, k/v append (Q/cache.py:216-234) */
+  QS_EPI_SILU_MUL = 3  /* silu(x@Wg) * (x@Wu)  (Q/model.py:397)      */
+};
+enum { QS_W_F16 = 0, QS_W_INT4 = 1 };
+
+/* Split-K flash-decode over the hierarchical store for one layer.
+ * Replaces draft_view/target_view (Q/cache.py:309-378) + _merged_attention
+ * (Q/model.py:176-195) for T query rows at once (Q/specdec.py:270-273). */
+typedef struct {
+  int B, Hkv, hd, G, T, r; /* r = query heads per kv head (1 = MHA) */
+  int n_queries;           /* T * r                                   */
+  int n_qgroups;           /* query-column groups (grid.y split)      */
+  int n_main;              /* main-region splits per head             */
+  int row_offset;          /* provisional rows already appended this cycle */
+  int main_is_fpcache;     /* 1: main region is an fp16 cache (causal tail) */
+  int fpcache_cps;         /* chunks per split for the fp16 cache       */
+  float sm_scale_log2;     /* log2(e) / sqrt(hd)                        */
+  const float* q;          /* [B][T][q_row_stride]                     */
+  float* out;              /* [B][T][q_row_stride]                     */
+  int64_t q_row_stride;
+  const int* n_blocks;     /* [B] quantised blocks                     */
+  const int* fp1_len;      /* [B]                                      */
+  const int* fp2_len;      /* [B] committed fp2 rows                   */
+  const int* fp_len;       /* [B] fp16-cache rows                      */
+  /* quantised planes, layer base (seq 0) */
+  const uint8_t *ku, *kl, *vu, *vl;
+  int64_t plane_seq_stride, plane_head_stride; /* bytes */
+  const void *kp, *vp;                         /* float2 (S,Z) */
+  int64_t kp_seq_stride, kp_head_stride, vp_seq_stride, vp_head_stride; /* float2 units */
+  /* fp16 main region (sensitive-layer archive or fp16 cache) */
+  const void *main_k, *main_v; /* half */
+  int64_t main_seq_stride, main_head_stride; /* halves */
+  /* fp1 / fp2 recent-token buffers (half) */
+  const void *fp1_k, *fp1_v, *fp2_k, *fp2_v;
+  int64_t fp_seq_stride; /* halves */
+  float* partials;       /* scratch */
+  int* counters;         /* [B*Hkv*n_qgroups] zero-initialised */
+} qs_attn_args;
+
+/* x @ W with fused epilogue.  Replaces the fp32 `h @ W` products of
+ * decode_step (Q/model.py:379-397) and, for QS_W_INT4, the dequantised f32
+ * copies of quantize_model_weights (Q/model.py:141-168). */
+typedef struct {
+  int wmode;          /* QS_W_F16 | QS_W_INT4                       */
+  int epi;            /* QS_EPI_*                                    */
+  int N, K;           /* output rows (d_out), reduction (d_in)       */
+  int ncols;          /* activation rows (B*T) <= 8*ncol_tiles       */
+  int ksplit;         /* k-ranges (grid.y)                           */
+  int krange;         /* k-steps (16) per range                      */
+  int wgroup;         /* INT4 group size along d_in                  */
+  const void* w;      /* frag16 halves or frag4 u32                  */
+  const void* wparams;/* INT4: float4 {S_g,Z_g,S_g8,Z_g8} per (mtile,group,g) */
+  const float* x;     /* [ncols][K] activations                      */
+  float* y;           /* [ncols][ldy] output (STORE/ADD/SILU)        */
+  int64_t ldy;
+  float* work;        /* split-K partial scratch                     */
+  int* counters;      /* [N/64] zero-initialised                     */
+  /* QKV epilogue */
+  int Nq, Nk, hd, T;  /* q rows, k rows (= v rows), head dim, rows per sequence */
+  float* q_out;       /* [ncols][Nq]                                 */
+  void *k_dst, *v_dst;/* half, head-major rows                       */
+  int64_t kv_seq_stride, kv_head_stride; /* halves */
+  const int* row_base;/* [B] first free row (fp2_len or fp16-cache len) */
+  int row_offset;
+  const int* pos_base;/* [B] position of row_base (seq_len)         */
+  const void* rope;   /* float2 [max_pos][hd/2] (cos, sin)           */
+  int max_pos;
+} qs_linear_args;
+
+/* KV store descriptor (device pointers + geometry), Q/cache.py:42-133 */
+typedef struct {
+  int B, L, Hkv, hd, G, max_blocks;
+  uint8_t *ku, *kl, *vu, *vl; /* [B][L][Hkv][max_blocks][G*hd/2]          */
+  void *kp, *vp;              /* float2 [B][L][Hkv][max_blocks][hd or G]   */
+  void *fp_k, *fp_v;          /* half [B][L][2][Hkv][G][hd]                */
+  void *arch_k, *arch_v;      /* half [B][n_sens][Hkv][max_blocks*G][hd]   */
+  uint64_t sens_mask[2];      /* bit l set: layer l is sensitive (archives fp16) */
+} qs_kv_store;
+
+const char* qs_version(void);
+qs_status qs_last_error(char* buf, size_t n);
+qs_status qs_device_check(void);
+
+/* ---- L0 quantisation entry points (Q/quant.py) ---- */
+/* encode_plane_hierarchical Q/quant.py:251-276 (with encode_plane_asym :220-248) */
+qs_status qs_encode_plane_hierarchical(const double* values, int64_t count, int group, int64_t row_len,
+                                       uint8_t* upper_codes, uint8_t* lower_codes, float* upper_scales,
+                                       float* upper_zeros, float* lower_scales, int* flags, void* stream);
+/* quantize_group_sym_s4 Q/quant.py:83-91 (scale already rounded to f32) */
+qs_status qs_quantize_sym_s4(const double* values, int64_t count, float scale, int8_t* codes, int* flags,
+                             void* stream);
+/* decode_plane_draft / decode_plane_target Q/quant.py:293-309 (target if lower_codes != NULL) */
+qs_status qs_decode_plane(const uint8_t* upper_codes, const uint8_t* lower_codes, const float* scales,
+                          const float* zeros, int64_t count, int group, int64_t row_len, double* out,
+                          void* stream);
+/* quantize_weights Q/quant.py:335-349: reference plane + frag4 device layout */
+qs_status qs_quantize_weights(const float* w, int d_in, int d_out, int group, uint8_t* ref_codes,
+                              float* scales, float* zeros, uint32_t* frag4, void* frag_params, int* flags,
+                              void* stream);
+/* fp16 weights into frag16 layout (no reference counterpart: storage format) */
+qs_status qs_pack_weights_f16(const float* w, int d_in, int d_out, void* frag16, void* stream);
+/* ---- L1 KV store (Q/cache.py) ---- */
+/* _quantize_block Q/cache.py:283-303 for nblk consecutive blocks of one (seq, layer)
+ * from head-major fp16 rows src[Hkv][src_rows][hd]; writes blocks dst_block.. */
+qs_status qs_kv_quantize_blocks(const qs_kv_store* st, int seq, int layer, const void* src_k, const void* src_v,
+                                int64_t src_head_stride, int nblk, int dst_block, int* flags, void* stream);
+/* flush_if_full Q/cache.py:249-281, full-fp1 branch: quantise fp1 of every layer
+ * into block dst_block, then fp1 <- fp2 */
+qs_status qs_kv_flush(const qs_kv_store* st, int seq, int dst_block, int* flags, void* stream);
+/* _decode_block / _quantized_region Q/cache.py:317-343: f32 view of blocks [0, nblk) */
+qs_status qs_kv_dequant_view(const qs_kv_store* st, int seq, int layer, int nblk, int target, float* out_k,
+                             float* out_v, void* stream);
+
+/* ---- L2 forward pieces (Q/model.py) ---- */
+qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream);
+int qs_attn_partials_floats(const qs_attn_args* a);
+qs_status qs_linear(const qs_linear_args* a, void* stream);
+/* rmsnorm Q/tensor.py:35-42 over rows [n][d] */
+qs_status qs_rmsnorm(const float* x, const float* gain, float* out, int n, int d, float eps, void* stream);
+/* embedding lookup (Q/model.py:375) for n tokens */
+qs_status qs_embed(const float* table, const int* tokens, float* out, int n, int d, int vocab, int* flags,
+                   void* stream);
+/* greedy selection np.argmax (first max), Q/specdec.py:209-212 */
+qs_status qs_argmax(const float* logits, int n, int vocab, int* out_idx, int out_stride, void* stream);
+/* greedy verification Q/specdec.py:276-299: drafts[0..gamma-1] (the verify
+ * forward's tokens 1..gamma), tgt[0..gamma] = target argmax per row.  Writes
+ * res = {v, next_token}, *next_token = next (the next cycle's pending token),
+ * and adds v+1 (rows kept after rollback(gamma - v)) to *bump0 / *bump1. */
+qs_status qs_greedy_accept(const int* drafts, const int* target, int gamma, int* res, int* next_token,
+                           int* bump0, int* bump1, void* stream);
+/* device-side length bump (append bookkeeping of Q/cache.py:234) */
+qs_status qs_add_int(int* p, int n, int delta, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QUANTSPEC_B200_H */

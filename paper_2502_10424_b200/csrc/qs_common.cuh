@@ -1,0 +1,179 @@
+// Shared device helpers for the QuantSpec B200 kernels (sm_100a only).
+//
+// Fragment conventions (mma.sync.m16n8k16, f16 x f16 -> f32), used by every
+// kernel that dequantises in registers:
+//   A (16x16, row-major): lane (g = lane>>2, t = lane&3) holds
+//     a0 = (row g,   cols 2t,2t+1)   a1 = (row g+8, cols 2t,2t+1)
+//     a2 = (row g,   cols 2t+8,2t+9) a3 = (row g+8, cols 2t+8,2t+9)
+//   B (16x8):  b0 = (rows 2t,2t+1, col g)  b1 = (rows 2t+8,2t+9, col g)
+//   D (16x8):  d0,d1 = (row g, cols 2t,2t+1)  d2,d3 = (row g+8, cols 2t,2t+1)
+//
+// Packed 4-bit A fragment ("frag4"): one u32 per lane per 16x16 tile.  Nibble
+// p (bits 4p..4p+3) holds A element
+//     j = p & 3, h = p >> 2:  row = g + 8*(j&1),  col = 2t + 8*(j>>1) + h
+// so a_j = lop3(x >> 4*(j&~1)..) style extraction yields (lo=nibble j, hi=nibble j+4)
+// directly as an f16x2 pair with the 0x6400 magic exponent.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef __CUDA_ARCH__
+#define QS_HOST_ONLY 1
+#endif
+
+namespace qs {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// tensor-core MMA (legacy warp-level path; per-column independent, so the
+// result for one query column does not depend on how many columns ride along)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t x, uint32_t mask, uint32_t magic) {
+  uint32_t r;
+  // (x & mask) | magic
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(x), "r"(mask), "r"(magic));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t lop3_select(uint32_t a, uint32_t b, uint32_t mask) {
+  // (a & mask) | (b & ~mask)
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;\n" : "=r"(r) : "r"(a), "r"(b), "r"(mask));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t h2_as_u32(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u32_as_h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+
+// 8 unsigned nibbles -> four exact f16x2 A registers (values 0..15).
+__device__ __forceinline__ void unpack_u4(uint32_t x, uint32_t (&a)[4]) {
+  const uint32_t MAGIC = 0x64006400u;  // f16 1024.0 in both halves
+  const __half2 k1024 = __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400));
+  const __half2 k1_16 = __halves2half2(__ushort_as_half(0x2C00), __ushort_as_half(0x2C00));  // 1/16
+  const __half2 km64 = __halves2half2(__ushort_as_half(0xD400), __ushort_as_half(0xD400));   // -64
+  uint32_t t = x >> 8;
+  a[0] = h2_as_u32(__hsub2(u32_as_h2(lop3_and_or(x, 0x000F000Fu, MAGIC)), k1024));
+  a[1] = h2_as_u32(__hfma2(u32_as_h2(lop3_and_or(x, 0x00F000F0u, MAGIC)), k1_16, km64));
+  a[2] = h2_as_u32(__hsub2(u32_as_h2(lop3_and_or(t, 0x000F000Fu, MAGIC)), k1024));
+  a[3] = h2_as_u32(__hfma2(u32_as_h2(lop3_and_or(t, 0x00F000F0u, MAGIC)), k1_16, km64));
+}
+
+// Upper nibbles x (c_u in 0..15) and lower nibbles y stored offset-binary
+// (c_l + 8 in 0..15) -> four f16x2 registers holding the exact combined code
+// 16*c_u + c_l (0..240 for codes produced by the encoder).
+__device__ __forceinline__ void unpack_u4l4(uint32_t x, uint32_t y, uint32_t (&a)[4]) {
+  const __half2 k1032 = __halves2half2(__ushort_as_half(0x6408), __ushort_as_half(0x6408));  // 1032
+  uint32_t ev = lop3_select(x << 4, y, 0xF0F0F0F0u);         // bytes: codes at nibble pos 0,2,4,6
+  uint32_t od = lop3_select(x, y >> 4, 0xF0F0F0F0u);         // bytes: codes at nibble pos 1,3,5,7
+  const uint32_t M = 0x64646464u;
+  a[0] = h2_as_u32(__hsub2(u32_as_h2(prmt(ev, M, 0x4240u)), k1032));  // pos0 (ev.b0), pos4 (ev.b2)
+  a[1] = h2_as_u32(__hsub2(u32_as_h2(prmt(od, M, 0x4240u)), k1032));  // pos1, pos5
+  a[2] = h2_as_u32(__hsub2(u32_as_h2(prmt(ev, M, 0x4341u)), k1032));  // pos2, pos6
+  a[3] = h2_as_u32(__hsub2(u32_as_h2(prmt(od, M, 0x4341u)), k1032));  // pos3, pos7
+}
+
+// split an f32 into f16 hi + f16 lo (hi + lo reproduces ~22 bits)
+__device__ __forceinline__ void split_hl(float v, __half& hi, __half& lo) {
+  hi = __float2half_rn(v);
+  lo = __float2half_rn(v - __half2float(hi));
+}
+
+// ---------------------------------------------------------------------------
+// ldmatrix / cp.async / bulk copy / mbarrier
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred = true) {
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity));
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// TMA-engine 1-D bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace qs

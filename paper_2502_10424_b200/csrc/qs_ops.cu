@@ -1,0 +1,140 @@
+// Small fused decode ops (sm_100a): RMSNorm, embedding gather, greedy argmax
+// and the device-side greedy accept/rollback bookkeeping.
+//   rmsnorm          /root/reference/pkg/src/quantspec/tensor.py:35-42
+//   embedding        /root/reference/pkg/src/quantspec/model.py:375
+//   argmax selection /root/reference/pkg/src/quantspec/specdec.py:209-212
+//   greedy verify    /root/reference/pkg/src/quantspec/specdec.py:276-299
+#include <math.h>
+
+#include "qs_common.cuh"
+#include "qs_api_internal.h"
+
+namespace qs {
+
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ gain, float* __restrict__ out,
+                               int d, float eps) {
+  const float* xr = x + (size_t)blockIdx.x * d;
+  float* orow = out + (size_t)blockIdx.x * d;
+  __shared__ float red[32];
+  float a = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) a += __fmul_rn(xr[i], xr[i]);
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  float ms = __fdiv_rn(red[0], (float)d);
+  float r = __fsqrt_rn(__fadd_rn(ms, eps));
+  for (int i = threadIdx.x; i < d; i += blockDim.x) orow[i] = __fmul_rn(__fdiv_rn(xr[i], r), gain[i]);
+}
+
+__global__ void embed_kernel(const float* __restrict__ table, const int* __restrict__ tok, float* __restrict__ out,
+                             int d, int vocab, int* flags) {
+  int t = tok[blockIdx.x];
+  if (t < 0 || t >= vocab) {
+    if (threadIdx.x == 0 && flags) atomicOr(flags, 2);
+    t = 0;
+  }
+  const float4* src = reinterpret_cast<const float4*>(table + (size_t)t * d);
+  float4* dst = reinterpret_cast<float4*>(out + (size_t)blockIdx.x * d);
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
+  for (int i = (d / 4) * 4 + threadIdx.x; i < d; i += blockDim.x) out[(size_t)blockIdx.x * d + i] = table[(size_t)t * d + i];
+}
+
+// larger value wins; NaN counts as the maximum (np.argmax returns the first NaN);
+// ties go to the lower index
+__device__ __forceinline__ bool better(float va, int ia, float vb, int ib) {
+  bool na = isnan(va), nb = isnan(vb);
+  if (na || nb) {
+    if (na && nb) return ia < ib;
+    return na;
+  }
+  if (va != vb) return va > vb;
+  return ia < ib;
+}
+
+__global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int* __restrict__ out, int out_stride) {
+  const float* row = logits + (size_t)blockIdx.x * vocab;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    float v = row[i];
+    if (better(v, i, bv, bi)) {
+      bv = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = bv;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (better(sv[w], si[w], bv, bi)) {
+        bv = sv[w];
+        bi = si[w];
+      }
+    out[(size_t)blockIdx.x * out_stride] = bi;
+  }
+}
+
+// tokens[0..gamma] of the verify forward = (pending, d_0..d_{gamma-1});
+// tgt[i] = argmax of target row i.  Greedy rule of Q/specdec.py:279-298.
+__global__ void greedy_accept_kernel(const int* __restrict__ drafts, const int* __restrict__ tgt, int gamma,
+                                     int* __restrict__ res, int* __restrict__ next_tok, int* bump0, int* bump1) {
+  if (threadIdx.x != 0) return;
+  int v = 0;
+  while (v < gamma && drafts[v] == tgt[v]) ++v;
+  int nxt = tgt[v];
+  res[0] = v;
+  res[1] = nxt;
+  if (next_tok) *next_tok = nxt;
+  if (bump0) *bump0 += v + 1;  // rows kept after rollback(gamma - v)
+  if (bump1) *bump1 += v + 1;
+}
+
+__global__ void add_int_kernel(int* p, int n, int delta) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] += delta;
+}
+
+cudaError_t launch_rmsnorm(const float* x, const float* gain, float* out, int n, int d, float eps, cudaStream_t s) {
+  rmsnorm_kernel<<<n, 256, 0, s>>>(x, gain, out, d, eps);
+  return cudaGetLastError();
+}
+cudaError_t launch_embed(const float* table, const int* tok, float* out, int n, int d, int vocab, int* flags,
+                         cudaStream_t s) {
+  embed_kernel<<<n, 256, 0, s>>>(table, tok, out, d, vocab, flags);
+  return cudaGetLastError();
+}
+cudaError_t launch_argmax(const float* logits, int n, int vocab, int* out, int out_stride, cudaStream_t s) {
+  argmax_kernel<<<n, 512, 0, s>>>(logits, vocab, out, out_stride);
+  return cudaGetLastError();
+}
+cudaError_t launch_greedy_accept(const int* drafts, const int* tgt, int gamma, int* res, int* next_tok, int* b0,
+                                 int* b1, cudaStream_t s) {
+  greedy_accept_kernel<<<1, 32, 0, s>>>(drafts, tgt, gamma, res, next_tok, b0, b1);
+  return cudaGetLastError();
+}
+cudaError_t launch_add_int(int* p, int n, int delta, cudaStream_t s) {
+  add_int_kernel<<<(n + 127) / 128, 128, 0, s>>>(p, n, delta);
+  return cudaGetLastError();
+}
+
+}  // namespace qs

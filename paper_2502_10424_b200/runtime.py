@@ -1,0 +1,403 @@
+"""Device-resident decoder runtime: packed weights, the per-forward kernel
+sequence, and CUDA-graph capture of draft / verify phases.
+
+One forward over T query rows per sequence replaces T reference
+``decode_step`` calls (/root/reference/pkg/src/quantspec/model.py:324-407):
+
+  embed -> per layer [rmsnorm -> QKV linear (+RoPE, +k/v append into fp2)
+  -> split-K attention over the store -> O linear (+residual) -> rmsnorm
+  -> gate/up linear (+SiLU*up) -> down linear (+residual)] -> rmsnorm ->
+  lm_head -> argmax
+
+Every launch goes through the C ABI in libqsb200.so.  Kernel arguments that
+change between steps (lengths, tokens) live in device memory, so a captured
+graph stays valid across cycles; the only host sync per speculative cycle
+is the readback of (accepted count, next token).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError
+
+SM_COUNT = 148
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# packed weights
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Geometry:
+    num_layers: int
+    hidden: int
+    num_heads: int
+    num_kv_heads: int
+    head_dim: int
+    mlp_hidden: int
+    vocab: int
+    max_positions: int
+    rope_base: float = 10000.0
+    norm_eps: float = 1e-5
+
+    @property
+    def nq(self) -> int:
+        return self.num_heads * self.head_dim
+
+    @property
+    def nk(self) -> int:
+        return self.num_kv_heads * self.head_dim
+
+
+def rope_table(hd: int, base: float, max_pos: int):
+    """cos/sin per (position, pair) computed exactly like Q/tensor.py:50-62 (f64 -> f32)."""
+    torch = _torch()
+    ex = np.arange(hd // 2, dtype=np.float64) * (2.0 / hd)
+    inv = base ** -ex
+    out = np.empty((max_pos, hd // 2, 2), dtype=np.float32)
+    step = 1 << 14
+    for p0 in range(0, max_pos, step):
+        pos = np.arange(p0, min(max_pos, p0 + step), dtype=np.float64)[:, None]
+        th = pos * inv[None, :]
+        out[p0 : p0 + pos.shape[0], :, 0] = np.cos(th).astype(np.float32)
+        out[p0 : p0 + pos.shape[0], :, 1] = np.sin(th).astype(np.float32)
+    return torch.from_numpy(out).cuda()
+
+
+def pack_f16(w):
+    """[d_in, d_out] f32 CUDA tensor -> frag16 halves."""
+    torch = _torch()
+    d_in, d_out = (int(x) for x in w.shape)
+    out = torch.empty((d_out // 16) * (d_in // 16) * 32 * 8, dtype=torch.float16, device=w.device)
+    _lib.call("qs_pack_weights_f16", w.data_ptr(), d_in, d_out, out.data_ptr(), _lib.stream_ptr())
+    return out
+
+
+def interleave_tiles(a, b, ntiles: int):
+    """Interleave two packed matrices m-tile by m-tile (gate/up fusion)."""
+    torch = _torch()
+    return torch.stack([a.view(ntiles, -1), b.view(ntiles, -1)], dim=1).reshape(-1)
+
+
+class PackedLinear:
+    """One linear layer in device layout (frag16 or frag4 + params)."""
+
+    def __init__(self, wmode: int, N: int, K: int, w, params=None, group: int = 0):
+        self.wmode, self.N, self.K, self.w, self.params, self.group = wmode, N, K, w, params, group
+
+    @classmethod
+    def f16(cls, w):
+        return cls(_lib.W_F16, int(w.shape[1]), int(w.shape[0]), pack_f16(w))
+
+    @classmethod
+    def f16_pair(cls, wa, wb):
+        a, b = pack_f16(wa), pack_f16(wb)
+        n = int(wa.shape[1])
+        return cls(_lib.W_F16, 2 * n, int(wa.shape[0]), interleave_tiles(a, b, n // 16))
+
+    @classmethod
+    def int4(cls, w, group: int):
+        from .quant import quantize_weights_device
+
+        _, _, _, frag, fp, g = quantize_weights_device(w, group, want_plane=False, want_frag=True)
+        return cls(_lib.W_INT4, int(w.shape[1]), int(w.shape[0]), frag, fp, g)
+
+    @classmethod
+    def int4_pair(cls, wa, wb, group: int):
+        from .quant import quantize_weights_device
+
+        _, _, _, fa, pa, g = quantize_weights_device(wa, group, want_plane=False, want_frag=True)
+        _, _, _, fb, pb, _ = quantize_weights_device(wb, group, want_plane=False, want_frag=True)
+        n = int(wa.shape[1])
+        return cls(_lib.W_INT4, 2 * n, int(wa.shape[0]), interleave_tiles(fa, fb, n // 16),
+                   interleave_tiles(pa, pb, n // 16), g)
+
+    def nbytes(self) -> int:
+        b = self.w.numel() * self.w.element_size()
+        if self.params is not None:
+            b += self.params.numel() * self.params.element_size()
+        return int(b)
+
+    def algorithmic_bytes(self) -> float:
+        """Bytes a GEMV must stream: 2 B/weight (f16) or 0.5 B/weight + 8 B/group (INT4)."""
+        n_w = self.N * self.K
+        if self.wmode == _lib.W_F16:
+            return 2.0 * n_w
+        return 0.5 * n_w + 8.0 * self.N * math.ceil(self.K / self.group)
+
+
+class DeviceWeights:
+    """Packed weights of one role (target fp16, or draft INT4) on the device."""
+
+    def __init__(self, geo: Geometry, layers: list[dict], lm_head: PackedLinear, *, embedding, attn_norms,
+                 mlp_norms, final_norm, rope, wmode: int):
+        self.geo = geo
+        self.layers = layers  # dict(qkv, o, gu, down)
+        self.lm_head = lm_head
+        self.embedding = embedding
+        self.attn_norms = attn_norms
+        self.mlp_norms = mlp_norms
+        self.final_norm = final_norm
+        self.rope = rope
+        self.wmode = wmode
+
+    def nbytes(self) -> int:
+        return sum(pl.nbytes() for lw in self.layers for pl in lw.values()) + self.lm_head.nbytes()
+
+    def algorithmic_bytes(self) -> float:
+        return sum(pl.algorithmic_bytes() for lw in self.layers for pl in lw.values()) + self.lm_head.algorithmic_bytes()
+
+
+def build_device_weights(geo: Geometry, layer_mats, embedding, final_norm, lm_head, attn_norms, mlp_norms, *,
+                         int4_group: int | None = None, rope=None, want_fp16: bool = True):
+    """layer_mats: iterable yielding per-layer dicts of CUDA f32 [d_in, d_out] tensors.
+
+    Returns (fp16 DeviceWeights or None, INT4 DeviceWeights or None); tensors
+    are consumed one layer at a time so only packed copies stay resident.
+    """
+    torch = _torch()
+    rope = rope if rope is not None else rope_table(geo.head_dim, geo.rope_base, geo.max_positions)
+    f_layers, q_layers = [], []
+    for mats in layer_mats:
+        qkv = torch.cat([mats["wq"], mats["wk"], mats["wv"]], dim=1)
+        if want_fp16:
+            f_layers.append(dict(qkv=PackedLinear.f16(qkv), o=PackedLinear.f16(mats["wo"]),
+                                 gu=PackedLinear.f16_pair(mats["w_gate"], mats["w_up"]),
+                                 down=PackedLinear.f16(mats["w_down"])))
+        if int4_group:
+            q_layers.append(dict(qkv=PackedLinear.int4(qkv, int4_group), o=PackedLinear.int4(mats["wo"], int4_group),
+                                 gu=PackedLinear.int4_pair(mats["w_gate"], mats["w_up"], int4_group),
+                                 down=PackedLinear.int4(mats["w_down"], int4_group)))
+        del qkv
+    common = dict(embedding=embedding, attn_norms=attn_norms, mlp_norms=mlp_norms, final_norm=final_norm, rope=rope)
+    fw = DeviceWeights(geo, f_layers, PackedLinear.f16(lm_head), wmode=_lib.W_F16, **common) if want_fp16 else None
+    qw = None
+    if int4_group:
+        qw = DeviceWeights(geo, q_layers, PackedLinear.int4(lm_head, int4_group), wmode=_lib.W_INT4, **common)
+    return fw, qw
+
+
+# ---------------------------------------------------------------------------
+# launch planning
+# ---------------------------------------------------------------------------
+
+
+def plan_linear(pl: PackedLinear, ncols: int) -> tuple[int, int]:
+    """(ksplit, krange): enough CTAs to cover the SMs twice, bounded smem."""
+    KS = pl.K // 16
+    mgroups = -(-pl.N // 64)
+    ntc = -(-ncols // 8)
+    ntc = 1 if ntc <= 1 else 2 if ntc <= 2 else 4 if ntc <= 4 else 8
+    align = 4 * max(1, pl.group // 16) if pl.wmode == _lib.W_INT4 else 1
+    max_kr = max(align, (256 // ntc) // align * align)
+    want = max(1, -(-2 * SM_COUNT // mgroups))
+    kr = -(-KS // want)
+    kr = max(kr, 16)
+    kr = min(kr, max_kr)
+    kr = -(-kr // align) * align
+    ks = -(-KS // kr)
+    return ks, kr
+
+
+def plan_attention_splits(n_heads_total: int, max_chunks: int) -> int:
+    """Main-region splits per head: ~2 CTAs per SM, never more than the chunks."""
+    target = max(1, (2 * SM_COUNT) // max(1, n_heads_total))
+    return max(1, min(target, max_chunks))
+
+
+# ---------------------------------------------------------------------------
+# forward runner
+# ---------------------------------------------------------------------------
+
+
+class Runner:
+    """Scratch buffers + kernel sequence for forwards against one cache."""
+
+    def __init__(self, geo: Geometry, cache, *, max_cols: int = 16, attn_splits: int | None = None):
+        torch = _torch()
+        self.geo = geo
+        self.cache = cache
+        self.B = cache.batch
+        self.max_cols = max_cols
+        dev = torch.device("cuda")
+        d, nq = geo.hidden, geo.nq
+        self.x = torch.zeros((max_cols, d), dtype=torch.float32, device=dev)
+        self.xn = torch.zeros_like(self.x)
+        self.q = torch.zeros((max_cols, nq), dtype=torch.float32, device=dev)
+        self.attn = torch.zeros_like(self.q)
+        self.h = torch.zeros((max_cols, geo.mlp_hidden), dtype=torch.float32, device=dev)
+        self.logits = torch.zeros((max_cols, geo.vocab), dtype=torch.float32, device=dev)
+        self.tok = torch.zeros(max_cols + 1, dtype=torch.int32, device=dev)
+        self.amax = torch.zeros(max_cols, dtype=torch.int32, device=dev)
+        self.res = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.is_fp = not hasattr(cache, "d_n_blocks")
+        r = geo.num_heads // geo.num_kv_heads
+        self.r = r
+        # attention scratch sized for the widest launch (T*r query columns)
+        if self.is_fp:
+            max_chunks = -(-cache.capacity // 64)
+        else:
+            max_chunks = -(-cache.max_blocks * cache.layout.group_size // 128)
+        self.attn_splits = attn_splits or plan_attention_splits(self.B * geo.num_kv_heads, max_chunks)
+        self.fp_cps = -(-max_chunks // self.attn_splits) if self.is_fp else 0
+        ncols_q = (max_cols // self.B) * r
+        self.n_qgroups_max = max(1, -(-ncols_q // 12))
+        per = -(-ncols_q // self.n_qgroups_max)
+        nt = max(1, -(-per // 4))
+        nparts = self.B * geo.num_kv_heads * self.n_qgroups_max * (self.attn_splits + 2) * nt * 4 * (geo.head_dim + 2)
+        self.partials = torch.zeros(nparts, dtype=torch.float32, device=dev)
+        self.attn_counters = torch.zeros(self.B * geo.num_kv_heads * self.n_qgroups_max, dtype=torch.int32, device=dev)
+        # linear scratch: ksplit * 64 cols * max N
+        nmax = max(geo.nq + 2 * geo.nk, 2 * geo.mlp_hidden, geo.vocab, geo.hidden)
+        self.work = torch.zeros(64 * 64 * nmax // 8, dtype=torch.float32, device=dev)
+        self.lin_counters = torch.zeros(-(-nmax // 64), dtype=torch.int32, device=dev)
+        self._lin_cache: dict = {}
+
+    # -- linear ---------------------------------------------------------------
+    def _linear(self, pl: PackedLinear, x, y, ncols: int, epi: int, *, ldy: int | None = None, layer: int = 0,
+                T: int = 1, row_offset: int = 0, stream: int) -> None:
+        key = (id(pl), ncols, epi, layer, T, row_offset, self.cache.generation)
+        a = self._lin_cache.get(key)
+        if a is None:
+            geo = self.geo
+            a = _lib.LinearArgs()
+            a.wmode, a.epi, a.N, a.K, a.ncols = pl.wmode, epi, pl.N, pl.K, ncols
+            a.ksplit, a.krange = plan_linear(pl, ncols)
+            ntc = -(-ncols // 8)
+            cols = 8 * (1 if ntc <= 1 else 2 if ntc <= 2 else 4 if ntc <= 4 else 8)
+            if a.ksplit * cols * pl.N > self.work.numel():
+                raise ConfigError("linear split-K scratch too small")
+            a.wgroup = pl.group
+            a.w = pl.w.data_ptr()
+            a.wparams = pl.params.data_ptr() if pl.params is not None else None
+            a.x = x.data_ptr()
+            a.y = y.data_ptr() if y is not None else None
+            a.ldy = ldy if ldy is not None else (y.shape[1] if y is not None else 0)
+            a.work = self.work.data_ptr()
+            a.counters = self.lin_counters.data_ptr()
+            if epi == _lib.EPI_QKV:
+                c = self.cache
+                a.Nq, a.Nk, a.hd, a.T = geo.nq, geo.nk, geo.head_dim, T
+                a.q_out = self.q.data_ptr()
+                a.row_offset = row_offset
+                a.rope = self._rope.data_ptr()
+                a.max_pos = geo.max_positions
+                if self.is_fp:
+                    L, H, cap, hd = c.num_layers, c.kv_heads, c.capacity, c.head_dim
+                    a.k_dst = c.k[0, layer].data_ptr()
+                    a.v_dst = c.v[0, layer].data_ptr()
+                    a.kv_seq_stride = L * H * cap * hd
+                    a.kv_head_stride = cap * hd
+                    a.row_base = c.d_len.data_ptr()
+                    a.pos_base = c.d_len.data_ptr()
+                else:
+                    lay = c.layout
+                    L, H, G, hd = lay.num_layers, lay.kv_heads, lay.group_size, lay.head_dim
+                    a.k_dst = c.fp_k[0, layer, 1].data_ptr()
+                    a.v_dst = c.fp_v[0, layer, 1].data_ptr()
+                    a.kv_seq_stride = L * 2 * H * G * hd
+                    a.kv_head_stride = G * hd
+                    a.row_base = c.d_fp2_len.data_ptr()
+                    a.pos_base = c.d_pos.data_ptr()
+            self._lin_cache[key] = a
+        _lib.check(_lib.load().qs_linear(a, stream), "qs_linear")
+
+    # -- attention --------------------------------------------------------------
+    def _attention(self, layer: int, view: int, T: int, row_offset: int, stream: int) -> None:
+        key = ("attn", layer, view, T, row_offset, self.cache.generation)
+        a = self._lin_cache.get(key)
+        if a is None:
+            geo, c = self.geo, self.cache
+            a = _lib.AttnArgs()
+            a.B, a.Hkv, a.hd, a.T, a.r = self.B, geo.num_kv_heads, geo.head_dim, T, self.r
+            a.n_queries = T * self.r
+            a.n_qgroups = max(1, -(-a.n_queries // 12))
+            a.n_main = self.attn_splits
+            a.row_offset = row_offset
+            a.sm_scale_log2 = float(1.4426950408889634 / math.sqrt(geo.head_dim))
+            a.q, a.out, a.q_row_stride = self.q.data_ptr(), self.attn.data_ptr(), geo.nq
+            a.partials, a.counters = self.partials.data_ptr(), self.attn_counters.data_ptr()
+            if self.is_fp:
+                a.G = 64
+                a.fp_len = c.d_len.data_ptr()
+                a.main_is_fpcache, a.fpcache_cps = 1, self.fp_cps
+                a.main_k, a.main_v = c.k[0, layer].data_ptr(), c.v[0, layer].data_ptr()
+                a.main_seq_stride = c.num_layers * c.kv_heads * c.capacity * c.head_dim
+                a.main_head_stride = c.capacity * c.head_dim
+                mode = _lib.VIEW_FP16
+            else:
+                lay = c.layout
+                L, H, G, hd, MB = lay.num_layers, lay.kv_heads, lay.group_size, lay.head_dim, c.max_blocks
+                a.G = G
+                a.n_blocks, a.fp1_len, a.fp2_len = c.d_n_blocks.data_ptr(), c.d_fp1_len.data_ptr(), c.d_fp2_len.data_ptr()
+                a.fp1_k, a.fp1_v = c.fp_k[0, layer, 0].data_ptr(), c.fp_v[0, layer, 0].data_ptr()
+                a.fp2_k, a.fp2_v = c.fp_k[0, layer, 1].data_ptr(), c.fp_v[0, layer, 1].data_ptr()
+                a.fp_seq_stride = L * 2 * H * G * hd
+                if layer in lay.sensitive_layers:
+                    slot = c._sens.index(layer)
+                    a.main_k, a.main_v = c.arch_k[0, slot].data_ptr(), c.arch_v[0, slot].data_ptr()
+                    a.main_seq_stride = len(c._sens) * H * MB * G * hd
+                    a.main_head_stride = MB * G * hd
+                    mode = _lib.VIEW_FP16
+                else:
+                    pb = G * hd // 2
+                    a.ku, a.kl = c.ku[0, layer].data_ptr(), c.kl[0, layer].data_ptr()
+                    a.vu, a.vl = c.vu[0, layer].data_ptr(), c.vl[0, layer].data_ptr()
+                    a.plane_seq_stride = L * H * MB * pb
+                    a.plane_head_stride = MB * pb
+                    a.kp, a.vp = c.kp[0, layer].data_ptr(), c.vp[0, layer].data_ptr()
+                    a.kp_seq_stride, a.kp_head_stride = L * H * MB * hd, MB * hd
+                    a.vp_seq_stride, a.vp_head_stride = L * H * MB * G, MB * G
+                    mode = view
+            self._lin_cache[key] = (a, mode)
+        else:
+            a, mode = a
+        _lib.check(_lib.load().qs_attn_decode(a, mode, stream), "qs_attn_decode")
+
+    # -- full forward -------------------------------------------------------------
+    def forward(self, w: DeviceWeights, T: int, view: int, *, row_offset: int = 0, tok_offset: int = 0,
+                argmax_to=None, stream=None) -> None:
+        """Run one forward over ``T`` rows per sequence reading tokens from
+        ``self.tok[tok_offset:]``; logits land in ``self.logits[:B*T]``."""
+        geo = self.geo
+        s = _lib.stream_ptr(stream)
+        lib = _lib.load()
+        ncols = self.B * T
+        if ncols > self.max_cols:
+            raise ConfigError(f"forward of {ncols} rows exceeds runner capacity {self.max_cols}")
+        self._rope = w.rope
+        d = geo.hidden
+        tok_ptr = self.tok.data_ptr() + 4 * tok_offset
+        _lib.check(lib.qs_embed(w.embedding.data_ptr(), tok_ptr, self.x.data_ptr(), ncols, d, geo.vocab,
+                                self.flags.data_ptr(), s), "qs_embed")
+        for li, lw in enumerate(w.layers):
+            _lib.check(lib.qs_rmsnorm(self.x.data_ptr(), w.attn_norms[li].data_ptr(), self.xn.data_ptr(), ncols, d,
+                                      geo.norm_eps, s), "qs_rmsnorm")
+            self._linear(lw["qkv"], self.xn, None, ncols, _lib.EPI_QKV, layer=li, T=T, row_offset=row_offset, stream=s)
+            self._attention(li, view, T, row_offset, s)
+            self._linear(lw["o"], self.attn, self.x, ncols, _lib.EPI_ADD, stream=s)
+            _lib.check(lib.qs_rmsnorm(self.x.data_ptr(), w.mlp_norms[li].data_ptr(), self.xn.data_ptr(), ncols, d,
+                                      geo.norm_eps, s), "qs_rmsnorm")
+            self._linear(lw["gu"], self.xn, self.h, ncols, _lib.EPI_SILU_MUL, ldy=geo.mlp_hidden, stream=s)
+            self._linear(lw["down"], self.h, self.x, ncols, _lib.EPI_ADD, stream=s)
+        _lib.check(lib.qs_rmsnorm(self.x.data_ptr(), w.final_norm.data_ptr(), self.xn.data_ptr(), ncols, d,
+                                  geo.norm_eps, s), "qs_rmsnorm")
+        self._linear(w.lm_head, self.xn, self.logits, ncols, _lib.EPI_STORE, stream=s)
+        if argmax_to is not None:
+            _lib.check(lib.qs_argmax(self.logits.data_ptr(), ncols, geo.vocab, argmax_to, 1, s), "qs_argmax")
+
+    def kernel_launches_per_forward(self, nlayers: int) -> int:
+        return 1 + nlayers * 7 + 2

@@ -1,0 +1,502 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle and the
+reference golden vectors.  Needs a B200: run with ``-m gpu``.
+
+Bars (stated per test):
+  * codes, scales, zero points, buffer state, accept decisions: bit-exact;
+  * attention outputs: max |err| <= 2e-3 * max|V| against the oracle's f64
+    _merged_attention over the oracle's views of the SAME fp16 K/V inputs;
+  * linear layers: <= 2e-3 relative (f16 weights/activations, f32 accumulate);
+  * logits: toy model vs the oracle decode_step on identical cache contents.
+"""
+
+import copy
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import qs_oracle as O
+
+from .conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2502_10424_b200 as qs  # noqa: E402
+from paper_2502_10424_b200 import _lib  # noqa: E402
+from paper_2502_10424_b200.runtime import Geometry, Runner  # noqa: E402
+
+
+def f16(a):
+    return np.asarray(a, np.float32).astype(np.float16).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# L0: quantisation entry points vs the reference's own golden vectors
+# ---------------------------------------------------------------------------
+
+
+def test_plane_encode_decode_golden_bit_exact():
+    z = np.load(os.path.join(GOLDEN, "quant_golden.npz"))
+    for i in range(int(z["n_cases"])):
+        g, rl = (int(x) for x in z[f"c{i}_group"])
+        up, lo = qs.encode_plane_hierarchical(z[f"c{i}_values"], g, "channel", rl or None)
+        for tag, p in (("up", up), ("lo", lo)):
+            assert np.array_equal(p.codes, z[f"c{i}_{tag}_codes"]), (i, tag)
+            assert np.array_equal(p.scales.view(np.uint32), z[f"c{i}_{tag}_scales"].view(np.uint32)), (i, tag)
+            assert np.array_equal(p.zeros.view(np.uint32), z[f"c{i}_{tag}_zeros"].view(np.uint32)), (i, tag)
+        assert np.array_equal(qs.decode_plane_draft(up), z[f"c{i}_draft"]), i
+        assert np.array_equal(qs.decode_plane_target(up, lo), z[f"c{i}_target"]), i
+
+
+def test_group_kats_and_errors():
+    with open(os.path.join(GOLDEN, "group_kat.json")) as f:
+        kats = json.load(f)
+    for k in kats:
+        (uc, up), (lc, lp) = qs.hierarchical_encode(k["values"])
+        assert uc.tolist() == k["cu"] and lc.tolist() == k["cl"]
+        assert up.scale == k["S"] and up.zero_point == k["Z"] and lp.scale == k["Sl"]
+    codes, p = qs.quantize_group_asym_u4([0.0, 1.0, 2.0, 3.0])
+    assert codes.tolist() == [0, 5, 10, 15] and p.zero_point == 0.0
+    codes, _ = qs.quantize_group_sym_s4([0.07], scale=0.0125)
+    assert codes.tolist() == [6]
+    codes, _ = qs.quantize_group_sym_s4([0.0125 * 12.0, -0.0125 * 12.0, 0.0125 * 7.49], scale=0.0125)
+    assert codes.tolist() == [7, -8, 7]
+    with pytest.raises(qs.DataError):
+        qs.quantize_group_asym_u4([])
+    with pytest.raises(qs.DataError):
+        qs.quantize_group_asym_u4([1.0, np.nan])
+    with pytest.raises(qs.ConfigError):
+        qs.quantize_group_sym_s4([0.1], scale=0.0)
+    with pytest.raises(qs.CacheIntegrityError):
+        qs.encode_plane_hierarchical(np.arange(10.0), 4, "token", 3)
+
+
+def test_weight_quant_golden_bit_exact():
+    z = np.load(os.path.join(GOLDEN, "quant_golden.npz"))
+    w = z["w_in"]
+    for g in (32, 16, 7):
+        q = qs.quantize_weights(w, g)
+        assert np.array_equal(q.plane.codes, z[f"w{g}_codes"])
+        assert np.array_equal(q.plane.scales, z[f"w{g}_scales"])
+        assert np.array_equal(q.plane.zeros, z[f"w{g}_zeros"])
+        assert np.array_equal(qs.dequantize_weights(q), z[f"w{g}_deq"])
+
+
+# ---------------------------------------------------------------------------
+# L1: the flush kernel (K1) and the store state machine
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("H,hd,G", [(2, 128, 128), (4, 16, 16), (4, 16, 128), (2, 64, 64), (8, 32, 32)])
+def test_flush_quantize_bit_exact_vs_oracle(H, hd, G):
+    rng = np.random.default_rng(H * 1000 + hd + G)
+    kv = H * hd
+    n = 4 * G + 7
+    k = f16(rng.standard_normal((n, kv)) * rng.uniform(0.1, 4.0, kv) + rng.uniform(-2, 2, kv))
+    v = f16(rng.standard_normal((n, kv)) * 3.0)
+    lay = qs.CacheLayout(1, H, hd, G)
+    cache = qs.HierarchicalKVCache.from_prefill(lay, [k], [v])
+    olay = O.Layout(1, H, hd, G)
+    assert cache.quantized_token_count == ((n - G) // G) * G
+    for b in range(cache.quantized_token_count // G):
+        want = O.quantize_kv_block(olay, k[b * G : (b + 1) * G], v[b * G : (b + 1) * G])
+        got = cache.export_block_planes(0, b)
+        for gp, wp in zip(got, (want.ku, want.kl, want.vu, want.vl)):
+            assert np.array_equal(gp.codes, wp.codes), b
+            assert np.array_equal(gp.scales.view(np.uint32), wp.scales.view(np.uint32)), b
+            assert np.array_equal(gp.zeros.view(np.uint32), wp.zeros.view(np.uint32)), b
+    # device f32 views == oracle views (same fp16 inputs), bit for bit
+    oc = O.OracleKVCache.from_prefill(olay, [k], [v])
+    for kind in ("draft", "target"):
+        vw = getattr(cache, f"{kind}_view")(0)
+        ov = oc.view(0, kind)
+        gk, gv = vw.concat()
+        assert np.array_equal(gk, ov.k) and np.array_equal(gv, ov.v), kind
+        assert (vw.quantized_bytes, vw.param_bytes, vw.fp_bytes, vw.quantized_elements) == (
+            ov.quantized_bytes, ov.param_bytes, ov.fp_bytes, ov.quantized_elements)
+
+
+def test_scripted_session_matches_oracle_state_machine():
+    """Replay the reference cache script (tests/golden/cache_script.json) on the
+    device store and on the oracle fed the same fp16-rounded rows."""
+    z = np.load(os.path.join(GOLDEN, "cache_golden.npz"))
+    with open(os.path.join(GOLDEN, "cache_script.json")) as f:
+        script = json.load(f)
+    keys = [f16(z["keys0"]), f16(z["keys1"])]
+    vals = [f16(z["vals0"]), f16(z["vals1"])]
+    lay = qs.CacheLayout(2, 2, 16, 16)
+    dev = qs.HierarchicalKVCache.from_prefill(lay, keys, vals, max_tokens=4096)
+    orc = O.OracleKVCache.from_prefill(O.Layout(2, 2, 16, 16), keys, vals)
+    ak, av = f16(z["appended_k"]), f16(z["appended_v"])
+    for op, arg in script:
+        if op == "append":
+            for layer in range(2):
+                dev.append_decode_token(layer, ak[arg][layer], av[arg][layer])
+                orc.append_decode_token(layer, ak[arg][layer], av[arg][layer])
+        elif op == "rollback":
+            dev.rollback(arg)
+            orc.rollback(arg)
+        elif op == "flush":
+            assert int(dev.flush_if_full()) == arg == int(orc.flush_if_full())
+        else:
+            assert [dev.quantized_token_count, dev.fp1_len, dev.fp2_len] == arg
+    for layer in range(2):
+        for kind in ("draft", "target"):
+            gk, gv = getattr(dev, f"{kind}_view")(layer).concat()
+            ov = orc.view(layer, kind)
+            assert np.array_equal(gk, ov.k) and np.array_equal(gv, ov.v)
+    rep = dev.memory_report()
+    assert [rep.upper_bytes, rep.lower_bytes, rep.param_bytes, rep.fp_buffer_bytes, rep.archived_fp_bytes] == z["mem"].tolist()
+
+
+def test_rollback_overflow_and_errors():
+    lay = qs.CacheLayout(2, 2, 16, 16)
+    rng = np.random.default_rng(1)
+    kv = 32
+    c = qs.HierarchicalKVCache.from_prefill(lay, [rng.standard_normal((32, kv))] * 2, [rng.standard_normal((32, kv))] * 2)
+    for _ in range(16):
+        for layer in range(2):
+            c.append_decode_token(layer, np.zeros(kv), np.zeros(kv))
+    with pytest.raises(qs.BufferOverflowError):
+        c.append_decode_token(0, np.zeros(kv), np.zeros(kv))
+    c.rollback(3)
+    assert c.fp2_len == 13
+    with pytest.raises(qs.CacheIntegrityError):
+        c.rollback(14)
+    with pytest.raises(qs.EmptyPromptError):
+        qs.HierarchicalKVCache.from_prefill(lay, [np.zeros((0, kv))] * 2, [np.zeros((0, kv))] * 2)
+    bad = np.ones((40, kv), np.float32)
+    bad[3, 5] = np.nan
+    with pytest.raises(qs.DataError):
+        qs.HierarchicalKVCache.from_prefill(lay, [bad] * 2, [bad] * 2)
+
+
+def test_sensitive_layers_and_snapshot_round_trip(tmp_path):
+    lay = qs.CacheLayout(2, 2, 16, 16, sensitive_layers=frozenset({0}))
+    rng = np.random.default_rng(2)
+    keys = [f16(rng.standard_normal((3 * 16 + 5, 32))) for _ in range(2)]
+    vals = [f16(rng.standard_normal((3 * 16 + 5, 32))) for _ in range(2)]
+    c = qs.HierarchicalKVCache.from_prefill(lay, keys, vals)
+    k0, v0 = c.draft_view(0).concat()
+    assert np.array_equal(k0, keys[0]) and np.array_equal(v0, vals[0])
+    assert c.draft_view(0).quantized_bytes == 0
+    p = tmp_path / "c.qskv"
+    c.save_snapshot(p)
+    d = qs.HierarchicalKVCache.load_snapshot(p)
+    for layer in range(2):
+        a = c.target_view(layer).concat()
+        b = d.target_view(layer).concat()
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    p2 = tmp_path / "d.qskv"
+    d.save_snapshot(p2)
+    assert p.read_bytes() == p2.read_bytes()
+
+
+def test_snapshot_interoperates_with_oracle_planes(tmp_path):
+    """Planes exported from the device store decode (oracle) to the device view."""
+    lay = qs.CacheLayout(1, 4, 16, 16)
+    rng = np.random.default_rng(4)
+    k = f16(rng.standard_normal((5 * 16, 64)))
+    v = f16(rng.standard_normal((5 * 16, 64)))
+    c = qs.HierarchicalKVCache.from_prefill(lay, [k], [v])
+    ku, kl, vu, vl = c.export_block_planes(0, 1)
+    blk = O.Block(*(O.Plane(p.codes, p.count, p.group_size, p.scales, p.zeros, p.mode, p.axis, p.row_len) for p in (ku, kl, vu, vl)))
+    ok, ov = O.dequant_kv_block(O.Layout(1, 4, 16, 16), blk, "target")
+    gk, gv = c.target_view(0).concat()
+    assert np.array_equal(gk[16:32], ok) and np.array_equal(gv[16:32], ov)
+
+
+# ---------------------------------------------------------------------------
+# L2: attention kernels (K2 draft, K3 verify, K4 fp16) vs oracle _merged_attention
+# ---------------------------------------------------------------------------
+
+
+def _attn_setup(H, hd, G, n_prompt, extra, seed=0, r=1):
+    rng = np.random.default_rng(seed)
+    kv = H * hd
+    k = f16(rng.standard_normal((n_prompt, kv)) * rng.uniform(0.2, 2.0, kv))
+    v = f16(rng.standard_normal((n_prompt, kv)))
+    lay = qs.CacheLayout(1, H * r, hd, G, num_kv_heads=H)
+    cache = qs.HierarchicalKVCache.from_prefill(lay, [k], [v], max_tokens=n_prompt + 4 * G)
+    olay = O.Layout(1, H, hd, G)
+    orc = O.OracleKVCache.from_prefill(olay, [k], [v])
+    rows_k = f16(rng.standard_normal((extra, kv)))
+    rows_v = f16(rng.standard_normal((extra, kv)))
+    return cache, orc, rows_k, rows_v, rng
+
+
+def _run_attention(cache, q, view, T, row_offset=0, r=1):
+    lay = cache.layout
+    geo = Geometry(1, lay.num_heads * lay.head_dim, lay.num_heads, lay.kv_heads, lay.head_dim, 16, 16, 1 << 20)
+    run = Runner(geo, cache, max_cols=max(T, 1))
+    run.q[:T] = torch.from_numpy(q.reshape(T, -1)).cuda()
+    run._attention(0, view, T, row_offset, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    return run.attn[:T].cpu().numpy()
+
+
+@pytest.mark.parametrize("H,hd,G,n_prompt", [(4, 128, 128, 5 * 128 + 40), (4, 16, 16, 300), (4, 16, 128, 700),
+                                             (2, 64, 64, 64 * 9 + 3)])
+@pytest.mark.parametrize("view", ["draft", "target"])
+@pytest.mark.parametrize("T", [1, 5, 9])
+def test_attention_vs_oracle(H, hd, G, n_prompt, view, T):
+    cache, orc, rk, rv, rng = _attn_setup(H, hd, G, n_prompt, T, seed=H + hd + G + T)
+    # append T new rows (as a verify forward would) then attend causally
+    room = G - cache.fp2_len
+    if room < T:
+        pytest.skip("fp2 too full for this T")
+    base = cache.fp2_len
+    for t in range(T):
+        for_oracle = (rk[t], rv[t])
+        cache.fp_k[0, 0, 1, :, base + t] = torch.from_numpy(rk[t]).cuda().half().reshape(H, hd)
+        cache.fp_v[0, 0, 1, :, base + t] = torch.from_numpy(rv[t]).cuda().half().reshape(H, hd)
+    q = (rng.standard_normal((T, H, hd)) * 2.0).astype(np.float32)
+    got = _run_attention(cache, q, _lib.VIEW_DRAFT if view == "draft" else _lib.VIEW_TARGET, T)
+    vmax = 0.0
+    for t in range(T):
+        orc.append_decode_token(0, rk[t], rv[t])
+        vw = orc.view(0, view)
+        want = O.attend_view(q[t], vw, H, hd)
+        vmax = max(vmax, float(np.abs(vw.v).max()))
+        err = np.abs(got[t].reshape(H, hd) - want).max()
+        assert err <= 2e-3 * vmax, (t, err)
+
+
+def test_attention_batch_invariance_bit_exact():
+    """Row t of a T-row launch == the same row launched alone at its position."""
+    H, hd, G = 4, 128, 128
+    cache, orc, rk, rv, rng = _attn_setup(H, hd, G, 3 * 128 + 17, 5, seed=11)
+    base = cache.fp2_len
+    for t in range(5):
+        cache.fp_k[0, 0, 1, :, base + t] = torch.from_numpy(rk[t]).cuda().half().reshape(H, hd)
+        cache.fp_v[0, 0, 1, :, base + t] = torch.from_numpy(rv[t]).cuda().half().reshape(H, hd)
+    q = (rng.standard_normal((5, H, hd)) * 2.0).astype(np.float32)
+    for view in (_lib.VIEW_DRAFT, _lib.VIEW_TARGET):
+        full = _run_attention(cache, q, view, 5)
+        for t in range(5):
+            one = _run_attention(cache, q[t : t + 1], view, 1, row_offset=t)
+            assert np.array_equal(one[0], full[t]), (view, t)
+
+
+def test_fp16_cache_attention_vs_oracle():
+    rng = np.random.default_rng(5)
+    H, hd, n = 4, 128, 1000
+    k = f16(rng.standard_normal((n, H * hd)))
+    v = f16(rng.standard_normal((n, H * hd)))
+    c = qs.FpKVCache.from_prefill([k[:-3]], [v[:-3]], head_dim=hd)
+    for t in range(3):
+        c.k[0, 0, :, n - 3 + t] = torch.from_numpy(k[n - 3 + t]).cuda().half().reshape(H, hd)
+        c.v[0, 0, :, n - 3 + t] = torch.from_numpy(v[n - 3 + t]).cuda().half().reshape(H, hd)
+    geo = Geometry(1, H * hd, H, H, hd, 16, 16, 1 << 20)
+    run = Runner(geo, c, max_cols=3)
+    q = rng.standard_normal((3, H, hd)).astype(np.float32)
+    run.q[:3] = torch.from_numpy(q.reshape(3, -1)).cuda()
+    run._attention(0, _lib.VIEW_FP16, 3, 0, _lib.stream_ptr())
+    got = run.attn[:3].cpu().numpy()
+    for t in range(3):
+        m = n - 3 + t + 1
+        want = O.merged_attention(q[t], [(k[:m].reshape(m, H, hd), v[:m].reshape(m, H, hd))], 1 / math.sqrt(hd))
+        assert np.abs(got[t].reshape(H, hd) - want).max() <= 2e-3 * np.abs(v).max()
+
+
+def test_chunked_attention_matches_monolithic():
+    rng = np.random.default_rng(6)
+    q = rng.standard_normal(16).astype(np.float32)
+    chunks = [(f16(rng.standard_normal((n, 16))), f16(rng.standard_normal((n, 16)))) for n in (7, 33, 1, 64)]
+    got = qs.chunked_attention(q, chunks)
+    k = np.concatenate([c[0] for c in chunks])
+    v = np.concatenate([c[1] for c in chunks])
+    want = O.merged_attention(q.reshape(1, 16), [(k.reshape(-1, 1, 16), v.reshape(-1, 1, 16))], 0.25).ravel()
+    assert np.abs(got - want).max() <= 2e-3 * np.abs(v).max()
+
+
+# ---------------------------------------------------------------------------
+# L2: linear layers (K5 W4A16, K6 fp16) vs an f32 torch reference
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("K,N,ncols", [(64, 48 * 4, 1), (4096, 4096, 1), (176, 64, 5), (4096, 11008 * 2, 9), (11008, 4096, 5)])
+@pytest.mark.parametrize("mode", ["f16", "int4"])
+def test_linear_vs_torch(K, N, ncols, mode):
+    from paper_2502_10424_b200.runtime import PackedLinear, plan_linear
+
+    g = torch.Generator(device="cuda").manual_seed(K + N)
+    w = torch.randn(K, N, device="cuda", generator=g) / math.sqrt(K)
+    x = torch.randn(ncols, K, device="cuda", generator=g)
+    if mode == "f16":
+        pl = PackedLinear.f16(w)
+        wref = w.half().float()
+    else:
+        pl = PackedLinear.int4(w, 32)
+        q = qs.quantize_weights(w.cpu().numpy(), 32)
+        wref = torch.from_numpy(qs.dequantize_weights(q)).cuda()
+    y = torch.zeros(ncols, N, device="cuda")
+    a = _lib.LinearArgs()
+    a.wmode, a.epi, a.N, a.K, a.ncols = pl.wmode, _lib.EPI_STORE, N, K, ncols
+    a.ksplit, a.krange = plan_linear(pl, ncols)
+    a.wgroup = pl.group
+    a.w = pl.w.data_ptr()
+    a.wparams = pl.params.data_ptr() if pl.params is not None else None
+    a.x, a.y, a.ldy = x.data_ptr(), y.data_ptr(), N
+    work = torch.zeros(a.ksplit * 64 * N, device="cuda")
+    cnt = torch.zeros(N // 64 + 1, dtype=torch.int32, device="cuda")
+    a.work, a.counters = work.data_ptr(), cnt.data_ptr()
+    _lib.check(_lib.load().qs_linear(a, _lib.stream_ptr()))
+    ref = x.half().float() @ wref
+    err = (y - ref).abs().max().item()
+    assert err <= 2e-3 * ref.abs().max().item() + 1e-4, err
+    assert int(cnt.sum().item()) == 0  # split-K semaphores reset
+
+
+# ---------------------------------------------------------------------------
+# L2/L3: model forward, accept rule, greedy losslessness
+# ---------------------------------------------------------------------------
+
+TOY = qs.ModelConfig(num_layers=2, num_heads=4, head_dim=16, hidden=64, mlp_hidden=176, vocab=64, max_positions=4096 + 256)
+OTOY = O.Config(2, 4, 16, 64, 176, 64, 4096 + 256)
+
+
+@pytest.fixture(scope="module")
+def toy():
+    return qs.init_weights(TOY, seed=7), O.init_weights(OTOY, seed=7)
+
+
+def _oracle_cache_like(dev_cache):
+    """Oracle cache holding exactly the device cache's contents (fp16 values)."""
+    lay = dev_cache.layout
+    olay = O.Layout(lay.num_layers, lay.num_heads, lay.head_dim, lay.group_size)
+    oc = O.OracleKVCache(olay)
+    G = lay.group_size
+    nb = dev_cache.quantized_token_count // G
+    for layer in range(lay.num_layers):
+        for b in range(nb):
+            ku, kl, vu, vl = dev_cache.export_block_planes(layer, b)
+            oc.blocks[layer].append(O.Block(*(O.Plane(p.codes, p.count, p.group_size, p.scales, p.zeros, p.mode, p.axis, p.row_len) for p in (ku, kl, vu, vl))))
+        for which, n in ((0, dev_cache.fp1_len), (1, dev_cache.fp2_len)):
+            if n:
+                k, v = dev_cache._fp_rows(which, layer, n)
+                buf = oc.fp1 if which == 0 else oc.fp2
+                buf[layer, 0, :n] = k
+                buf[layer, 1, :n] = v
+    oc.fp1_len = dev_cache.fp1_len
+    oc.fp2_lens[:] = dev_cache.fp2_len
+    oc.quantized_token_count = dev_cache.quantized_token_count
+    return oc
+
+
+def test_weights_bit_exact_with_oracle(toy):
+    w, ow = toy
+    assert np.array_equal(w.embedding, ow["embedding"]) and np.array_equal(w.lm_head, ow["lm_head"])
+    for lw, olw in zip(w.layers, ow["layers"]):
+        for n in O.MATS:
+            assert np.array_equal(getattr(lw, n), olw[n])
+
+
+@pytest.mark.parametrize("view", ["draft", "target"])
+def test_decode_step_logits_vs_oracle(toy, view):
+    """Same cache contents, same token: logits agree to fp16-weight tolerance."""
+    w, ow = toy
+    prompt = np.random.default_rng(31).integers(0, 64, size=300)
+    _, cache = qs.prefill(w, prompt, "hierarchical", group_size=16)
+    oc = _oracle_cache_like(cache)
+    # oracle uses the fp16-rounded weights the device holds
+    ow16 = copy.deepcopy(ow)
+    for olw in ow16["layers"]:
+        for n in O.MATS:
+            olw[n] = f16(olw[n])
+    ow16["lm_head"] = f16(ow16["lm_head"])
+    lg, cost = qs.decode_step(w, 11, cache, view=view)
+    olg, ocost = O.decode_step(ow16, 11, oc, view)
+    scale = max(1.0, float(np.abs(olg).max()))
+    assert np.abs(lg - olg).max() <= 2e-2 * scale, np.abs(lg - olg).max()
+    assert [cost.flops, cost.weight_bytes, cost.kv_quantized_bytes, cost.kv_param_bytes, cost.kv_fp_bytes,
+            cost.kv_quantized_elements] == [ocost.flops, ocost.weight_bytes, ocost.kv_quantized_bytes,
+                                            ocost.kv_param_bytes, ocost.kv_fp_bytes, ocost.kv_quantized_elements]
+
+
+def test_greedy_accept_kernel_matches_oracle_rule():
+    rng = np.random.default_rng(9)
+    dev = torch.device("cuda")
+    for trial in range(200):
+        gamma = int(rng.integers(0, 9))
+        V = 37
+        logits = rng.standard_normal((gamma + 1, V)).astype(np.float32)
+        if trial % 3 == 0:
+            logits[:, 5] = logits.max(axis=1) + 0.0  # exact ties -> lowest index wins
+        tgt = logits.argmax(axis=1)
+        drafts = [int(tgt[i]) if rng.random() < 0.7 else int(rng.integers(0, V)) for i in range(gamma)]
+        want_v, corr, bonus = O.greedy_accept(drafts, list(logits))
+        lg = torch.from_numpy(logits).to(dev)
+        am = torch.zeros(gamma + 1, dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().qs_argmax(lg.data_ptr(), gamma + 1, V, am.data_ptr(), 1, _lib.stream_ptr()))
+        toks = torch.tensor([0] + drafts + [0], dtype=torch.int32, device=dev)
+        res = torch.zeros(4, dtype=torch.int32, device=dev)
+        l1 = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().qs_greedy_accept(toks.data_ptr() + 4, am.data_ptr(), gamma, res.data_ptr(),
+                                                toks.data_ptr(), l1.data_ptr(), None, _lib.stream_ptr()))
+        r = res.cpu().tolist()
+        assert am.cpu().tolist() == tgt.tolist()
+        assert r[0] == want_v and r[1] == (corr if corr is not None else bonus)
+        assert int(l1.item()) == want_v + 1 and int(toks[0].item()) == r[1]
+
+
+@pytest.mark.parametrize("gamma", [1, 2, 4, 6])
+def test_greedy_spec_equals_gpu_target_ar(toy, gamma):
+    """Internal exactness: spec decode == target-view AR on the same kernels (token for token)."""
+    w, _ = toy
+    for seed in (2, 5):
+        prompt = np.random.default_rng(seed).integers(0, 64, size=80)
+        res = qs.SpeculativeDecoder(w, qs.SpecConfig(gamma=gamma, decode_len=60), group_size=16).run(prompt)
+        ar = qs.autoregressive_decode(w, prompt, 60, group_size=16)
+        assert res.tokens == ar
+        assert len(res.tokens) == 60
+
+
+def test_int4_draft_still_lossless_and_fp2_edge(toy):
+    w, _ = toy
+    prompt = np.random.default_rng(3).integers(0, 64, size=80)
+    res = qs.SpeculativeDecoder(w, qs.SpecConfig(gamma=4, decode_len=60, weight_mode="int4"), group_size=16).run(prompt)
+    assert res.tokens == qs.autoregressive_decode(w, prompt, 60, group_size=16)
+    prompt = np.random.default_rng(4).integers(0, 64, size=3 * 16 - 1)
+    res = qs.SpeculativeDecoder(w, qs.SpecConfig(gamma=6, decode_len=60), group_size=16).run(prompt)
+    assert res.tokens == qs.autoregressive_decode(w, prompt, 60, group_size=16)
+    assert any(len(s.drafted) < 6 for s in res.trace.steps)
+
+
+def test_lossless_config_accepts_everything(toy):
+    w, _ = toy
+    prompt = np.random.default_rng(1).integers(0, 64, size=40)
+    res = qs.SpeculativeDecoder(w, qs.SpecConfig(gamma=4, decode_len=40), kv_quant=False).run(prompt)
+    assert res.metrics.acceptance_rate == 1.0
+    assert res.tokens == qs.autoregressive_decode(w, prompt, 40, kv_quant=False)
+
+
+def test_graph_replay_equals_eager(toy):
+    w, _ = toy
+    prompt = np.random.default_rng(8).integers(0, 64, size=120)
+    a = qs.SpeculativeDecoder(w, qs.SpecConfig(gamma=4, decode_len=50), group_size=16, use_graphs=True).run(prompt)
+    b = qs.SpeculativeDecoder(w, qs.SpecConfig(gamma=4, decode_len=50), group_size=16, use_graphs=False).run(prompt)
+    assert a.tokens == b.tokens
+    assert a.trace.to_ndjson() == b.trace.to_ndjson()
+
+
+def test_trace_matches_reference_structure(toy):
+    """Emission budget, trace reconciliation and buffer invariants (pkg/tests/test_specdec.py:136-216)."""
+    w, _ = toy
+    for decode_len in (1, 2, 7, 77):
+        prompt = np.random.default_rng(10).integers(0, 64, size=80)
+        res = qs.SpeculativeDecoder(w, qs.SpecConfig(gamma=4, decode_len=decode_len), group_size=16).run(prompt)
+        assert len(res.tokens) == decode_len
+        rebuilt = [res.tokens[0]]
+        for s in res.trace.steps:
+            rebuilt.extend(s.emitted)
+        assert rebuilt == res.tokens
+        for line in res.trace.to_ndjson().strip().splitlines() if res.trace.steps else []:
+            rec = json.loads(line)
+            assert set(rec) == {"step", "drafted", "accepted", "corrected", "bonus", "flushed", "draft_bytes", "target_bytes"}
