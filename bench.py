@@ -1,0 +1,512 @@
+#!/usr/bin/env python
+"""Benchmark of the QuantSpec decode hot path on B200 (BASELINE.json config 3).
+
+Workload (default): Llama-2-7B-shaped random-init model (32 layers, 32 heads,
+hd 128, d 4096, mlp 11008, vocab 32000), a 128K-token synthetic prompt,
+batch 1, gamma = 4, greedy.  A "step" is one draft/verify cycle of
+self-speculative decoding (INT4 hierarchical KV + INT4 draft weights, the
+config-3 mode); the same kernels also run the kv_only mode (fp16 draft
+weights) and the FP16 autoregressive baseline (fp16 weights + fp16 KV) for
+the speed-up.  Prefill is setup, outside every timed region.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle
+(oracle/qs_oracle.py, the NumPy restatement of the reference) on a bounded
+sample of the same workload instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LLAMA2_7B = dict(num_layers=32, num_heads=32, num_kv_heads=32, head_dim=128, hidden=4096, mlp_hidden=11008, vocab=32000)
+METRIC = "decode tokens/sec @128K ctx + speedup vs FP16 AR; attn HBM GB/s vs peak"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=24)
+    p.add_argument("--warmup", type=int, default=4)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--context", type=int, default=131072)
+    p.add_argument("--gamma", type=int, default=4)
+    p.add_argument("--layers", type=int, default=32)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-graphs", action="store_true")
+    p.add_argument("--modes", default="both,kv_only,fp16_ar")
+    p.add_argument("--profile-kernels", action="store_true", help="only run the isolated kernel timings (for ncu)")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sms, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------
+# model + caches (setup, untimed)
+# ---------------------------------------------------------------------------
+
+
+def build_workload(args, dev_index: int):
+    import numpy as np
+    import torch
+
+    from paper_2502_10424_b200 import _lib
+    from paper_2502_10424_b200._prefill import run_prefill
+    from paper_2502_10424_b200.cache import CacheLayout, FpKVCache, HierarchicalKVCache
+    from paper_2502_10424_b200.runtime import DeviceWeights, Geometry, PackedLinear, rope_table
+
+    cfg = dict(LLAMA2_7B)
+    cfg["num_layers"] = args.layers
+    S = args.context
+    margin = 2048
+    geo = Geometry(cfg["num_layers"], cfg["hidden"], cfg["num_heads"], cfg["num_kv_heads"], cfg["head_dim"],
+                   cfg["mlp_hidden"], cfg["vocab"], S + margin)
+    d, m, V = geo.hidden, geo.mlp_hidden, geo.vocab
+    gen = torch.Generator(device="cuda").manual_seed(args.seed + 1000 * dev_index)
+
+    def mat(r, c):
+        # N(0,1)/sqrt(fan_in), the reference's init recipe (Q/model.py:94-95), drawn on device
+        return torch.randn(r, c, device="cuda", generator=gen) / math.sqrt(r)
+
+    t0 = time.time()
+    emb = torch.randn(V, d, device="cuda", generator=gen)
+    head = mat(d, V)
+    ones = torch.ones(d, device="cuda")
+    rope = rope_table(geo.head_dim, geo.rope_base, geo.max_positions)
+    G = 128
+    lay = CacheLayout(geo.num_layers, geo.num_heads, geo.head_dim, G)
+    hcache = HierarchicalKVCache(lay, max_tokens=S + margin)
+    fcache = FpKVCache(geo.num_layers, geo.nk, capacity=S + margin, head_dim=geo.head_dim)
+    f_layers, q_layers = [], []
+
+    def layers():
+        for _ in range(geo.num_layers):
+            mats = {"wq": mat(d, d), "wk": mat(d, d), "wv": mat(d, d), "wo": mat(d, d), "w_gate": mat(d, m),
+                    "w_up": mat(d, m), "w_down": mat(m, d)}
+            qkv = torch.cat([mats["wq"], mats["wk"], mats["wv"]], dim=1)
+            f_layers.append(dict(qkv=PackedLinear.f16(qkv), o=PackedLinear.f16(mats["wo"]),
+                                 gu=PackedLinear.f16_pair(mats["w_gate"], mats["w_up"]), down=PackedLinear.f16(mats["w_down"])))
+            q_layers.append(dict(qkv=PackedLinear.int4(qkv, 32), o=PackedLinear.int4(mats["wo"], 32),
+                                 gu=PackedLinear.int4_pair(mats["w_gate"], mats["w_up"], 32),
+                                 down=PackedLinear.int4(mats["w_down"], 32)))
+            del qkv
+            mats["attn_norm"] = ones
+            mats["mlp_norm"] = ones
+            yield mats
+
+    prompt = torch.from_numpy(np.random.default_rng(args.seed + 1).integers(0, V, size=S).astype(np.int32)).cuda()
+
+    def sink(l, k, v):
+        hcache.load_prefill_layer(l, k, v)
+        fcache.load_prefill_layer(l, k, v)
+
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+
+    with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.CUDNN_ATTENTION]):
+        logits = run_prefill(geo, prompt, emb, layers(), ones, head, rope, sink, dtype=torch.float16)
+    hcache.finish_prefill(S)
+    fcache.finish_prefill(S)
+    common = dict(embedding=emb, attn_norms=[ones] * geo.num_layers, mlp_norms=[ones] * geo.num_layers,
+                  final_norm=ones, rope=rope)
+    fw = DeviceWeights(geo, f_layers, PackedLinear.f16(head), wmode=_lib.W_F16, **common)
+    qw = DeviceWeights(geo, q_layers, PackedLinear.int4(head, 32), wmode=_lib.W_INT4, **common)
+    del head
+    torch.cuda.synchronize()
+    first = int(torch.argmax(logits).item())
+    setup_s = time.time() - t0
+    return geo, fw, qw, hcache, fcache, first, setup_s
+
+
+def time_kernel(fn, iters: int = 20):
+    """Average device time of fn() over iters launches (CUDA events on the launching stream)."""
+    import torch
+
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters / 1e3
+
+
+def kernel_roofline(geo, fw, qw, hcache, fcache, peak):
+    """Isolated timings of the hot kernels at the bench context (inputs >> L2)."""
+    import torch
+
+    from paper_2502_10424_b200 import _lib
+    from paper_2502_10424_b200.runtime import Runner
+
+    out = {}
+    G = hcache.layout.group_size
+    kv = geo.nk
+    nq_tok = hcache.quantized_token_count
+    nfp = hcache.fp1_len + hcache.fp2_len + 1
+    run = Runner(geo, hcache, max_cols=16)
+    run.q.normal_()
+    s = _lib.stream_ptr()
+    per_tok = {"draft": kv * 1.0 + 8.0 * kv / G + 8.0 * math.ceil(kv / G),
+               "target": kv * 2.0 + 8.0 * kv / G + 8.0 * math.ceil(kv / G)}
+    for name, view, T in (("attn_draft", _lib.VIEW_DRAFT, 1), ("attn_verify", _lib.VIEW_TARGET, 5)):
+        dt = time_kernel(lambda: run._attention(0, view, T, 0, s))
+        algo = nq_tok * per_tok["draft" if view == _lib.VIEW_DRAFT else "target"] + (nfp + T) * kv * 4.0 + T * geo.nq * 8.0
+        out[name] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak}
+    frun = Runner(geo, fcache, max_cols=16)
+    frun.q.normal_()
+    n = fcache.seq_len + 1
+    dt = time_kernel(lambda: frun._attention(0, _lib.VIEW_FP16, 1, 0, s))
+    algo = n * kv * 4.0 + geo.nq * 8.0
+    out["attn_fp16"] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak}
+    for name, w in (("gemv_f16_down", fw.layers[0]["down"]), ("gemv_int4_down", qw.layers[0]["down"]),
+                    ("gemv_f16_lm_head", fw.lm_head)):
+        x = run.h if w.K == geo.mlp_hidden else run.xn
+        x.normal_()
+        y = run.x if w.N == geo.hidden else run.logits
+        dt = time_kernel(lambda: run._linear(w, x, y, 1, _lib.EPI_STORE, stream=s))
+        algo = w.algorithmic_bytes() + 4.0 * w.K
+        out[name] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak}
+    torch.cuda.synchronize()
+    return out
+
+
+def measure_spec(fw, dw, cache, first, gamma, steps, warmup, use_graphs, clocks=None):
+    import torch
+
+    from paper_2502_10424_b200.engine import SpecEngine
+
+    eng = SpecEngine(fw, dw, cache, gamma, use_graphs=use_graphs)
+    eng.set_pending(first)
+    nxt = first
+
+    def one():
+        nonlocal nxt
+        gs = max(0, min(gamma, cache.fp2_space() - 1))
+        drafts, v, nxt = eng.cycle(gs)
+        cache.flush_if_full()
+        return gs, v
+
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    l0 = eng.launches
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    emitted = drafted = accepted = 0
+    s.record()
+    for _ in range(steps):
+        gs, v = one()
+        drafted += gs
+        accepted += v
+        emitted += v + 1
+    e.record()
+    torch.cuda.synchronize()
+    dt = s.elapsed_time(e) / 1e3
+    launches = eng.launches - l0
+    # e2e: the public engine API with the step input (pending token) staged from pinned
+    # host memory and the step result (accepted count, tokens) read back every cycle
+    host_tok = torch.zeros(1, dtype=torch.int32).pin_memory()
+    host_tok[0] = nxt
+    e_emit = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        eng.run.tok[0:1].copy_(host_tok, non_blocking=True)
+        gs, v = one()
+        host_tok[0] = nxt
+        e_emit += v + 1
+    torch.cuda.synchronize()
+    e2e_dt = time.perf_counter() - t0
+    return {"tok_s": emitted / dt, "ms_per_step": dt * 1e3 / steps, "acceptance": accepted / max(1, drafted),
+            "tokens_per_cycle": emitted / steps, "e2e_tok_s": e_emit / e2e_dt, "launches": launches,
+            "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4 * (2 + gamma + 1), "context_after": cache.seq_len}
+
+
+def measure_ar(fw, cache, first, steps, warmup, use_graphs):
+    import torch
+
+    from paper_2502_10424_b200.engine import ARAutoEngine
+
+    eng = ARAutoEngine(fw, cache, use_graphs=use_graphs)
+    eng.set_pending(first)
+    for _ in range(warmup):
+        eng.step(sync=False)
+        cache.flush_if_full()
+    torch.cuda.synchronize()
+    l0 = eng.launches
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        eng.step(sync=False)
+        cache.flush_if_full()
+    e.record()
+    torch.cuda.synchronize()
+    dt = s.elapsed_time(e) / 1e3
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        eng.step(sync=True)
+        cache.flush_if_full()
+    e2e_dt = time.perf_counter() - t0
+    return {"tok_s": steps / dt, "ms_per_step": dt * 1e3 / steps, "e2e_tok_s": steps / e2e_dt,
+            "launches": eng.launches - l0}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle (NumPy restatement of the reference) on a bounded sample
+# ---------------------------------------------------------------------------
+
+
+def cpu_baseline(context: int, layers: int, sample_tokens: int = 16384, reps: int = 1):
+    """Per-token target-view AR decode time of the reference algorithm at
+    Llama-2-7B shape, extrapolated from a bounded sample: one layer's
+    attention (oracle merged_attention over a dequantised f32 view of
+    ``sample_tokens`` tokens, scaled linearly to ``context``) plus one
+    layer's f32 projections, times ``layers``, plus the lm_head GEMV."""
+    import numpy as np
+
+    from oracle import qs_oracle as O
+
+    cores = os.cpu_count() or 1
+    H, hd, d, m, V, G = 32, 128, 4096, 11008, 32000, 128
+    rng = np.random.default_rng(0)
+    blk = O.quantize_kv_block(O.Layout(1, H, hd, G), rng.standard_normal((G, d)).astype(np.float32),
+                              rng.standard_normal((G, d)).astype(np.float32))
+    kb, vb = O.dequant_kv_block(O.Layout(1, H, hd, G), blk, "target")
+    reps_blk = sample_tokens // G
+    view = O.View(np.tile(kb, (reps_blk, 1)), np.tile(vb, (reps_blk, 1)))
+    view.segments = [(view.k, view.v)]
+    q = rng.standard_normal((H, hd)).astype(np.float32)
+    mats = [rng.standard_normal((d, n), dtype=np.float32) for n in (3 * d, d)] + [
+        rng.standard_normal((d, 2 * m), dtype=np.float32), rng.standard_normal((m, d), dtype=np.float32)]
+    head = rng.standard_normal((d, V), dtype=np.float32)
+    x = rng.standard_normal(d).astype(np.float32)
+    xm = rng.standard_normal(m).astype(np.float32)
+    t_att, t_mat, t_head = [], [], []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.attend_view(q, view, H, hd)
+        t_att.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        _ = x @ mats[0]
+        _ = x @ mats[1]
+        _ = x @ mats[2]
+        _ = xm @ mats[3]
+        t_mat.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        _ = x @ head
+        t_head.append(time.perf_counter() - t0)
+    att = min(t_att) * context / sample_tokens
+    per_tok = layers * (att + min(t_mat)) + min(t_head)
+    sample_s = sum(t_att) + sum(t_mat) + sum(t_head)
+    return {"value": 1.0 / per_tok, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": (f"oracle target-view decode, 1 layer: merged_attention over {sample_tokens} quantised tokens "
+                       f"(scaled x{context / sample_tokens:.0f} to {context}) + f32 projections, x{layers} layers + lm_head; "
+                       f"extrapolated per-token time {per_tok:.2f} s; sample wall {sample_s:.1f} s"),
+            "per_token_s": per_tok}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    t0 = time.time()
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        pass
+    vals = []
+    cb = None
+    for _ in range(max(1, min(args.steps, 3))):
+        cb = cpu_baseline(args.context, args.layers)
+        vals.append(cb["value"])
+    v = statistics.median(vals)
+    cb["value"] = v
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": len(vals),
+            "warmup": 0, "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64/f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "config3: Llama-2-7B shape, 128K ctx, batch 1, gamma 4 (CPU oracle sample)",
+                       "context": args.context, "layers": args.layers},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.time() - t0}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+
+    __graft_entry__.build()
+    peak, peak_kind = load_peaks()
+    geo, fw, qw, hcache, fcache, first, setup_s = build_workload(args, rank)
+    use_graphs = not args.no_graphs
+    modes = args.modes.split(",")
+    kr = kernel_roofline(geo, fw, qw, hcache, fcache, peak)
+    if args.profile_kernels:
+        print(json.dumps({"kernels": kr}))
+        return
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    res = {}
+    clocks = ClockSampler(local)
+    with clocks:
+        barrier()
+        t_all = time.time()
+        if "both" in modes:
+            res["both"] = measure_spec(fw, qw, hcache, first, args.gamma, args.steps, args.warmup, use_graphs)
+        if "kv_only" in modes:
+            res["kv_only"] = measure_spec(fw, fw, hcache, first, args.gamma, args.steps, args.warmup, use_graphs)
+        if "fp16_ar" in modes:
+            res["fp16_ar"] = measure_ar(fw, fcache, first, args.steps, args.warmup, use_graphs)
+        barrier()
+        wall = time.time() - t_all
+    head = res.get("both") or res.get("kv_only")
+    # max over ranks of the per-step time -> whole-job throughput
+    vals = torch.tensor([head["ms_per_step"], head["tok_s"], head["e2e_tok_s"]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        t = vals.clone()
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        s2 = vals.clone()
+        dist.all_reduce(s2, op=dist.ReduceOp.SUM)
+        ms = float(t[0])
+        value = float(s2[1])
+        e2e = float(s2[2])
+    else:
+        ms, value, e2e = head["ms_per_step"], head["tok_s"], head["e2e_tok_s"]
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return
+    ar = res.get("fp16_ar")
+    dom = kr["attn_draft"]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("attn_draft_bytes_per_launch")
+        except Exception:
+            traffic = None
+    cb = cpu_baseline(args.context, args.layers) if world == 1 or rank == 0 else None
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f16 (KV int4/int8 planes, INT4 draft weights), f32 accumulate",
+        "data": "synthetic (random-init weights, uniform random prompt tokens)",
+        "config": {"workload": "config3: Llama-2-7B shape random init, 128K ctx, batch 1 per GPU, gamma 4, greedy, "
+                               "mode=both (INT4 KV + INT4 draft weights)",
+                   "context": args.context, "layers": args.layers, "gamma": args.gamma,
+                   "l2": "working set per forward (GBs) >> 126 MB L2; no flush needed",
+                   "parallelism": f"replicas x{world} (one sequence per GPU)", "cuda_graphs": use_graphs},
+        "speedup_vs_fp16_ar": (value / world) / ar["tok_s"] if ar else None,
+        "modes": res,
+        "kernels": kr,
+        "roofline": {"bound": "hbm", "kernel": "attn_draft (K2, upper INT4 plane, split-K)", "achieved": dom["gbs"],
+                     "peak": peak, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst copy)", "unit": "GB/s",
+                     "frac": dom["gbs"] / peak, "traffic": traffic, "algorithmic_bytes_per_launch": dom["bytes"]},
+        "cpu_baseline": cb,
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": head["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": head["d2h_bytes_per_step"]},
+        "gpu_launches": head["launches"],
+        "clocks": clocks.summary(),
+        "setup_s": setup_s,
+        "timed_wall_s": wall,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

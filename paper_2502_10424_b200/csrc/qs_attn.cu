@@ -34,8 +34,9 @@ struct AttnCfg {
   static constexpr int VEC = KS >= 4 ? 4 : KS;
   static constexpr int PLANE_CHUNK = HD * QS_CHUNK_Q / 2;  // bytes of one plane per 128-token chunk
   static constexpr int NPLANE = (MODE == MODE_QTARGET) ? 4 : 2;
-  // quant stage: planes + key params (<= 8 blocks * HD) + value params (128 tokens)
-  static constexpr int KP_BYTES = 8 * HD * 8;
+  // quant stage: planes + key params + value params (128 tokens).  Valid
+  // layouts have G >= HD, so a chunk holds (128/G)*HD <= 128 key channels-blocks.
+  static constexpr int KP_BYTES = QS_CHUNK_Q * 8;
   static constexpr int QSTAGE = NPLANE * PLANE_CHUNK + KP_BYTES + QS_CHUNK_Q * 8;
   static constexpr int NSTAGE_Q = (MODE == MODE_QTARGET) ? 3 : 4;
   static constexpr int FSTAGE = 2 * QS_CHUNK_F * HD * 2;  // K + V fp16 rows
@@ -44,7 +45,7 @@ struct AttnCfg {
   static constexpr int REGION_F = NSTAGE_F * FSTAGE;
   static constexpr int REGION = REGION_Q > REGION_F ? REGION_Q : REGION_F;
   static constexpr int NQ = NT * 4;                        // query columns (hi/lo pairs) per CTA
-  static constexpr int BQ_WORDS = 8 * KS * NT * 32 * 2;    // u32 per Bq buffer (8 blocks max)
+  static constexpr int BQ_WORDS = 8 * NT * 32 * 2;         // u32 per Bq buffer: (128/G)*KS <= 8 tiles
   static constexpr int PW_HALVES = 2 * NT * 8 * 16;        // per-warp P transpose tile
   // merge scratch reuses REGION: 4 warps * NQ * (HD + 4) floats
   static constexpr int MERGE_FLOATS = 4 * NQ * (HD + 4);

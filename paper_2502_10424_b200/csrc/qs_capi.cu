@@ -186,6 +186,8 @@ qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream) {
   if (per > 12) QS_FAIL(QS_ERR_CONFIG, "at most 12 query columns per CTA (got %d); raise n_qgroups", per);
   if (a->n_main < 1) QS_FAIL(QS_ERR_CONFIG, "need at least one main split");
   if (mode != QS_VIEW_FP16 && (a->G % 16 || a->G > 128 || 128 % a->G)) QS_FAIL(QS_ERR_CONFIG, "group size %d unsupported", a->G);
+  if (mode != QS_VIEW_FP16 && !(a->G % a->hd == 0 || a->Hkv * a->hd <= a->G))
+    QS_FAIL(QS_ERR_CONFIG, "value groups of %d channels would split a %d-channel head", a->G, a->hd);
   return cuda_status(launch_attention(*a, mode, S(stream)), "attn_decode");
 }
 

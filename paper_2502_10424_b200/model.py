@@ -366,7 +366,7 @@ def verify_step(weights: ModelWeights, tokens, cache, *, view: str = "target", w
 def prefill(weights: ModelWeights, tokens, cache_mode: str = "fp", *, group_size: int | None = None,
             sensitive_layers: frozenset = frozenset(), max_tokens: int | None = None):
     """Causal forward over the prompt; returns last-token logits and a device cache (Q/model.py:268-321)."""
-    from .prefill import prefill_device
+    from ._prefill import prefill_device
 
     cfg = weights.config
     ids = np.asarray(tokens, dtype=np.int64).ravel()
