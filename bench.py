@@ -214,7 +214,7 @@ def kernel_roofline(geo, fw, qw, hcache, fcache, peak):
     kv = geo.nk
     nq_tok = hcache.quantized_token_count
     nfp = hcache.fp1_len + hcache.fp2_len + 1
-    run = Runner(geo, hcache, max_cols=16)
+    run = Runner(geo, hcache, max_cols=5)
     run.q.normal_()
     s = _lib.stream_ptr()
     per_tok = {"draft": kv * 1.0 + 8.0 * kv / G + 8.0 * math.ceil(kv / G),
@@ -223,7 +223,7 @@ def kernel_roofline(geo, fw, qw, hcache, fcache, peak):
         dt = time_kernel(lambda: run._attention(0, view, T, 0, s))
         algo = nq_tok * per_tok["draft" if view == _lib.VIEW_DRAFT else "target"] + (nfp + T) * kv * 4.0 + T * geo.nq * 8.0
         out[name] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak}
-    frun = Runner(geo, fcache, max_cols=16)
+    frun = Runner(geo, fcache, max_cols=1)
     frun.q.normal_()
     n = fcache.seq_len + 1
     dt = time_kernel(lambda: frun._attention(0, _lib.VIEW_FP16, 1, 0, s))

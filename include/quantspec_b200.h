@@ -156,6 +156,9 @@ qs_status qs_kv_dequant_view(const qs_kv_store* st, int seq, int layer, int nblk
 /* ---- L2 forward pieces (Q/model.py) ---- */
 qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream);
 int qs_attn_partials_floats(const qs_attn_args* a);
+/* resident CTAs per SM of the attention kernel for (head_dim, query columns per CTA, mode);
+ * the host sizes the split-K grid with it (fixed per view so results stay batch-invariant) */
+int qs_attn_occupancy(int hd, int n_query_cols, int mode);
 qs_status qs_linear(const qs_linear_args* a, void* stream);
 /* rmsnorm Q/tensor.py:35-42 over rows [n][d] */
 qs_status qs_rmsnorm(const float* x, const float* gain, float* out, int n, int d, float eps, void* stream);

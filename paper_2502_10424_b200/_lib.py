@@ -76,6 +76,7 @@ _SIGS = {
     "qs_kv_dequant_view": (i32, [C.POINTER(KVStore), i32, i32, i32, i32, vp, vp, vp]),
     "qs_attn_decode": (i32, [C.POINTER(AttnArgs), i32, vp]),
     "qs_attn_partials_floats": (i32, [C.POINTER(AttnArgs)]),
+    "qs_attn_occupancy": (i32, [i32, i32, i32]),
     "qs_linear": (i32, [C.POINTER(LinearArgs), vp]),
     "qs_rmsnorm": (i32, [vp, vp, vp, i32, i32, f32, vp]),
     "qs_embed": (i32, [vp, vp, vp, i32, i32, i32, vp, vp]),

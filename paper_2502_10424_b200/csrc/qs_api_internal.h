@@ -9,6 +9,7 @@ using LinearParams = qs_linear_args;
 
 cudaError_t launch_attention(const AttnParams& p, int mode, cudaStream_t s);
 int attention_smem_bytes(int hd, int nt, int mode);
+int attention_occupancy(int hd, int nt, int mode);
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s);
 
 // error reporting shared by all translation units

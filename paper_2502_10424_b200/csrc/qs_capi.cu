@@ -178,6 +178,12 @@ int qs_attn_partials_floats(const qs_attn_args* a) {
   return a->B * a->Hkv * a->n_qgroups * (a->n_main + 2) * nt * 4 * (a->hd + 2);
 }
 
+int qs_attn_occupancy(int hd, int n_query_cols, int mode) {
+  int nt = (n_query_cols + 3) / 4;
+  if (nt < 1) nt = 1;
+  return qs::attention_occupancy(hd, nt, mode);
+}
+
 qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream) {
   if (!a) QS_FAIL(QS_ERR_CONFIG, "null args");
   if (a->hd != 16 && a->hd != 32 && a->hd != 64 && a->hd != 128) QS_FAIL(QS_ERR_CONFIG, "head_dim %d unsupported", a->hd);

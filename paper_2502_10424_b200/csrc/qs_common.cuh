@@ -89,6 +89,28 @@ __device__ __forceinline__ void unpack_u4l4(uint32_t x, uint32_t y, uint32_t (&a
   a[3] = h2_as_u32(__hsub2(u32_as_h2(prmt(od, M, 0x4341u)), k1032));  // pos3, pos7
 }
 
+// Offset forms for the attention kernels: no per-element subtraction; the
+// constant offsets are folded into per-block score biases / per-column sums.
+//   unpack_u4_raw:   a0,a2 = 1024 + c (rows g),  a1,a3 = 1024 + 16 c (rows g+8)
+//   unpack_u4l4_raw: all = 1032 + (16 c_u + c_l)
+__device__ __forceinline__ void unpack_u4_raw(uint32_t x, uint32_t (&a)[4]) {
+  const uint32_t MAGIC = 0x64006400u;
+  uint32_t t = x >> 8;
+  a[0] = lop3_and_or(x, 0x000F000Fu, MAGIC);
+  a[1] = lop3_and_or(x, 0x00F000F0u, MAGIC);
+  a[2] = lop3_and_or(t, 0x000F000Fu, MAGIC);
+  a[3] = lop3_and_or(t, 0x00F000F0u, MAGIC);
+}
+__device__ __forceinline__ void unpack_u4l4_raw(uint32_t x, uint32_t y, uint32_t (&a)[4]) {
+  uint32_t ev = lop3_select(x << 4, y, 0xF0F0F0F0u);
+  uint32_t od = lop3_select(x, y >> 4, 0xF0F0F0F0u);
+  const uint32_t M = 0x64646464u;
+  a[0] = prmt(ev, M, 0x4240u);
+  a[1] = prmt(od, M, 0x4240u);
+  a[2] = prmt(ev, M, 0x4341u);
+  a[3] = prmt(od, M, 0x4341u);
+}
+
 // split an f32 into f16 hi + f16 lo (hi + lo reproduces ~22 bits)
 __device__ __forceinline__ void split_hl(float v, __half& hi, __half& lo) {
   hi = __float2half_rn(v);
@@ -145,6 +167,9 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 // TMA-engine 1-D bulk copy global -> shared, completion counted on an mbarrier.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

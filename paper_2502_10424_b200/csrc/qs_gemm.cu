@@ -32,7 +32,7 @@ struct LinCfg {
 
 __device__ __forceinline__ float silu_f32(float x) { return __fdiv_rn(x, __fadd_rn(1.0f, expf(-x))); }
 
-template <int WMODE, int NTC, int EPI>
+template <int WMODE, int NTC, int EPI, int GKS>
 __global__ void __launch_bounds__(kGemmThreads) linear_kernel(const __grid_constant__ LinearParams P) {
   constexpr int COLS = 8 * NTC;
   extern __shared__ __align__(16) uint8_t sm[];
@@ -45,13 +45,38 @@ __global__ void __launch_bounds__(kGemmThreads) linear_kernel(const __grid_const
   const int nks = ks1 - ks0;
   const int MT = P.N / 16;
   const int ncols = P.ncols;
-  const int gks = (WMODE == QS_W_INT4) ? (P.wgroup / 16) : 1;  // k-steps per weight group
-  const int ngr = (WMODE == QS_W_INT4) ? (nks + gks - 1) / gks : 0;
+  // INT4: k-steps per weight group is the compile-time GKS (the host checks P.wgroup == 16*GKS)
+  const int ngr = (WMODE == QS_W_INT4) ? (nks + GKS - 1) / GKS : 0;
+  const int ngr_max = (WMODE == QS_W_INT4) ? (P.krange + GKS - 1) / GKS : 0;
 
-  uint2* bs = reinterpret_cast<uint2*>(sm);                       // [nks][NTC][32]
-  float* xsum = reinterpret_cast<float*>(bs + (size_t)P.krange * NTC * 32);  // [ngr][COLS]
-  float* ys = xsum + (WMODE == QS_W_INT4 ? (size_t)((P.krange + gks - 1) / gks) * COLS : 0);  // [64][COLS]
+  uint2* bs = reinterpret_cast<uint2*>(sm);                                   // [krange][NTC][32]
+  float4* psm = reinterpret_cast<float4*>(bs + (size_t)P.krange * NTC * 32);   // [4 mtiles][ngr_max][8]
+  float* xsum = reinterpret_cast<float*>(psm + (WMODE == QS_W_INT4 ? (size_t)4 * ngr_max * 8 : 0));  // [ngr][COLS]
+  float* ys = xsum + (WMODE == QS_W_INT4 ? (size_t)ngr_max * COLS : 0);       // [64][COLS]
   int* ticket = reinterpret_cast<int*>(ys + 64 * COLS);
+
+  const int mt = mg * 4 + warp;
+  // ---- issue this warp's first weight loads before staging (overlaps the prologue) ----
+  constexpr int U = 8;  // uint4 per lane per buffer: 8 k-steps (f16) or 32 k-steps (INT4)
+  const uint4* wp;
+  int nq4;  // uint4 steps of this warp
+  if constexpr (WMODE == QS_W_F16) {
+    wp = reinterpret_cast<const uint4*>(P.w) + ((size_t)mt * KS + ks0) * 32 + lane;
+    nq4 = nks;
+  } else {
+    const int ks_pad = (KS + 3) / 4 * 4;  // frag4 words [mt][KSpad/4][32][4]; ks0 % 4 == 0
+    wp = reinterpret_cast<const uint4*>(P.w) + ((size_t)mt * (ks_pad / 4) + ks0 / 4) * 32 + lane;
+    nq4 = (nks + 3) / 4;
+  }
+  const bool active = mt < MT;
+  uint4 buf0[U], buf1[U];
+  auto ld = [&](uint4 (&b)[U], int base) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      b[u] = (active && base + u < nq4) ? ldg_nc_v4(wp + (size_t)(base + u) * 32) : make_uint4(0, 0, 0, 0);
+  };
+  ld(buf0, 0);
+  if (nq4 > U) ld(buf1, U);
 
   // ---- stage the activation slice as f16 B fragments ----
   for (int i = tid; i < nks * NTC * 32; i += kGemmThreads) {
@@ -72,31 +97,32 @@ __global__ void __launch_bounds__(kGemmThreads) linear_kernel(const __grid_const
       int col = i % COLS, gr = i / COLS;
       float a = 0.f;
       if (col < ncols) {
-        int k0 = (ks0 + gr * gks) * 16, k1 = min(ks1, ks0 + (gr + 1) * gks) * 16;
+        int k0 = (ks0 + gr * GKS) * 16, k1 = min(ks1, ks0 + (gr + 1) * GKS) * 16;
         const float* xr = P.x + (size_t)col * P.K;
         for (int k = k0; k < k1; ++k) a += __half2float(__float2half_rn(xr[k]));
       }
       xsum[i] = a;
     }
+    // (S, Z) of rows g and g+8 of the CTA's 4 m-tiles for the groups of this k-range
+    const int gpr = (P.K + P.wgroup - 1) / P.wgroup;
+    const int gr0 = ks0 / GKS;
+    const float4* pp = reinterpret_cast<const float4*>(P.wparams);
+    for (int i = tid; i < 4 * ngr * 8; i += kGemmThreads) {
+      int gg = i & 7, gr = (i >> 3) % ngr, w = i / (8 * ngr);
+      int m = mg * 4 + w;
+      psm[(w * ngr_max + gr) * 8 + gg] = m < MT ? __ldg(pp + ((size_t)m * gpr + gr0 + gr) * 8 + gg) : make_float4(0, 0, 0, 0);
+    }
   }
   __syncthreads();
 
-  const int mt = mg * 4 + warp;
   float acc[NTC][4];
 #pragma unroll
   for (int nt = 0; nt < NTC; ++nt)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
 
-  if (mt < MT) {
+  if (active) {
     if constexpr (WMODE == QS_W_F16) {
-      const uint4* wp = reinterpret_cast<const uint4*>(P.w) + ((size_t)mt * KS + ks0) * 32 + lane;
-      constexpr int U = 8;
-      uint4 buf0[U], buf1[U];
-      auto ld = [&](uint4 (&b)[U], int base) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) b[u] = (base + u < nks) ? ldg_nc_v4(wp + (size_t)(base + u) * 32) : make_uint4(0, 0, 0, 0);
-      };
       auto mm = [&](uint4 (&b)[U], int base) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -110,38 +136,42 @@ __global__ void __launch_bounds__(kGemmThreads) linear_kernel(const __grid_const
           }
         }
       };
-      ld(buf0, 0);
       for (int base = 0; base < nks; base += 2 * U) {
-        if (base + U < nks) ld(buf1, base + U);
         mm(buf0, base);
         if (base + 2 * U < nks) ld(buf0, base + 2 * U);
-        if (base + U < nks) mm(buf1, base + U);
+        if (base + U < nks) {
+          mm(buf1, base + U);
+          if (base + 3 * U < nks) ld(buf1, base + 3 * U);
+        }
       }
     } else {
-      // frag4 words [mt][KSpad/4][32][4]; ks0 is a multiple of 4 (host guarantees)
-      const int ks_pad = (KS + 3) / 4 * 4;
-      const uint4* wp = reinterpret_cast<const uint4*>(P.w) + ((size_t)mt * (ks_pad / 4) + ks0 / 4) * 32 + lane;
-      const float4* pp = reinterpret_cast<const float4*>(P.wparams);
-      const int gpr = (P.K + P.wgroup - 1) / P.wgroup;
-      constexpr int U = 4;  // uint4 = 4 k-steps
-      const int nq = (nks + 3) / 4;
+      const float4* pw4 = psm + (size_t)warp * ngr_max * 8 + g;
       float tmp[NTC][4];
 #pragma unroll
       for (int nt = 0; nt < NTC; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) tmp[nt][e] = 0.f;
-      uint4 buf0[U], buf1[U];
-      auto ld = [&](uint4 (&b)[U], int base) {
+      auto flush_group = [&](int gl) {
+        const float4 sp = pw4[gl * 8];
 #pragma unroll
-        for (int u = 0; u < U; ++u) b[u] = (base + u < nq) ? ldg_nc_v4(wp + (size_t)(base + u) * 32) : make_uint4(0, 0, 0, 0);
+        for (int nt = 0; nt < NTC; ++nt) {
+          const int c0 = nt * 8 + 2 * t4;
+          const float x0 = xsum[gl * COLS + c0], x1 = xsum[gl * COLS + c0 + 1];
+          acc[nt][0] += sp.x * tmp[nt][0] + sp.y * x0;
+          acc[nt][1] += sp.x * tmp[nt][1] + sp.y * x1;
+          acc[nt][2] += sp.z * tmp[nt][2] + sp.w * x0;
+          acc[nt][3] += sp.z * tmp[nt][3] + sp.w * x1;
+          tmp[nt][0] = tmp[nt][1] = tmp[nt][2] = tmp[nt][3] = 0.f;
+        }
       };
+      // base counts uint4 steps (4 k-steps each); 4*U k-steps per buffer is a multiple of GKS
       auto mm = [&](uint4 (&b)[U], int base) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          uint32_t wv[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+          const uint32_t wv[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
-            int kk = (base + u) * 4 + v;  // local k-step
+            const int kk = (base + u) * 4 + v;  // local k-step
             if (kk < nks) {
               uint32_t a[4];
               unpack_u4(wv[v], a);
@@ -150,32 +180,18 @@ __global__ void __launch_bounds__(kGemmThreads) linear_kernel(const __grid_const
                 uint2 bb = bs[((size_t)kk * NTC + nt) * 32 + lane];
                 mma16816(tmp[nt], a, bb.x, bb.y);
               }
-              bool gend = ((kk + 1) % gks == 0) || (kk + 1 == nks);
-              if (gend) {
-                int gl = kk / gks;                       // local group
-                int gi = (ks0 + kk) * 16 / P.wgroup;      // global group
-                float4 sp = __ldg(pp + ((size_t)mt * gpr + gi) * 8 + g);
-#pragma unroll
-                for (int nt = 0; nt < NTC; ++nt) {
-                  int c0 = nt * 8 + 2 * t4;
-                  float x0 = xsum[gl * COLS + c0], x1 = xsum[gl * COLS + c0 + 1];
-                  acc[nt][0] += sp.x * tmp[nt][0] + sp.y * x0;
-                  acc[nt][1] += sp.x * tmp[nt][1] + sp.y * x1;
-                  acc[nt][2] += sp.z * tmp[nt][2] + sp.w * x0;
-                  acc[nt][3] += sp.z * tmp[nt][3] + sp.w * x1;
-                  tmp[nt][0] = tmp[nt][1] = tmp[nt][2] = tmp[nt][3] = 0.f;
-                }
-              }
+              if (((u * 4 + v + 1) % GKS) == 0 || kk + 1 == nks) flush_group(kk / GKS);
             }
           }
         }
       };
-      ld(buf0, 0);
-      for (int base = 0; base < nq; base += 2 * U) {
-        if (base + U < nq) ld(buf1, base + U);
+      for (int base = 0; base < nq4; base += 2 * U) {
         mm(buf0, base);
-        if (base + 2 * U < nq) ld(buf0, base + 2 * U);
-        if (base + U < nq) mm(buf1, base + U);
+        if (base + 2 * U < nq4) ld(buf0, base + 2 * U);
+        if (base + U < nq4) {
+          mm(buf1, base + U);
+          if (base + 3 * U < nq4) ld(buf1, base + 3 * U);
+        }
       }
     }
   }
@@ -183,16 +199,20 @@ __global__ void __launch_bounds__(kGemmThreads) linear_kernel(const __grid_const
   // ---- collect the 64 x COLS tile (split-K reduced in fixed order) ----
   const int row0 = mg * 64;
   if (P.ksplit > 1) {
-    float* wk = P.work + (size_t)ksp * COLS * P.N;  // [ksplit][COLS][N]
+    float* wk = P.work + (size_t)ksp * ncols * P.N;  // [ksplit][ncols][N]
     if (mt < MT) {
 #pragma unroll
       for (int nt = 0; nt < NTC; ++nt) {
         int c0 = nt * 8 + 2 * t4;
         int r = mt * 16 + g;
-        wk[(size_t)c0 * P.N + r] = acc[nt][0];
-        wk[(size_t)(c0 + 1) * P.N + r] = acc[nt][1];
-        wk[(size_t)c0 * P.N + r + 8] = acc[nt][2];
-        wk[(size_t)(c0 + 1) * P.N + r + 8] = acc[nt][3];
+        if (c0 < ncols) {
+          wk[(size_t)c0 * P.N + r] = acc[nt][0];
+          wk[(size_t)c0 * P.N + r + 8] = acc[nt][2];
+        }
+        if (c0 + 1 < ncols) {
+          wk[(size_t)(c0 + 1) * P.N + r] = acc[nt][1];
+          wk[(size_t)(c0 + 1) * P.N + r + 8] = acc[nt][3];
+        }
       }
     }
     __threadfence();
@@ -201,11 +221,11 @@ __global__ void __launch_bounds__(kGemmThreads) linear_kernel(const __grid_const
     __syncthreads();
     if (*ticket != P.ksplit - 1) return;
     __threadfence();
-    for (int i = tid; i < 64 * COLS; i += kGemmThreads) {
+    for (int i = tid; i < 64 * ncols; i += kGemmThreads) {
       int r = i % 64, c = i / 64;
       float a = 0.f;
       if (row0 + r < P.N)
-        for (int s = 0; s < P.ksplit; ++s) a += __ldcg(P.work + ((size_t)s * COLS + c) * P.N + row0 + r);
+        for (int s = 0; s < P.ksplit; ++s) a += __ldcg(P.work + ((size_t)s * ncols + c) * P.N + row0 + r);
       ys[r * COLS + c] = a;
     }
     if (tid == 0) P.counters[mg] = 0;
@@ -282,13 +302,12 @@ __global__ void __launch_bounds__(kGemmThreads) linear_kernel(const __grid_const
   }
 }
 
-template <int WMODE, int NTC, int EPI>
+template <int WMODE, int NTC, int EPI, int GKS>
 static cudaError_t launch_lin_t(const LinearParams& p, cudaStream_t s) {
   constexpr int COLS = 8 * NTC;
-  int gks = (WMODE == QS_W_INT4) ? p.wgroup / 16 : 1;
-  size_t smem = (size_t)p.krange * NTC * 32 * 8 + (WMODE == QS_W_INT4 ? (size_t)((p.krange + gks - 1) / gks) * COLS * 4 : 0) +
-                64 * COLS * 4 + 16;
-  auto kern = linear_kernel<WMODE, NTC, EPI>;
+  size_t ngr = (WMODE == QS_W_INT4) ? (size_t)((p.krange + GKS - 1) / GKS) : 0;
+  size_t smem = (size_t)p.krange * NTC * 32 * 8 + ngr * 4 * 8 * 16 + ngr * COLS * 4 + 64 * COLS * 4 + 16;
+  auto kern = linear_kernel<WMODE, NTC, EPI, GKS>;
   static size_t configured = 48 * 1024;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -300,30 +319,38 @@ static cudaError_t launch_lin_t(const LinearParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int WMODE, int NTC>
+template <int WMODE, int NTC, int GKS>
 static cudaError_t launch_lin_e(const LinearParams& p, cudaStream_t s) {
   switch (p.epi) {
-    case QS_EPI_STORE: return launch_lin_t<WMODE, NTC, QS_EPI_STORE>(p, s);
-    case QS_EPI_ADD: return launch_lin_t<WMODE, NTC, QS_EPI_ADD>(p, s);
-    case QS_EPI_QKV: return launch_lin_t<WMODE, NTC, QS_EPI_QKV>(p, s);
-    case QS_EPI_SILU_MUL: return launch_lin_t<WMODE, NTC, QS_EPI_SILU_MUL>(p, s);
+    case QS_EPI_STORE: return launch_lin_t<WMODE, NTC, QS_EPI_STORE, GKS>(p, s);
+    case QS_EPI_ADD: return launch_lin_t<WMODE, NTC, QS_EPI_ADD, GKS>(p, s);
+    case QS_EPI_QKV: return launch_lin_t<WMODE, NTC, QS_EPI_QKV, GKS>(p, s);
+    case QS_EPI_SILU_MUL: return launch_lin_t<WMODE, NTC, QS_EPI_SILU_MUL, GKS>(p, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
-template <int WMODE>
+template <int WMODE, int GKS>
 static cudaError_t launch_lin_n(const LinearParams& p, cudaStream_t s) {
   int ntc = (p.ncols + 7) / 8;
-  if (ntc <= 1) return launch_lin_e<WMODE, 1>(p, s);
-  if (ntc <= 2) return launch_lin_e<WMODE, 2>(p, s);
-  if (ntc <= 4) return launch_lin_e<WMODE, 4>(p, s);
-  if (ntc <= 8) return launch_lin_e<WMODE, 8>(p, s);
+  if (ntc <= 1) return launch_lin_e<WMODE, 1, GKS>(p, s);
+  if (ntc <= 2) return launch_lin_e<WMODE, 2, GKS>(p, s);
+  if (ntc <= 4) return launch_lin_e<WMODE, 4, GKS>(p, s);
+  if (ntc <= 8) return launch_lin_e<WMODE, 8, GKS>(p, s);
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {
-  if (p.wmode == QS_W_F16) return launch_lin_n<QS_W_F16>(p, s);
-  if (p.wmode == QS_W_INT4) return launch_lin_n<QS_W_INT4>(p, s);
+  if (p.wmode == QS_W_F16) return launch_lin_n<QS_W_F16, 1>(p, s);
+  if (p.wmode == QS_W_INT4) {
+    switch (p.wgroup) {
+      case 16: return launch_lin_n<QS_W_INT4, 1>(p, s);
+      case 32: return launch_lin_n<QS_W_INT4, 2>(p, s);
+      case 64: return launch_lin_n<QS_W_INT4, 4>(p, s);
+      case 128: return launch_lin_n<QS_W_INT4, 8>(p, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   return cudaErrorInvalidValue;
 }
 

@@ -66,7 +66,7 @@ class SpecEngine:
         self.draft = draft
         self.cache = cache
         self.gamma = gamma
-        self.run = runner or Runner(target.geo, cache, max_cols=max(16, gamma + 1))
+        self.run = runner or Runner(target.geo, cache, max_cols=cache.batch * (gamma + 1))
         self.graphs = _GraphCache(use_graphs)
         self.host = torch.zeros(4 + gamma + 2, dtype=torch.int32).pin_memory()
         self.launches = 0
@@ -131,7 +131,7 @@ class ARAutoEngine:
         torch = _torch()
         self.target = target
         self.cache = cache
-        self.run = runner or Runner(target.geo, cache, max_cols=16)
+        self.run = runner or Runner(target.geo, cache, max_cols=cache.batch)
         self.graphs = _GraphCache(use_graphs)
         self.is_fp = not hasattr(cache, "d_n_blocks")
         self.host = torch.zeros(8, dtype=torch.int32).pin_memory()

@@ -202,7 +202,7 @@ def plan_linear(pl: PackedLinear, ncols: int) -> tuple[int, int]:
     ntc = 1 if ntc <= 1 else 2 if ntc <= 2 else 4 if ntc <= 4 else 8
     align = 4 * max(1, pl.group // 16) if pl.wmode == _lib.W_INT4 else 1
     max_kr = max(align, (256 // ntc) // align * align)
-    want = max(1, -(-2 * SM_COUNT // mgroups))
+    want = max(1, -(-4 * SM_COUNT // mgroups))
     kr = -(-KS // want)
     kr = max(kr, 16)
     kr = min(kr, max_kr)
@@ -211,9 +211,10 @@ def plan_linear(pl: PackedLinear, ncols: int) -> tuple[int, int]:
     return ks, kr
 
 
-def plan_attention_splits(n_heads_total: int, max_chunks: int) -> int:
-    """Main-region splits per head: ~2 CTAs per SM, never more than the chunks."""
-    target = max(1, (2 * SM_COUNT) // max(1, n_heads_total))
+def plan_attention_splits(n_heads_total: int, max_chunks: int, ctas_per_sm: int = 2) -> int:
+    """Main-region splits per head so every main CTA is resident in one wave
+    (the two short tail CTAs per head are scheduled after them)."""
+    target = max(1, (ctas_per_sm * SM_COUNT) // max(1, n_heads_total))
     return max(1, min(target, max_chunks))
 
 
@@ -246,25 +247,45 @@ class Runner:
         self.is_fp = not hasattr(cache, "d_n_blocks")
         r = geo.num_heads // geo.num_kv_heads
         self.r = r
-        # attention scratch sized for the widest launch (T*r query columns)
+        # attention: split-K grid per view, fixed for every T so row results are
+        # batch-invariant (a T-row verify == T single-row steps, bit for bit)
         if self.is_fp:
-            max_chunks = -(-cache.capacity // 64)
+            self.max_chunks = -(-cache.capacity // 64)
         else:
-            max_chunks = -(-cache.max_blocks * cache.layout.group_size // 128)
-        self.attn_splits = attn_splits or plan_attention_splits(self.B * geo.num_kv_heads, max_chunks)
-        self.fp_cps = -(-max_chunks // self.attn_splits) if self.is_fp else 0
-        ncols_q = (max_cols // self.B) * r
+            self.max_chunks = -(-cache.max_blocks * cache.layout.group_size // 128)
+        self.max_T = max(1, max_cols // self.B)
+        self._attn_splits_override = attn_splits
+        self._splits: dict = {}
+        ncols_q = self.max_T * r
         self.n_qgroups_max = max(1, -(-ncols_q // 12))
         per = -(-ncols_q // self.n_qgroups_max)
         nt = max(1, -(-per // 4))
-        nparts = self.B * geo.num_kv_heads * self.n_qgroups_max * (self.attn_splits + 2) * nt * 4 * (geo.head_dim + 2)
+        max_splits = attn_splits or max(1, min(self.max_chunks, 4 * SM_COUNT))
+        nparts = self.B * geo.num_kv_heads * self.n_qgroups_max * (max_splits + 2) * nt * 4 * (geo.head_dim + 2)
         self.partials = torch.zeros(nparts, dtype=torch.float32, device=dev)
         self.attn_counters = torch.zeros(self.B * geo.num_kv_heads * self.n_qgroups_max, dtype=torch.int32, device=dev)
+        self.fp_cps = 0
+        if self.is_fp:
+            self.fp_cps = -(-self.max_chunks // self.splits_for(_lib.VIEW_FP16))
         # linear scratch: ksplit * 64 cols * max N
         nmax = max(geo.nq + 2 * geo.nk, 2 * geo.mlp_hidden, geo.vocab, geo.hidden)
         self.work = torch.zeros(64 * 64 * nmax // 8, dtype=torch.float32, device=dev)
         self.lin_counters = torch.zeros(-(-nmax // 64), dtype=torch.int32, device=dev)
         self._lin_cache: dict = {}
+
+    def splits_for(self, view: int) -> int:
+        """Main-region splits of the attention grid for one view (cached)."""
+        n = self._splits.get(view)
+        if n is None:
+            if self._attn_splits_override:
+                n = self._attn_splits_override
+            else:
+                cols = self.r if view == _lib.VIEW_DRAFT else min(12, self.max_T * self.r)
+                occ = _lib.load().qs_attn_occupancy(self.geo.head_dim, cols, view)
+                occ = occ if occ > 0 else 1
+                n = plan_attention_splits(self.B * self.geo.num_kv_heads * self.n_qgroups_max, self.max_chunks, occ)
+            self._splits[view] = n
+        return n
 
     # -- linear ---------------------------------------------------------------
     def _linear(self, pl: PackedLinear, x, y, ncols: int, epi: int, *, ldy: int | None = None, layer: int = 0,
@@ -278,7 +299,7 @@ class Runner:
             a.ksplit, a.krange = plan_linear(pl, ncols)
             ntc = -(-ncols // 8)
             cols = 8 * (1 if ntc <= 1 else 2 if ntc <= 2 else 4 if ntc <= 4 else 8)
-            if a.ksplit * cols * pl.N > self.work.numel():
+            if a.ksplit * ncols * pl.N > self.work.numel():
                 raise ConfigError("linear split-K scratch too small")
             a.wgroup = pl.group
             a.w = pl.w.data_ptr()
@@ -325,7 +346,7 @@ class Runner:
             a.B, a.Hkv, a.hd, a.T, a.r = self.B, geo.num_kv_heads, geo.head_dim, T, self.r
             a.n_queries = T * self.r
             a.n_qgroups = max(1, -(-a.n_queries // 12))
-            a.n_main = self.attn_splits
+            a.n_main = self.splits_for(view if not self.is_fp else _lib.VIEW_FP16)
             a.row_offset = row_offset
             a.sm_scale_log2 = float(1.4426950408889634 / math.sqrt(geo.head_dim))
             a.q, a.out, a.q_row_stride = self.q.data_ptr(), self.attn.data_ptr(), geo.nq

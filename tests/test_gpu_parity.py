@@ -234,7 +234,7 @@ def _attn_setup(H, hd, G, n_prompt, extra, seed=0, r=1):
 def _run_attention(cache, q, view, T, row_offset=0, r=1):
     lay = cache.layout
     geo = Geometry(1, lay.num_heads * lay.head_dim, lay.num_heads, lay.kv_heads, lay.head_dim, 16, 16, 1 << 20)
-    run = Runner(geo, cache, max_cols=max(T, 1))
+    run = Runner(geo, cache, max_cols=16)
     run.q[:T] = torch.from_numpy(q.reshape(T, -1)).cuda()
     run._attention(0, view, T, row_offset, _lib.stream_ptr())
     torch.cuda.synchronize()
