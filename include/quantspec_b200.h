@@ -77,6 +77,7 @@ typedef struct {
   int64_t fp_seq_stride; /* halves */
   float* partials;       /* scratch */
   int* counters;         /* [B*Hkv*n_qgroups] zero-initialised */
+  int dbg;               /* 0; diagnostic bits (1: skip consumer math, 2: skip producer fold) */
 } qs_attn_args;
 
 /* x @ W with fused epilogue.  Replaces the fp32 `h @ W` products of

@@ -38,7 +38,7 @@ class AttnArgs(C.Structure):
         ("kp_seq_stride", i64), ("kp_head_stride", i64), ("vp_seq_stride", i64), ("vp_head_stride", i64),
         ("main_k", vp), ("main_v", vp), ("main_seq_stride", i64), ("main_head_stride", i64),
         ("fp1_k", vp), ("fp1_v", vp), ("fp2_k", vp), ("fp2_v", vp), ("fp_seq_stride", i64),
-        ("partials", vp), ("counters", vp),
+        ("partials", vp), ("counters", vp), ("dbg", i32),
     ]
 
 

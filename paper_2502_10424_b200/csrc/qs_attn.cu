@@ -45,7 +45,8 @@ template <int HD, int NT, int MODE>
 struct AttnCfg {
   static constexpr bool QUANT = MODE != MODE_FP16;
   static constexpr int NCW = QUANT ? 8 : 4;            // compute warps
-  static constexpr int NWARPS = NCW + (QUANT ? 1 : 0);  // + producer warp
+  static constexpr int NPW = QUANT ? 2 : 0;            // producer warps (TMA issue + query-scale fold)
+  static constexpr int NWARPS = NCW + NPW;
   static constexpr int THREADS = NWARPS * 32;
   static constexpr int KS = HD / 16;
   static constexpr int NQ = NT * 4;                      // queries (hi/lo column pairs) per CTA
@@ -59,7 +60,8 @@ struct AttnCfg {
   static constexpr int BIAS_OFF = BQ_OFF + BQ_WORDS * 4;
   static constexpr int BIAS_FLOATS = 8 * NQ * 2;          // [block][q][row g | row g+8]
   static constexpr int QSTAGE = (BIAS_OFF + BIAS_FLOATS * 4 + 127) / 128 * 128;
-  static constexpr int NSTAGE = 4;
+  // deep TMA ring: ~4 chunks in flight per CTA (the loaded HBM latency is a few microseconds)
+  static constexpr int NSTAGE = NT <= 2 ? 5 : 4;
   // resident CTAs per SM the register budget targets (wide verify launches keep 1 to avoid spills)
   static constexpr int MIN_BLOCKS = QUANT ? ((MODE == MODE_QDRAFT && NT == 1) ? 2 : 1) : 3;
   // ---- fp16 chunks: 64 tokens in the fp16 kernel, 32 in the quantised kernel's tails ----
@@ -74,7 +76,10 @@ struct AttnCfg {
   static constexpr int REGION = R0 > MERGE_BYTES ? R0 : MERGE_BYTES;
   static constexpr int BQF_WORDS = KS * NT * 64;          // raw-query fragments for fp16 chunks
   static constexpr int PW_HALVES = NT * 8 * PSTRIDE;
-  static constexpr int SMEM = REGION + BQF_WORDS * 4 + NQ * HD * 4 + NCW * PW_HALVES * 2 + 3 * 8 * 8 + 16;
+  static constexpr int VPAD = 2 * NQ <= 8 ? 8 : 2 * NQ <= 16 ? 16 : 32;      // reduce-scatter width
+  static constexpr int PSCR_FLOATS = 2 * 8 * VPAD * (NPW > 0 ? NPW : 1);    // producer partial sums
+  static constexpr int SMEM =
+      REGION + BQF_WORDS * 4 + NQ * HD * 4 + NCW * PW_HALVES * 2 + PSCR_FLOATS * 4 + 3 * 8 * 8 + 16;
 };
 
 __device__ __forceinline__ int swz16(int chunk, int row, int nchunk) {
@@ -284,7 +289,7 @@ __device__ __forceinline__ void fp16_region(uint8_t* region, uint32_t* bqf, cons
 // quantised region: producer warp + 8 consumer warps
 // ---------------------------------------------------------------------------
 template <typename C, int HD, int NT, int MODE>
-__device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, const float* q_s, __half* pw, int nq,
+__device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, const float* q_s, __half* pw, float* pscr, int nq,
                                              int seq, int head, int n_tok, int c_begin, int c_end,
                                              const AttnParams& P, Softmax (&st)[NT], float (&acc)[C::KS][NT][4]) {
   constexpr int KS = C::KS, NQ = C::NQ, S = C::NSTAGE;
@@ -303,8 +308,9 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   const int nchunk = c_end - c_begin;
   auto stage_ptr = [&](int s) { return region + s * C::QSTAGE; };
 
-  if (warp == C::NCW) {
-    // ======================= producer warp =======================
+  if (warp >= C::NCW) {
+    // ======================= producer warps (NPW) =======================
+    const int pwid = warp - C::NCW;
     const size_t ph = ((size_t)seq * P.plane_seq_stride) + (size_t)head * P.plane_head_stride;
     const uint8_t* ku = P.ku + ph;
     const uint8_t* vu = P.vu + ph;
@@ -328,72 +334,107 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       bulk_g2s(sp + C::KP_OFF, kp + (size_t)b0 * HD, kpb, &tma_b[s]);
       bulk_g2s(sp + C::VP_OFF, vp + (size_t)b0 * G, vpb, &tma_b[s]);
     };
-    // this lane's channel pairs of every query, held in registers for the CTA's lifetime
-    constexpr int CPL = (HD / 2 + 31) / 32;  // channel pairs per lane
-    constexpr bool QREG = NQ <= 8;           // wide launches re-read shared memory instead (registers)
+    // the channel pairs this lane folds: cp = pwid*32 + lane + 32*NPW*k; query values kept in registers
+    constexpr int NPW = C::NPW;
+    constexpr int CPL = (HD / 2 + 32 * NPW - 1) / (32 * NPW);
+    constexpr bool QREG = NQ <= 8;  // wide launches re-read shared memory instead (registers)
     float2 qr[QREG ? NQ : 1][CPL];
     if constexpr (QREG) {
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
-          const int cp = lane + 32 * k;
+          const int cp = pwid * 32 + lane + 32 * NPW * k;
           qr[q][k] = cp < HD / 2 ? *reinterpret_cast<const float2*>(q_s + q * HD + 2 * cp) : make_float2(0.f, 0.f);
         }
     }
-    if (lane == 0)
+    if (pwid == 0 && lane == 0)
       for (int i = 0; i < S && i < nchunk; ++i) issue(i);
+    // chunk j is prepared (B fragments + biases) while the consumers work on
+    // chunk j-1; then the stage of chunk j-1 is refilled with chunk j-1+S
     for (int j = 0; j < nchunk; ++j) {
       const int s = j % S;
       uint8_t* sp = stage_ptr(s);
-      mbar_wait(&tma_b[s], (j / S) & 1);
+      mbar_wait_sleep(&tma_b[s], (j / S) & 1);
       const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + j) * QS_CHUNK_Q);
       const int nbl = (ntok_chunk + G - 1) >> lgG;
       const float2* kps = reinterpret_cast<const float2*>(sp + C::KP_OFF);
       uint32_t* bqb = reinterpret_cast<uint32_t*>(sp + C::BQ_OFF);
       float* bias = reinterpret_cast<float*>(sp + C::BIAS_OFF);
+      float* scr = pscr + (j & 1) * (NPW * 8 * C::VPAD);  // per-warp partial sums (double-buffered)
       // q'_c = q_c * S_c as f16 hi/lo B fragments; per (block, query): bias = sum q Z - offset * sum(q').
       // All queries are processed together so the warp reductions overlap (ILP), not serialise.
-      for (int bl = 0; bl < nbl; ++bl) {
+      for (int bl = 0; bl < ((P.dbg & 2) ? 0 : nbl); ++bl) {
         float zs[NQ], bs[NQ];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) zs[q] = bs[q] = 0.f;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
-          const int cp = lane + 32 * k;
+          const int cp = pwid * 32 + lane + 32 * NPW * k;
           if (cp < HD / 2) {
             const float4 pz = *reinterpret_cast<const float4*>(kps + bl * HD + 2 * cp);  // (S0, Z0, S1, Z1)
             const float s0 = pz.x * kvs, s1 = pz.z * kvs;
-            uint32_t* tb = bqb + (size_t)(bl * KS + (cp >> 3)) * NT * 64;
+            const int jj = cp & 7;
+            uint32_t* tb = bqb + (size_t)(bl * KS + (cp >> 3)) * NT * 64 + (jj & 3) * 2 + (jj >> 2);
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
               if (q < nq) {
                 const float2 qv = QREG ? qr[QREG ? q : 0][k] : *reinterpret_cast<const float2*>(q_s + q * HD + 2 * cp);
-                __half h0, l0, h1, l1;
-                split_hl(qv.x * s0, h0, l0);
-                split_hl(qv.y * s1, h1, l1);
-                put_qfrag(tb, cp, q, h0, h1, l0, l1);
+                const float v0 = qv.x * s0, v1 = qv.y * s1;
+                const __half2 hi = __floats2half2_rn(v0, v1);
+                const float2 hf = __half22float2(hi);
+                const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+                const float2 lf = __half22float2(lo);
+                uint32_t* bb = tb + ((2 * q) >> 3) * 64 + ((2 * q) & 7) * 8;
+                bb[0] = h2_as_u32(hi);
+                bb[8] = h2_as_u32(lo);
                 zs[q] += qv.x * pz.y + qv.y * pz.w;
-                bs[q] += (__half2float(h0) + __half2float(l0)) + (__half2float(h1) + __half2float(l1));
+                bs[q] += (hf.x + hf.y) + (lf.x + lf.y);
               }
             }
           }
         }
+        // warp reduce-scatter of the 2*NQ partial sums (zs then bs): each level halves
+        // the values a lane holds, so 2*NQ-1 shuffles replace 5*2*NQ dependent ones
+        constexpr int V = C::VPAD;  // 2*NQ padded to a power of two
+        constexpr int LV = V == 8 ? 3 : V == 16 ? 4 : 5;
+        float vals[V];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+        for (int i = 0; i < V; ++i) vals[i] = 0.f;
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            zs[q] += __shfl_xor_sync(0xffffffffu, zs[q], o);
-            bs[q] += __shfl_xor_sync(0xffffffffu, bs[q], o);
+        for (int q = 0; q < NQ; ++q) {
+          vals[q] = zs[q];
+          vals[NQ + q] = bs[q];
+        }
+#pragma unroll
+        for (int l = 0, h = V / 2; l < LV; ++l, h >>= 1) {
+          const int o = 16 >> l;
+          const bool up = lane & o;
+#pragma unroll
+          for (int i = 0; i < h; ++i) {
+            const float send = up ? vals[i] : vals[i + h];
+            const float keep = up ? vals[i + h] : vals[i];
+            vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
           }
-        if (lane < nq) {
-          float z = zs[0], b = bs[0];
+        }
+        float tot = vals[0];
 #pragma unroll
-          for (int q = 1; q < NQ; ++q)
-            if (lane == q) {
-              z = zs[q];
-              b = bs[q];
-            }
+        for (int o = 16 >> LV; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        const int idx = (lane >> (5 - LV)) & (V - 1);  // which of the 2*NQ sums this lane holds
+        if ((lane & ((1 << (5 - LV)) - 1)) == 0) scr[(pwid * 8 + bl) * V + idx] = tot;
+        if constexpr (NPW > 1) {
+          // all producer warps: partial sums written (and fragments stored) before warp 0 combines
+          asm volatile("bar.sync 1, %0;" ::"n"(NPW * 32));
+        } else {
+          __syncwarp();
+        }
+        if (pwid == 0 && lane < nq) {
+          float z = 0.f, b = 0.f;
+#pragma unroll
+          for (int w = 0; w < NPW; ++w) {
+            z += scr[(w * 8 + bl) * V + lane];
+            b += scr[(w * 8 + bl) * V + NQ + lane];
+          }
           // draft rows g carry 1024 + c, rows g+8 carry (1024 + 16c) (scaled by 1/16 after the MMA);
           // target rows carry 1032 + (16 c_u + c_l)
           bias[(bl * NQ + lane) * 2 + 0] = z - (TGT ? 1032.f : 1024.f) * b;
@@ -401,10 +442,10 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_b[s]);
+      if (lane == 0) mbar_arrive(&full_b[s]);  // full barrier counts one arrival per producer warp
       // refill the stage consumed by chunk j-1
-      if (j >= 1 && j - 1 + S < nchunk) {
-        mbar_wait(&empty_b[(j - 1) % S], ((j - 1) / S) & 1);
+      if (pwid == 0 && j >= 1 && j - 1 + S < nchunk) {
+        mbar_wait_sleep(&empty_b[(j - 1) % S], ((j - 1) / S) & 1);
         if (lane == 0) issue(j - 1 + S);
       }
     }
@@ -417,9 +458,9 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   for (int i = 0; i < nchunk; ++i) {
     const int s = i % S;
     const uint8_t* sp = stage_ptr(s);
-    mbar_wait(&full_b[s], (i / S) & 1);
+    mbar_wait_sleep(&full_b[s], (i / S) & 1);
     const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
-    const bool live = mt * 16 < ntok_chunk;  // tiles are whole: G is a multiple of 16
+    const bool live = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
     if (live) {
       const int bl = (mt * 16) >> lgG;
       const uint32_t* bqb = reinterpret_cast<const uint32_t*>(sp + C::BQ_OFF);
@@ -466,8 +507,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         __half h0, l0, h1, l1;
         split_hl(p[0] * (sz0.x * kvs), h0, l0);
         split_hl(p[1] * (sz1.x * kvs), h1, l1);
-        if constexpr (!TGT)
-          st[nt].ps += (__half2float(h0) + __half2float(l0)) + (__half2float(h1) + __half2float(l1));
+        st[nt].ps += (__half2float(h0) + __half2float(l0)) + (__half2float(h1) + __half2float(l1));
         put_p(pw, nt, g, t4, h0, l0, h1, l1);
       }
       __syncwarp();
@@ -481,7 +521,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
 #pragma unroll
       for (int cm = 0; cm < KS; ++cm) {
         uint32_t a[4];
-        if constexpr (TGT) unpack_u4l4(vw[cm], vwl[cm], a);  // exact codes: long accumulation
+        if constexpr (TGT) unpack_u4l4_raw(vw[cm], vwl[cm], a);
         else unpack_u4_raw(vw[cm], a);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) mma16816(acc[cm][nt], a, bpv[nt][0], bpv[nt][1]);
@@ -504,7 +544,8 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
   uint32_t* bqf = reinterpret_cast<uint32_t*>(smem + C::REGION);      // [KS][NT][32][2]
   float* q_s = reinterpret_cast<float*>(bqf + C::BQF_WORDS);          // [NQ][HD]
   __half* pw_all = reinterpret_cast<__half*>(q_s + NQ * HD);           // [NCW][PW_HALVES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pw_all + NCW * C::PW_HALVES);  // tma[8] full[8] empty[8]
+  float* pscr = reinterpret_cast<float*>(pw_all + NCW * C::PW_HALVES);  // producer partial sums
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pscr + C::PSCR_FLOATS);  // tma[8] full[8] empty[8]
   int* ticket_s = reinterpret_cast<int*>(bars + 24);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -537,7 +578,7 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
   if (tid == 0) {
     for (int i = 0; i < 8; ++i) {
       mbar_init(&bars[i], 1);         // TMA transactions
-      mbar_init(&bars[8 + i], 1);     // producer -> consumers
+      mbar_init(&bars[8 + i], C::NPW > 0 ? C::NPW : 1);  // producers -> consumers
       mbar_init(&bars[16 + i], NCW);  // consumers -> producer
     }
     fence_mbar_init();
@@ -603,8 +644,8 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
   bool offset_pv = false;
   if (region_kind == 0) {
     if constexpr (C::QUANT) {
-      if (c_end > c_begin) quant_region<C, HD, NT, MODE>(region, bars, q_s, pw, nq, seq, head, n_tok, c_begin, c_end, P, st, acc);
-      offset_pv = MODE == MODE_QDRAFT;
+      if (c_end > c_begin) quant_region<C, HD, NT, MODE>(region, bars, q_s, pw, pscr, nq, seq, head, n_tok, c_begin, c_end, P, st, acc);
+      offset_pv = true;
     }
   } else if (c_end > c_begin) {
     fp16_region<C, HD, NT>(region, bqf, q_s, pw, nq, fk, fv, n_tok, c_begin, c_end, causal, qg, P, st, acc);
@@ -630,10 +671,12 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
         row[0] = st[nt].m;
         row[1] = l;
       }
-      // draft P.V offsets: rows g carried (1024 + c) p', rows g+8 carried (1024 + 16c) p'
-      const float off_g = offset_pv ? 1024.f * ps : 0.f;
-      const float off_g8 = offset_pv ? 64.f * ps : 0.f;
-      const float sc8 = offset_pv ? 0.0625f : 1.0f;
+      // P.V offsets of the quantised path: draft rows g carried (1024 + c) p' and rows g+8
+      // (1024 + 16c) p'; target rows carried (1032 + 16 c_u + c_l) p'
+      constexpr bool TGTM = MODE == MODE_QTARGET;
+      const float off_g = offset_pv ? (TGTM ? 1032.f : 1024.f) * ps : 0.f;
+      const float off_g8 = offset_pv ? (TGTM ? 1032.f : 64.f) * ps : 0.f;
+      const float sc8 = (offset_pv && !TGTM) ? 0.0625f : 1.0f;
 #pragma unroll
       for (int cm = 0; cm < KS; ++cm) {
         row[4 + cm * 16 + g] = ((acc[cm][nt][0] + acc[cm][nt][1]) - off_g) + z;

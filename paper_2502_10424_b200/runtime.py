@@ -214,8 +214,15 @@ def plan_linear(pl: PackedLinear, ncols: int) -> tuple[int, int]:
 def plan_attention_splits(n_heads_total: int, max_chunks: int, ctas_per_sm: int = 2) -> int:
     """Main-region splits per head so every main CTA is resident in one wave
     (the two short tail CTAs per head are scheduled after them)."""
-    target = max(1, (ctas_per_sm * SM_COUNT) // max(1, n_heads_total))
-    return max(1, min(target, max_chunks))
+    slots = ctas_per_sm * SM_COUNT
+    heads = max(1, n_heads_total)
+    best, best_eff = 1, -1.0
+    for waves in (1, 2):  # each extra wave pays one more pipeline fill
+        n = max(1, (waves * slots) // heads)
+        eff = (n * heads) / (math.ceil(n * heads / slots) * slots)
+        if eff > best_eff + 0.05:
+            best, best_eff = n, eff
+    return max(1, min(best, max_chunks))
 
 
 # ---------------------------------------------------------------------------
