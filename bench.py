@@ -231,11 +231,12 @@ def kernel_roofline(geo, fw, qw, hcache, fcache, peak):
     out["attn_fp16"] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak}
     for name, w in (("gemv_f16_down", fw.layers[0]["down"]), ("gemv_int4_down", qw.layers[0]["down"]),
                     ("gemv_f16_lm_head", fw.lm_head)):
-        x = run.h if w.K == geo.mlp_hidden else run.xn
-        x.normal_()
+        src = (run.hh, run.hs) if w.K == geo.mlp_hidden else (run.xh, run.xs)
+        src[0].normal_()
+        src[1].normal_()
         y = run.x if w.N == geo.hidden else run.logits
-        dt = time_kernel(lambda: run._linear(w, x, y, 1, _lib.EPI_STORE, stream=s))
-        algo = w.algorithmic_bytes() + 4.0 * w.K
+        dt = time_kernel(lambda: run._linear(w, src, y, 1, _lib.EPI_STORE, stream=s))
+        algo = w.algorithmic_bytes() + 2.0 * w.K + 4.0 * w.N
         out[name] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak}
     torch.cuda.synchronize()
     return out

@@ -87,16 +87,23 @@ typedef struct {
   int wmode;          /* QS_W_F16 | QS_W_INT4                       */
   int epi;            /* QS_EPI_*                                    */
   int N, K;           /* output rows (d_out), reduction (d_in)       */
-  int ncols;          /* activation rows (B*T) <= 8*ncol_tiles       */
-  int ksplit;         /* k-ranges (grid.y)                           */
-  int krange;         /* k-steps (16) per range                      */
+  int ncols;          /* activation rows (B*T), 1..16                */
+  int nctas;          /* stream-K grid (fixed per layer: results do not depend on ncols) */
+  int maxc;           /* max contributing CTAs per 64-row tile (workspace slots) */
   int wgroup;         /* INT4 group size along d_in                  */
   const void* w;      /* frag16 halves or frag4 u32                  */
   const void* wparams;/* INT4: float4 {S_g,Z_g,S_g8,Z_g8} per (mtile,group,g) */
-  const float* x;     /* [ncols][K] activations                      */
-  float* y;           /* [ncols][ldy] output (STORE/ADD/SILU)        */
+  const void* xh;     /* half [ncols][ldxh]: f16 activations (qs_prep_act) */
+  int64_t ldxh;       /* halves, multiple of 8, >= K + 64             */
+  const float* xs;    /* [ncols][ldxs] sums of 16 consecutive f16 activations */
+  int64_t ldxs;       /* floats, multiple of 4, >= K/16 + 4           */
+  float* y;           /* [ncols][ldy] output (STORE/ADD) or SILU f32 copy (may be NULL) */
   int64_t ldy;
-  float* work;        /* split-K partial scratch                     */
+  void* yh;           /* SILU: half [ncols][ldyh] prepared input of the next layer */
+  int64_t ldyh;
+  float* ys;          /* SILU: [ncols][ldys] 16-sums of yh           */
+  int64_t ldys;
+  float* work;        /* [N/64][maxc][16][64] partial tiles           */
   int* counters;      /* [N/64] zero-initialised                     */
   /* QKV epilogue */
   int Nq, Nk, hd, T;  /* q rows, k rows (= v rows), head dim, rows per sequence */
@@ -136,7 +143,8 @@ qs_status qs_quantize_sym_s4(const double* values, int64_t count, float scale, i
 qs_status qs_decode_plane(const uint8_t* upper_codes, const uint8_t* lower_codes, const float* scales,
                           const float* zeros, int64_t count, int group, int64_t row_len, double* out,
                           void* stream);
-/* quantize_weights Q/quant.py:335-349: reference plane + frag4 device layout */
+/* quantize_weights Q/quant.py:335-349: reference plane + frag4 device layout.
+ * frag_params: per (16-row tile, group, g) float4 {S_g, Z_g - 1024 S_g, S_g8/16, Z_g8 - 64 S_g8} */
 qs_status qs_quantize_weights(const float* w, int d_in, int d_out, int group, uint8_t* ref_codes,
                               float* scales, float* zeros, uint32_t* frag4, void* frag_params, int* flags,
                               void* stream);
@@ -163,6 +171,14 @@ int qs_attn_occupancy(int hd, int n_query_cols, int mode);
 qs_status qs_linear(const qs_linear_args* a, void* stream);
 /* rmsnorm Q/tensor.py:35-42 over rows [n][d] */
 qs_status qs_rmsnorm(const float* x, const float* gain, float* out, int n, int d, float eps, void* stream);
+/* linear-layer input prep: xh = f16(rmsnorm(x) * gain) (or f16(x) when gain is NULL),
+ * xs = f32 sums of every 16 consecutive f16 values (INT4 zero-point term) */
+qs_status qs_prep_act(const float* x, const float* gain, float eps, void* xh, int64_t ldxh, float* xs,
+                      int64_t ldxs, int n, int d, void* stream);
+/* workspace slots (per 64-row tile) a stream-K grid of nctas CTAs needs for one linear layer */
+qs_status qs_linear_plan(int wmode, int N, int K, int nctas, int* maxc);
+/* resident linear-kernel CTAs per SM (the host fixes nctas = SMs * this, independent of ncols) */
+int qs_linear_occupancy(int wmode, int wgroup, int ncols);
 /* embedding lookup (Q/model.py:375) for n tokens */
 qs_status qs_embed(const float* table, const int* tokens, float* out, int n, int d, int vocab, int* flags,
                    void* stream);

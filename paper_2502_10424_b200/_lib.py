@@ -44,9 +44,11 @@ class AttnArgs(C.Structure):
 
 class LinearArgs(C.Structure):
     _fields_ = [
-        ("wmode", i32), ("epi", i32), ("N", i32), ("K", i32), ("ncols", i32), ("ksplit", i32),
-        ("krange", i32), ("wgroup", i32),
-        ("w", vp), ("wparams", vp), ("x", vp), ("y", vp), ("ldy", i64), ("work", vp), ("counters", vp),
+        ("wmode", i32), ("epi", i32), ("N", i32), ("K", i32), ("ncols", i32), ("nctas", i32),
+        ("maxc", i32), ("wgroup", i32),
+        ("w", vp), ("wparams", vp), ("xh", vp), ("ldxh", i64), ("xs", vp), ("ldxs", i64),
+        ("y", vp), ("ldy", i64), ("yh", vp), ("ldyh", i64), ("ys", vp), ("ldys", i64),
+        ("work", vp), ("counters", vp),
         ("Nq", i32), ("Nk", i32), ("hd", i32), ("T", i32),
         ("q_out", vp), ("k_dst", vp), ("v_dst", vp), ("kv_seq_stride", i64), ("kv_head_stride", i64),
         ("row_base", vp), ("row_offset", i32), ("pos_base", vp), ("rope", vp), ("max_pos", i32),
@@ -78,7 +80,10 @@ _SIGS = {
     "qs_attn_partials_floats": (i32, [C.POINTER(AttnArgs)]),
     "qs_attn_occupancy": (i32, [i32, i32, i32]),
     "qs_linear": (i32, [C.POINTER(LinearArgs), vp]),
+    "qs_linear_plan": (i32, [i32, i32, i32, i32, C.POINTER(i32)]),
+    "qs_linear_occupancy": (i32, [i32, i32, i32]),
     "qs_rmsnorm": (i32, [vp, vp, vp, i32, i32, f32, vp]),
+    "qs_prep_act": (i32, [vp, vp, f32, vp, i64, vp, i64, i32, i32, vp]),
     "qs_embed": (i32, [vp, vp, vp, i32, i32, i32, vp, vp]),
     "qs_argmax": (i32, [vp, i32, i32, vp, i32, vp]),
     "qs_greedy_accept": (i32, [vp, vp, i32, vp, vp, vp, vp, vp]),

@@ -200,15 +200,30 @@ qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream) {
 qs_status qs_linear(const qs_linear_args* a, void* stream) {
   if (!a) QS_FAIL(QS_ERR_CONFIG, "null args");
   if (a->K % 16 || a->N % 16) QS_FAIL(QS_ERR_DIMENSION, "linear dims must be multiples of 16 (N=%d K=%d)", a->N, a->K);
-  if (a->ncols < 1 || a->ncols > 64) QS_FAIL(QS_ERR_DIMENSION, "1..64 activation rows supported (got %d)", a->ncols);
+  if (a->ncols < 1 || a->ncols > 16) QS_FAIL(QS_ERR_DIMENSION, "1..16 activation rows supported (got %d)", a->ncols);
   if (a->epi == QS_EPI_SILU_MUL && a->N % 32) QS_FAIL(QS_ERR_DIMENSION, "gate/up interleave needs N multiple of 32");
-  if (a->wmode == QS_W_INT4) {
-    if (a->wgroup % 16) QS_FAIL(QS_ERR_CONFIG, "INT4 group %d must be a multiple of 16", a->wgroup);
-    if (a->krange % 4 || a->krange % (a->wgroup / 16))
-      QS_FAIL(QS_ERR_CONFIG, "k-range must align to 4 k-steps and to the weight group");
-  }
-  if ((long long)a->krange * a->ksplit * 16 < a->K) QS_FAIL(QS_ERR_CONFIG, "k-ranges do not cover K");
+  if (a->wmode == QS_W_INT4 && a->wgroup != 16 && a->wgroup != 32 && a->wgroup != 64 && a->wgroup != 128)
+    QS_FAIL(QS_ERR_CONFIG, "INT4 group %d unsupported on the device path (16/32/64/128)", a->wgroup);
+  if (a->nctas < 1) QS_FAIL(QS_ERR_CONFIG, "nctas must be >= 1");
+  if (a->maxc < qs::linear_maxc(a->wmode, a->N, a->K, a->nctas))
+    QS_FAIL(QS_ERR_CONFIG, "workspace slots (maxc=%d) too few for this grid", a->maxc);
+  if (a->ldxh % 8 || a->ldxh < a->K + 64 || (a->wmode == QS_W_INT4 && (a->ldxs % 4 || a->ldxs < a->K / 16 + 4)))
+    QS_FAIL(QS_ERR_CONFIG, "activation buffers need padded, 16-byte aligned rows");
   return cuda_status(launch_linear(*a, S(stream)), "linear");
+}
+
+qs_status qs_linear_plan(int wmode, int N, int K, int nctas, int* maxc) {
+  if (!maxc || nctas < 1 || N < 16 || K < 16) QS_FAIL(QS_ERR_CONFIG, "bad linear plan request");
+  *maxc = qs::linear_maxc(wmode, N, K, nctas);
+  return QS_OK;
+}
+
+int qs_linear_occupancy(int wmode, int wgroup, int ncols) { return qs::linear_occupancy(wmode, wgroup, ncols); }
+
+qs_status qs_prep_act(const float* x, const float* gain, float eps, void* xh, int64_t ldxh, float* xs, int64_t ldxs,
+                      int n, int d, void* stream) {
+  if (n < 1 || d < 16 || d % 16) QS_FAIL(QS_ERR_DIMENSION, "prep_act needs rows of a multiple of 16 (d=%d)", d);
+  return cuda_status(qs::launch_prep_act(x, gain, eps, xh, ldxh, xs, ldxs, n, d, S(stream)), "prep_act");
 }
 
 qs_status qs_rmsnorm(const float* x, const float* gain, float* out, int n, int d, float eps, void* stream) {

@@ -4,16 +4,21 @@
 // Replaces the fp32 `h @ W` products of decode_step
 //   /root/reference/pkg/src/quantspec/model.py:379-397, :405
 // and, in INT4 mode, the dequantised f32 weight copies of the draft path
-//   /root/reference/pkg/src/quantspec/model.py:141-168 (quantize_model_weights)
-// with a weight-streaming tensor-core kernel: W^T tiles are pre-permuted into
-// mma.sync A-fragment order (frag16: one 16-byte load per lane per 16x16 tile;
-// frag4: one u32 of packed codes per tile, dequantised in registers with the
-// per-(row, group) scale applied to the fp32 partial of each group), and the
-// activation rows ride as the N=8 columns (swap-AB).  Split-K across CTAs is
-// reduced in a fixed order by the last CTA of each 64-row tile, so every
-// column's result is independent of how many columns share the launch.
-// Fused epilogues: residual add, SiLU*up (Q/model.py:397), and q/k RoPE
-// (Q/tensor.py:65-82) + k/v append into the fp16 recent-token buffer
+//   /root/reference/pkg/src/quantspec/model.py:141-168 (quantize_model_weights).
+//
+// Weight-streaming stream-K kernel.  W^T is pre-permuted into mma.sync
+// A-fragment order (frag16: 16 B per lane per 16x16 tile; frag4: one u32 of
+// packed codes per tile), so a (64-row tile, k-chunk) work unit is four
+// contiguous byte ranges.  The grid is a fixed number of CTAs (one or two per
+// SM) that split the flattened list of units evenly: every SM streams the same
+// number of bytes.  A producer warp moves each unit (weights, f16 activations,
+// INT4 scales and activation group sums) into a shared-memory ring with TMA
+// bulk copies; four consumer warps run swap-AB tensor-core MMAs (activation
+// rows ride as the N=8 columns).  A tile that spans several CTAs is reduced by
+// its last contributor in a fixed slot order, so each column's result is
+// independent of how many columns share the launch.  Fused epilogues: residual
+// add, SiLU*up (Q/model.py:397) producing the next layer's f16 input, and q/k
+// RoPE (Q/tensor.py:65-82) + k/v append into the fp16 recent-token buffer
 // (Q/cache.py:216-234).
 #include <math.h>
 
@@ -23,320 +28,525 @@
 
 namespace qs {
 
-constexpr int kGemmThreads = 128;
+constexpr int kMaxCols = 16;
 
-template <int NTC>
+template <int WMODE, int NTC, int GKS>
 struct LinCfg {
-  static constexpr int COLS = 8 * NTC;
+  static constexpr int NCW = 4;                                  // consumer warps: one m-tile each
+  static constexpr int THREADS = (NCW + 1) * 32;                 // + producer warp
+  static constexpr int KCH = WMODE == QS_W_F16 ? 8 : 16;         // k-steps per unit (16 KB / 8 KB of weights)
+  static constexpr int WBYTES = WMODE == QS_W_F16 ? KCH * 512 : KCH / 4 * 512;  // per m-tile per unit
+  static constexpr int ROWS = 8 * NTC;                           // activation rows in the B region
+  static constexpr int BROW = KCH * 32 + 16;                     // bytes per activation row (+pad: no conflicts)
+  static constexpr int PBYTES_MAX = WMODE == QS_W_F16 ? 0 : (KCH / GKS) * 128;  // per m-tile: {S,Z} x 16 rows x groups
+  static constexpr int XROW = WMODE == QS_W_F16 ? 0 : KCH * 4 + 16;  // INT4: 16-sums of activations (+pad)
+  static constexpr int OFF_B = NCW * WBYTES;
+  static constexpr int OFF_P = OFF_B + ROWS * BROW;
+  static constexpr int OFF_X = OFF_P + NCW * PBYTES_MAX;
+  static constexpr int STAGE = (OFF_X + ROWS * XROW + 127) / 128 * 128;
+  static constexpr int NSTAGE = 4;
+  static constexpr int ZROW = WMODE == QS_W_F16 ? 0 : BROW;      // zero B row (INT4 group slots)
+  static constexpr int SMEM = NSTAGE * STAGE + 64 * ROWS * 4 + ZROW + 2 * NSTAGE * 8 + 16;
 };
+
+// mma.sync without `volatile` (pure: lets ptxas interleave the group's MMAs with unpacking)
+__device__ __forceinline__ void mma_acc(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_zc(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  const float z = 0.f;
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%10,%10,%10};\n"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(z));
+}
+
+// sum of N consecutive floats in shared memory (N in {1,2,4,8}; 4N-byte aligned)
+template <int N>
+__device__ __forceinline__ float sum_n(const float* p) {
+  if constexpr (N == 1) {
+    return p[0];
+  } else if constexpr (N == 2) {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    return __fadd_rn(v.x, v.y);
+  } else {
+    float a = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(p + i);
+      a = __fadd_rn(a, __fadd_rn(__fadd_rn(v.x, v.y), __fadd_rn(v.z, v.w)));
+    }
+    return a;
+  }
+}
 
 __device__ __forceinline__ float silu_f32(float x) { return __fdiv_rn(x, __fadd_rn(1.0f, expf(-x))); }
 
-template <int WMODE, int NTC, int EPI, int GKS>
-__global__ void __launch_bounds__(kGemmThreads) linear_kernel(const __grid_constant__ LinearParams P) {
+__host__ __device__ __forceinline__ long long cta_of_unit(long long u, long long U, long long C) {
+  return ((u + 1) * C - 1) / U;
+}
+
+// INT4 work unit of one consumer warp (one 16-row m-tile x nks k-steps).
+//
+// Offset-form codes (unpack_u4_raw): rows g carry 1024 + c, rows g+8 carry 1024 + 16c, so per
+// weight group  y += S * sum(code * x) + (Z - 1024 S) * sum(x)  (params are pre-folded).
+// The per-group MMA partials are kept apart in the MMA's N columns: with CW = activation columns
+// rounded up to a power of two, column n = slot * CW + c holds group slot `slot` of activation c
+// (a lane's B fragment is the activation row when its slot is current, else a zero row).  One
+// accumulator thus carries 8/CW groups, and the scale/zero-point epilogue runs once per window
+// of 8/CW groups instead of once per group; the slot partials are then summed across the quad.
+template <class C, int NTC, int GKS, int CW>
+__device__ __forceinline__ void int4_unit(const uint4* __restrict__ wa, const uint8_t* bbase, const uint8_t* zrow,
+                                          const float4* pp, const float* xsm, const int nks, const int g,
+                                          const int t4, float (&acc)[NTC][4]) {
+  static_assert(NTC == 1 || CW == 8, "two n-tiles only with one group per window");
+  constexpr int KCH = C::KCH;
+  constexpr int G8 = 8 / CW;
+  constexpr int WIN = (G8 * GKS < KCH) ? G8 * GKS : KCH;  // k-steps per window
+  constexpr int NSLOT = WIN / GKS;                          // groups per window
+  constexpr int XW = C::XROW / 4;
+  const int my_slot = g / CW;
+#pragma unroll
+  for (int w = 0; w < KCH / WIN; ++w) {
+    const int k0 = w * WIN;
+    if (k0 >= nks) break;
+    float D[NTC][4];
+#pragma unroll
+    for (int sl = 0; sl < NSLOT; ++sl) {
+      const uint8_t* brow[NTC];
+#pragma unroll
+      for (int nt = 0; nt < NTC; ++nt)
+        brow[nt] = (my_slot == sl ? bbase + (nt * 8 + g % CW) * C::BROW : zrow) + 4 * t4;
+#pragma unroll
+      for (int j = 0; j < GKS; ++j) {
+        const int ks = k0 + sl * GKS + j;
+        if (ks < nks) {
+          const uint4 w4 = wa[(ks >> 2) * 32];
+          const uint32_t wv = (ks & 3) == 0 ? w4.x : (ks & 3) == 1 ? w4.y : (ks & 3) == 2 ? w4.z : w4.w;
+          uint32_t a[4];
+          unpack_u4_raw(wv, a);
+#pragma unroll
+          for (int nt = 0; nt < NTC; ++nt) {
+            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32);
+            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32 + 16);
+            if (sl == 0 && j == 0) mma_zc(D[nt], a, b0, b1);
+            else mma_acc(D[nt], a, b0, b1);
+          }
+        }
+      }
+    }
+    // ---- window epilogue: scale + zero point per (row, column) ----
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt) {
+      float vg[2], v8[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 2 * t4 + e;
+        const int sl = n / CW, c = nt * 8 + n % CW;
+        const int gl = k0 / GKS + sl;  // group index within the unit
+        const int kk0 = gl * GKS;
+        vg[e] = v8[e] = 0.f;
+        if (sl < NSLOT && kk0 < nks) {
+          const float4 p = pp[gl * 8];  // {S_g, Z_g - 1024 S_g, S_g8 / 16, Z_g8 - 64 S_g8}
+          const float* xc = xsm + c * XW + kk0;
+          float X;
+          if (kk0 + GKS <= nks) {
+            X = sum_n<GKS>(xc);
+          } else {
+            X = 0.f;
+            for (int q = 0; q < nks - kk0; ++q) X = __fadd_rn(X, xc[q]);
+          }
+          vg[e] = __fmaf_rn(p.x, D[nt][e], __fmul_rn(p.y, X));
+          v8[e] = __fmaf_rn(p.z, D[nt][e + 2], __fmul_rn(p.w, X));
+        }
+      }
+      if constexpr (CW == 1) {
+        float r0 = __fadd_rn(vg[0], vg[1]), r2 = __fadd_rn(v8[0], v8[1]);
+        r0 = __fadd_rn(r0, __shfl_xor_sync(0xffffffffu, r0, 1));
+        r2 = __fadd_rn(r2, __shfl_xor_sync(0xffffffffu, r2, 1));
+        r0 = __fadd_rn(r0, __shfl_xor_sync(0xffffffffu, r0, 2));
+        r2 = __fadd_rn(r2, __shfl_xor_sync(0xffffffffu, r2, 2));
+        acc[nt][0] = __fadd_rn(acc[nt][0], r0);
+        acc[nt][2] = __fadd_rn(acc[nt][2], r2);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if constexpr (CW == 2) {
+            vg[e] = __fadd_rn(vg[e], __shfl_xor_sync(0xffffffffu, vg[e], 1));
+            v8[e] = __fadd_rn(v8[e], __shfl_xor_sync(0xffffffffu, v8[e], 1));
+          }
+          if constexpr (CW <= 4) {
+            vg[e] = __fadd_rn(vg[e], __shfl_xor_sync(0xffffffffu, vg[e], 2));
+            v8[e] = __fadd_rn(v8[e], __shfl_xor_sync(0xffffffffu, v8[e], 2));
+          }
+          acc[nt][e] = __fadd_rn(acc[nt][e], vg[e]);
+          acc[nt][e + 2] = __fadd_rn(acc[nt][e + 2], v8[e]);
+        }
+      }
+    }
+  }
+}
+
+template <int WMODE, int NTC, int EPI, int GKS, int CW>
+__global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS>::THREADS) linear_kernel(const __grid_constant__ LinearParams P) {
+  using C = LinCfg<WMODE, NTC, GKS>;
   constexpr int COLS = 8 * NTC;
-  extern __shared__ __align__(16) uint8_t sm[];
+  constexpr int KCH = C::KCH;
+  extern __shared__ __align__(128) uint8_t sm[];
+  float* ysm = reinterpret_cast<float*>(sm + C::NSTAGE * C::STAGE);  // [64][COLS]
+  uint8_t* zrow = reinterpret_cast<uint8_t*>(ysm + 64 * COLS);  // INT4: zero B row (C::ZROW bytes)
+  uint64_t* full_b = reinterpret_cast<uint64_t*>(zrow + C::ZROW);
+  uint64_t* empty_b = full_b + C::NSTAGE;
+  int* flag = reinterpret_cast<int*>(empty_b + C::NSTAGE);
+
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int mg = blockIdx.x, ksp = blockIdx.y;
   const int KS = P.K / 16;
-  const int ks0 = ksp * P.krange;
-  const int ks1 = min(KS, ks0 + P.krange);
-  const int nks = ks1 - ks0;
   const int MT = P.N / 16;
+  const int MG = (P.N + 63) / 64;
+  const int KC = (KS + KCH - 1) / KCH;  // k-chunks per 64-row tile
+  const long long U = (long long)MG * KC;
+  const long long Cn = gridDim.x;
+  const long long u_lo = (long long)blockIdx.x * U / Cn, u_hi = (long long)(blockIdx.x + 1) * U / Cn;
+  const int nunits = (int)(u_hi - u_lo);
   const int ncols = P.ncols;
-  // INT4: k-steps per weight group is the compile-time GKS (the host checks P.wgroup == 16*GKS)
-  const int ngr = (WMODE == QS_W_INT4) ? (nks + GKS - 1) / GKS : 0;
-  const int ngr_max = (WMODE == QS_W_INT4) ? (P.krange + GKS - 1) / GKS : 0;
+  const int gpr = WMODE == QS_W_INT4 ? (P.K + P.wgroup - 1) / P.wgroup : 1;
+  const int ks_pad = (KS + 3) / 4 * 4;
 
-  uint2* bs = reinterpret_cast<uint2*>(sm);                                   // [krange][NTC][32]
-  float4* psm = reinterpret_cast<float4*>(bs + (size_t)P.krange * NTC * 32);   // [4 mtiles][ngr_max][8]
-  float* xsum = reinterpret_cast<float*>(psm + (WMODE == QS_W_INT4 ? (size_t)4 * ngr_max * 8 : 0));  // [ngr][COLS]
-  float* ys = xsum + (WMODE == QS_W_INT4 ? (size_t)ngr_max * COLS : 0);       // [64][COLS]
-  int* ticket = reinterpret_cast<int*>(ys + 64 * COLS);
-
-  const int mt = mg * 4 + warp;
-  // ---- issue this warp's first weight loads before staging (overlaps the prologue) ----
-  constexpr int U = 8;  // uint4 per lane per buffer: 8 k-steps (f16) or 32 k-steps (INT4)
-  const uint4* wp;
-  int nq4;  // uint4 steps of this warp
-  if constexpr (WMODE == QS_W_F16) {
-    wp = reinterpret_cast<const uint4*>(P.w) + ((size_t)mt * KS + ks0) * 32 + lane;
-    nq4 = nks;
-  } else {
-    const int ks_pad = (KS + 3) / 4 * 4;  // frag4 words [mt][KSpad/4][32][4]; ks0 % 4 == 0
-    wp = reinterpret_cast<const uint4*>(P.w) + ((size_t)mt * (ks_pad / 4) + ks0 / 4) * 32 + lane;
-    nq4 = (nks + 3) / 4;
-  }
-  const bool active = mt < MT;
-  uint4 buf0[U], buf1[U];
-  auto ld = [&](uint4 (&b)[U], int base) {
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      b[u] = (active && base + u < nq4) ? ldg_nc_v4(wp + (size_t)(base + u) * 32) : make_uint4(0, 0, 0, 0);
-  };
-  ld(buf0, 0);
-  if (nq4 > U) ld(buf1, U);
-
-  // ---- stage the activation slice as f16 B fragments ----
-  for (int i = tid; i < nks * NTC * 32; i += kGemmThreads) {
-    int ln = i & 31, nt = (i >> 5) % NTC, kk = i / (NTC * 32);
-    int gg = ln >> 2, tt = ln & 3;
-    int col = nt * 8 + gg;
-    uint2 v = make_uint2(0u, 0u);
-    if (col < ncols) {
-      const float* xr = P.x + (size_t)col * P.K + (size_t)(ks0 + kk) * 16 + 2 * tt;
-      v.x = h2_as_u32(__floats2half2_rn(xr[0], xr[1]));
-      v.y = h2_as_u32(__floats2half2_rn(xr[8], xr[9]));
+  for (int i = tid; i < C::ZROW / 4; i += C::THREADS) reinterpret_cast<uint32_t*>(zrow)[i] = 0u;
+  if (tid == 0) {
+    for (int s = 0; s < C::NSTAGE; ++s) {
+      mbar_init(&full_b[s], 1);
+      mbar_init(&empty_b[s], C::NCW);
     }
-    bs[i] = v;
-  }
-  if constexpr (WMODE == QS_W_INT4) {
-    // per-group column sums of the f16-rounded activations (zero-point term)
-    for (int i = tid; i < ngr * COLS; i += kGemmThreads) {
-      int col = i % COLS, gr = i / COLS;
-      float a = 0.f;
-      if (col < ncols) {
-        int k0 = (ks0 + gr * GKS) * 16, k1 = min(ks1, ks0 + (gr + 1) * GKS) * 16;
-        const float* xr = P.x + (size_t)col * P.K;
-        for (int k = k0; k < k1; ++k) a += __half2float(__float2half_rn(xr[k]));
-      }
-      xsum[i] = a;
-    }
-    // (S, Z) of rows g and g+8 of the CTA's 4 m-tiles for the groups of this k-range
-    const int gpr = (P.K + P.wgroup - 1) / P.wgroup;
-    const int gr0 = ks0 / GKS;
-    const float4* pp = reinterpret_cast<const float4*>(P.wparams);
-    for (int i = tid; i < 4 * ngr * 8; i += kGemmThreads) {
-      int gg = i & 7, gr = (i >> 3) % ngr, w = i / (8 * ngr);
-      int m = mg * 4 + w;
-      psm[(w * ngr_max + gr) * 8 + gg] = m < MT ? __ldg(pp + ((size_t)m * gpr + gr0 + gr) * 8 + gg) : make_float4(0, 0, 0, 0);
-    }
+    fence_mbar_init();
   }
   __syncthreads();
+  if (nunits <= 0) return;
 
+  if (warp == C::NCW) {
+    // ======================= producer warp =======================
+    if (lane != 0) return;
+    for (int i = 0; i < nunits; ++i) {
+      const int s = i % C::NSTAGE;
+      if (i >= C::NSTAGE) mbar_wait_sleep(&empty_b[s], ((i / C::NSTAGE) - 1) & 1);
+      const long long u = u_lo + i;
+      const int mg = (int)(u / KC), kc = (int)(u % KC);
+      const int ks0 = kc * KCH, nks = min(KCH, KS - ks0);
+      uint8_t* sp = sm + s * C::STAGE;
+      uint32_t bytes = 0;
+      const int nmt = min(C::NCW, MT - mg * 4);
+      uint32_t wb, bb, pb = 0, xb = 0;
+      if constexpr (WMODE == QS_W_F16) {
+        wb = (uint32_t)nks * 512;
+      } else {
+        wb = (uint32_t)((nks + 3) / 4) * 512;
+      }
+      bb = (uint32_t)nks * 32;
+      const int ngr = WMODE == QS_W_INT4 ? (nks * 16 + P.wgroup - 1) / P.wgroup : 0;
+      if constexpr (WMODE == QS_W_INT4) {
+        pb = (uint32_t)ngr * 128;
+        xb = (uint32_t)((nks + 3) / 4) * 16;
+      }
+      bytes = nmt * (wb + pb) + ncols * (bb + xb);
+      mbar_arrive_expect_tx(&full_b[s], bytes);
+      for (int w = 0; w < nmt; ++w) {
+        const int mt = mg * 4 + w;
+        if constexpr (WMODE == QS_W_F16) {
+          bulk_g2s(sp + w * C::WBYTES, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)mt * KS + ks0) * 512, wb,
+                   &full_b[s]);
+        } else {
+          bulk_g2s(sp + w * C::WBYTES, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)mt * (ks_pad / 4) + ks0 / 4) * 512,
+                   wb, &full_b[s]);
+          const int gr0 = ks0 * 16 / P.wgroup;
+          bulk_g2s(sp + C::OFF_P + w * C::PBYTES_MAX,
+                   reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)mt * gpr + gr0) * 128, pb, &full_b[s]);
+        }
+      }
+      for (int c = 0; c < ncols; ++c) {
+        bulk_g2s(sp + C::OFF_B + c * C::BROW, reinterpret_cast<const __half*>(P.xh) + (size_t)c * P.ldxh + ks0 * 16, bb,
+                 &full_b[s]);
+        if constexpr (WMODE == QS_W_INT4)
+          bulk_g2s(sp + C::OFF_X + c * C::XROW, P.xs + (size_t)c * P.ldxs + ks0, xb, &full_b[s]);
+      }
+    }
+    return;
+  }
+
+  // ======================= consumer warps =======================
   float acc[NTC][4];
 #pragma unroll
   for (int nt = 0; nt < NTC; ++nt)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
 
-  if (active) {
-    if constexpr (WMODE == QS_W_F16) {
-      auto mm = [&](uint4 (&b)[U], int base) {
+  for (int i = 0; i < nunits; ++i) {
+    const int s = i % C::NSTAGE;
+    const long long u = u_lo + i;
+    const int mg = (int)(u / KC), kc = (int)(u % KC);
+    const int ks0 = kc * KCH, nks = min(KCH, KS - ks0);
+    const int mt = mg * 4 + warp;
+    const uint8_t* sp = sm + s * C::STAGE;
+    mbar_wait_sleep(&full_b[s], (i / C::NSTAGE) & 1);
+    if (mt < MT) {
+      // B fragments: row r = activation column; columns >= ncols read stale shared memory,
+      // which only ever reaches the matching (discarded) output columns of the MMA.
+      const uint8_t* bst = sp + C::OFF_B + g * C::BROW + 4 * t4;
+      if constexpr (WMODE == QS_W_F16) {
+        const uint4* wa = reinterpret_cast<const uint4*>(sp + warp * C::WBYTES) + lane;
+        if (nks == KCH) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (base + u < nks) {
-            uint32_t a[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+          for (int ks = 0; ks < KCH; ++ks) {
+            const uint4 w4 = wa[ks * 32];
+            const uint32_t a[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
             for (int nt = 0; nt < NTC; ++nt) {
-              uint2 bb = bs[((size_t)(base + u) * NTC + nt) * 32 + lane];
-              mma16816(acc[nt], a, bb.x, bb.y);
+              const uint8_t* row = bst + nt * 8 * C::BROW + ks * 32;
+              mma_acc(acc[nt], a, *reinterpret_cast<const uint32_t*>(row), *reinterpret_cast<const uint32_t*>(row + 16));
+            }
+          }
+        } else {
+          for (int ks = 0; ks < nks; ++ks) {
+            const uint4 w4 = wa[ks * 32];
+            const uint32_t a[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int nt = 0; nt < NTC; ++nt) {
+              const uint8_t* row = bst + nt * 8 * C::BROW + ks * 32;
+              mma_acc(acc[nt], a, *reinterpret_cast<const uint32_t*>(row), *reinterpret_cast<const uint32_t*>(row + 16));
             }
           }
         }
-      };
-      for (int base = 0; base < nks; base += 2 * U) {
-        mm(buf0, base);
-        if (base + 2 * U < nks) ld(buf0, base + 2 * U);
-        if (base + U < nks) {
-          mm(buf1, base + U);
-          if (base + 3 * U < nks) ld(buf1, base + 3 * U);
-        }
-      }
-    } else {
-      const float4* pw4 = psm + (size_t)warp * ngr_max * 8 + g;
-      float tmp[NTC][4];
-#pragma unroll
-      for (int nt = 0; nt < NTC; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) tmp[nt][e] = 0.f;
-      auto flush_group = [&](int gl) {
-        const float4 sp = pw4[gl * 8];
-#pragma unroll
-        for (int nt = 0; nt < NTC; ++nt) {
-          const int c0 = nt * 8 + 2 * t4;
-          const float x0 = xsum[gl * COLS + c0], x1 = xsum[gl * COLS + c0 + 1];
-          acc[nt][0] += sp.x * tmp[nt][0] + sp.y * x0;
-          acc[nt][1] += sp.x * tmp[nt][1] + sp.y * x1;
-          acc[nt][2] += sp.z * tmp[nt][2] + sp.w * x0;
-          acc[nt][3] += sp.z * tmp[nt][3] + sp.w * x1;
-          tmp[nt][0] = tmp[nt][1] = tmp[nt][2] = tmp[nt][3] = 0.f;
-        }
-      };
-      // base counts uint4 steps (4 k-steps each); 4*U k-steps per buffer is a multiple of GKS
-      auto mm = [&](uint4 (&b)[U], int base) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t wv[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int kk = (base + u) * 4 + v;  // local k-step
-            if (kk < nks) {
-              uint32_t a[4];
-              unpack_u4(wv[v], a);
-#pragma unroll
-              for (int nt = 0; nt < NTC; ++nt) {
-                uint2 bb = bs[((size_t)kk * NTC + nt) * 32 + lane];
-                mma16816(tmp[nt], a, bb.x, bb.y);
-              }
-              if (((u * 4 + v + 1) % GKS) == 0 || kk + 1 == nks) flush_group(kk / GKS);
-            }
-          }
-        }
-      };
-      for (int base = 0; base < nq4; base += 2 * U) {
-        mm(buf0, base);
-        if (base + 2 * U < nq4) ld(buf0, base + 2 * U);
-        if (base + U < nq4) {
-          mm(buf1, base + U);
-          if (base + 3 * U < nq4) ld(buf1, base + 3 * U);
-        }
+      } else {
+        const uint4* wa = reinterpret_cast<const uint4*>(sp + warp * C::WBYTES) + lane;
+        const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P + warp * C::PBYTES_MAX) + g;
+        const float* xsm = reinterpret_cast<const float*>(sp + C::OFF_X);
+        if (nks == KCH)
+          int4_unit<C, NTC, GKS, CW>(wa, sp + C::OFF_B, zrow, pp, xsm, KCH, g, t4, acc);
+        else
+          int4_unit<C, NTC, GKS, CW>(wa, sp + C::OFF_B, zrow, pp, xsm, nks, g, t4, acc);
       }
     }
-  }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_b[s]);
 
-  // ---- collect the 64 x COLS tile (split-K reduced in fixed order) ----
-  const int row0 = mg * 64;
-  if (P.ksplit > 1) {
-    float* wk = P.work + (size_t)ksp * ncols * P.N;  // [ksplit][ncols][N]
+    // ---- tile boundary: publish this CTA's partial of 64-row tile mg ----
+    const bool last_unit_of_tile = (kc == KC - 1) || (i == nunits - 1);
+    if (!last_unit_of_tile) continue;
+    const long long cf = cta_of_unit((long long)mg * KC, U, Cn);
+    const long long cl = cta_of_unit((long long)mg * KC + KC - 1, U, Cn);
+    const int ncontrib = (int)(cl - cf + 1);
+    const int slot = (int)(blockIdx.x - cf);
+    float* wk = P.work + ((size_t)mg * P.maxc + slot) * kMaxCols * 64;  // [col][row]
     if (mt < MT) {
 #pragma unroll
       for (int nt = 0; nt < NTC; ++nt) {
-        int c0 = nt * 8 + 2 * t4;
-        int r = mt * 16 + g;
+        const int c0 = nt * 8 + 2 * t4;
+        const int r = warp * 16 + g;
         if (c0 < ncols) {
-          wk[(size_t)c0 * P.N + r] = acc[nt][0];
-          wk[(size_t)c0 * P.N + r + 8] = acc[nt][2];
+          wk[c0 * 64 + r] = acc[nt][0];
+          wk[c0 * 64 + r + 8] = acc[nt][2];
         }
         if (c0 + 1 < ncols) {
-          wk[(size_t)(c0 + 1) * P.N + r] = acc[nt][1];
-          wk[(size_t)(c0 + 1) * P.N + r + 8] = acc[nt][3];
+          wk[(c0 + 1) * 64 + r] = acc[nt][1];
+          wk[(c0 + 1) * 64 + r + 8] = acc[nt][3];
+        }
+        acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+      }
+    }
+    __threadfence();
+    asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
+    if (tid == 0) *flag = atomicAdd(&P.counters[mg], 1) == ncontrib - 1;
+    asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
+    if (!*flag) continue;
+    __threadfence();
+    const int row0 = mg * 64;
+    const int nthr = C::NCW * 32;
+    for (int e = tid; e < 64 * ncols; e += nthr) {
+      const int r = e % 64, c = e / 64;
+      float a = 0.f;
+      for (int q = 0; q < ncontrib; ++q) a = a + __ldcg(P.work + (((size_t)mg * P.maxc + q) * kMaxCols + c) * 64 + r);
+      ysm[r * COLS + c] = a;
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
+    if (tid == 0) P.counters[mg] = 0;
+
+    // ---- fused epilogue over the 64 x ncols tile ----
+    if constexpr (EPI == QS_EPI_STORE || EPI == QS_EPI_ADD) {
+      for (int e = tid; e < 64 * ncols; e += nthr) {
+        const int r = e % 64, c = e / 64;
+        const int n = row0 + r;
+        if (n >= P.N) continue;
+        const float v = ysm[r * COLS + c];
+        float* dst = P.y + (size_t)c * P.ldy + n;
+        if (EPI == QS_EPI_ADD) *dst = __fadd_rn(*dst, v);
+        else *dst = v;
+      }
+    } else if constexpr (EPI == QS_EPI_SILU_MUL) {
+      // m-tiles interleaved: local tiles (0,1) = (gate, up) of output tile 2*mg, (2,3) of 2*mg+1;
+      // output: f16 input of the down projection + its 16-sums (one sum per output tile)
+      for (int e = tid; e < 32 * ncols; e += nthr) {
+        const int rr = e % 32, c = e / 32;
+        const int pair = rr / 16, r16 = rr % 16;
+        const int rg = pair * 32 + r16, ru = rg + 16;
+        if (row0 + rg >= P.N) continue;
+        const int n = (mg * 2 + pair) * 16 + r16;
+        const float h = __fmul_rn(silu_f32(ysm[rg * COLS + c]), ysm[ru * COLS + c]);
+        const __half hh = __float2half_rn(h);
+        reinterpret_cast<__half*>(P.yh)[(size_t)c * P.ldyh + n] = hh;
+        if (P.y) P.y[(size_t)c * P.ldy + n] = h;
+        ysm[rg * COLS + c] = __half2float(hh);  // gate slot now holds the f16-rounded output
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
+      for (int e = tid; e < 2 * ncols; e += nthr) {
+        const int pair = e % 2, c = e / 2;
+        if (row0 + pair * 32 >= P.N) continue;
+        float a = 0.f;
+        for (int r16 = 0; r16 < 16; ++r16) a += ysm[(pair * 32 + r16) * COLS + c];
+        P.ys[(size_t)c * P.ldys + mg * 2 + pair] = a;
+      }
+    } else if constexpr (EPI == QS_EPI_QKV) {
+      const float2* rope = reinterpret_cast<const float2*>(P.rope);
+      const int hd = P.hd;
+      for (int e = tid; e < 32 * ncols; e += nthr) {
+        const int pr = e % 32, c = e / 32;
+        const int r = 2 * pr;
+        const int n = row0 + r;
+        if (n >= P.N) continue;
+        const int sq = c / P.T, t = c % P.T;
+        float ev = ysm[r * COLS + c], ov = ysm[(r + 1) * COLS + c];
+        if (n < P.Nq + P.Nk) {
+          const int nn = n < P.Nq ? n : n - P.Nq;
+          const int d = nn % hd;
+          const int pos = P.pos_base[sq] + P.row_offset + t;
+          const float2 cs = rope[(size_t)pos * (hd / 2) + d / 2];
+          const float e2 = __fsub_rn(__fmul_rn(ev, cs.x), __fmul_rn(ov, cs.y));
+          const float o2 = __fadd_rn(__fmul_rn(ev, cs.y), __fmul_rn(ov, cs.x));
+          ev = e2;
+          ov = o2;
+        }
+        if (n < P.Nq) {
+          P.q_out[(size_t)c * P.Nq + n] = ev;
+          P.q_out[(size_t)c * P.Nq + n + 1] = ov;
+        } else {
+          const bool isk = n < P.Nq + P.Nk;
+          const int nn = isk ? n - P.Nq : n - P.Nq - P.Nk;
+          const int head = nn / hd, d = nn % hd;
+          const int row = P.row_base[sq] + P.row_offset + t;
+          __half* dst = reinterpret_cast<__half*>(isk ? P.k_dst : P.v_dst) + (size_t)sq * P.kv_seq_stride +
+                        (size_t)head * P.kv_head_stride + (size_t)row * hd + d;
+          *reinterpret_cast<__half2*>(dst) = __floats2half2_rn(ev, ov);
         }
       }
     }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) *ticket = atomicAdd(&P.counters[mg], 1);
-    __syncthreads();
-    if (*ticket != P.ksplit - 1) return;
-    __threadfence();
-    for (int i = tid; i < 64 * ncols; i += kGemmThreads) {
-      int r = i % 64, c = i / 64;
-      float a = 0.f;
-      if (row0 + r < P.N)
-        for (int s = 0; s < P.ksplit; ++s) a += __ldcg(P.work + ((size_t)s * ncols + c) * P.N + row0 + r);
-      ys[r * COLS + c] = a;
-    }
-    if (tid == 0) P.counters[mg] = 0;
-  } else {
-    if (mt < MT) {
-#pragma unroll
-      for (int nt = 0; nt < NTC; ++nt) {
-        int c0 = nt * 8 + 2 * t4;
-        int r = warp * 16 + g;
-        ys[r * COLS + c0] = acc[nt][0];
-        ys[r * COLS + c0 + 1] = acc[nt][1];
-        ys[(r + 8) * COLS + c0] = acc[nt][2];
-        ys[(r + 8) * COLS + c0 + 1] = acc[nt][3];
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- fused epilogue ----
-  if constexpr (EPI == QS_EPI_STORE || EPI == QS_EPI_ADD) {
-    for (int i = tid; i < 64 * ncols; i += kGemmThreads) {
-      int r = i % 64, c = i / 64;
-      int n = row0 + r;
-      if (n >= P.N) continue;
-      float v = ys[r * COLS + c];
-      float* dst = P.y + (size_t)c * P.ldy + n;
-      if (EPI == QS_EPI_ADD) *dst = __fadd_rn(*dst, v);
-      else *dst = v;
-    }
-  } else if constexpr (EPI == QS_EPI_SILU_MUL) {
-    // m-tiles interleaved: local tiles (0,1) = (gate, up) of output tile 2*mg, (2,3) of 2*mg+1
-    for (int i = tid; i < 32 * ncols; i += kGemmThreads) {
-      int rr = i % 32, c = i / 32;
-      int pair = rr / 16, r16 = rr % 16;
-      int rg = pair * 32 + r16, ru = rg + 16;
-      int n = (mg * 2 + pair) * 16 + r16;
-      if ((row0 + rg) >= P.N) continue;
-      float gv = ys[rg * COLS + c], uv = ys[ru * COLS + c];
-      P.y[(size_t)c * P.ldy + n] = __fmul_rn(silu_f32(gv), uv);
-    }
-  } else if constexpr (EPI == QS_EPI_QKV) {
-    const float2* rope = reinterpret_cast<const float2*>(P.rope);
-    const int hd = P.hd;
-    for (int i = tid; i < 32 * ncols; i += kGemmThreads) {
-      int pr = i % 32, c = i / 32;
-      int r = 2 * pr;
-      int n = row0 + r;
-      if (n >= P.N) continue;
-      int seq = c / P.T, t = c % P.T;
-      float e = ys[r * COLS + c], o = ys[(r + 1) * COLS + c];
-      if (n < P.Nq + P.Nk) {
-        int nn = n < P.Nq ? n : n - P.Nq;
-        int d = nn % hd;
-        int pos = P.pos_base[seq] + P.row_offset + t;
-        float2 cs = rope[(size_t)pos * (hd / 2) + d / 2];
-        float e2 = __fsub_rn(__fmul_rn(e, cs.x), __fmul_rn(o, cs.y));
-        float o2 = __fadd_rn(__fmul_rn(e, cs.y), __fmul_rn(o, cs.x));
-        e = e2;
-        o = o2;
-      }
-      if (n < P.Nq) {
-        P.q_out[(size_t)c * P.Nq + n] = e;
-        P.q_out[(size_t)c * P.Nq + n + 1] = o;
-      } else {
-        bool isk = n < P.Nq + P.Nk;
-        int nn = isk ? n - P.Nq : n - P.Nq - P.Nk;
-        int head = nn / hd, d = nn % hd;
-        int row = P.row_base[seq] + P.row_offset + t;
-        __half* dst = reinterpret_cast<__half*>(isk ? P.k_dst : P.v_dst) + (size_t)seq * P.kv_seq_stride +
-                      (size_t)head * P.kv_head_stride + (size_t)row * hd + d;
-        *reinterpret_cast<__half2*>(dst) = __floats2half2_rn(e, o);
-      }
-    }
+    asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));  // ysm reuse by the next tile
   }
 }
 
-template <int WMODE, int NTC, int EPI, int GKS>
-static cudaError_t launch_lin_t(const LinearParams& p, cudaStream_t s) {
-  constexpr int COLS = 8 * NTC;
-  size_t ngr = (WMODE == QS_W_INT4) ? (size_t)((p.krange + GKS - 1) / GKS) : 0;
-  size_t smem = (size_t)p.krange * NTC * 32 * 8 + ngr * 4 * 8 * 16 + ngr * COLS * 4 + 64 * COLS * 4 + 16;
-  auto kern = linear_kernel<WMODE, NTC, EPI, GKS>;
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
+// ---------------------------------------------------------------------------
+// activation prep: f16 copy (optionally RMS-normalised) + 16-sums
+// ---------------------------------------------------------------------------
+__global__ void prep_act_kernel(const float* __restrict__ x, const float* __restrict__ gain, float eps,
+                                __half* __restrict__ xh, long long ldxh, float* __restrict__ xs, long long ldxs,
+                                int d) {
+  const float* xr = x + (size_t)blockIdx.x * d;
+  __half* hr = xh + (size_t)blockIdx.x * ldxh;
+  float* sr = xs + (size_t)blockIdx.x * ldxs;
+  __shared__ float red[32];
+  __shared__ float s_inv;
+  float scale = 1.f;
+  if (gain) {
+    float a = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) a += __fmul_rn(xr[i], xr[i]);
+    a = warp_sum(a);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+      v = warp_sum(v);
+      if (threadIdx.x == 0) s_inv = __fsqrt_rn(__fadd_rn(__fdiv_rn(v, (float)d), eps));
+    }
+    __syncthreads();
+    scale = s_inv;
   }
-  dim3 grid((p.N + 63) / 64, p.ksplit);
-  kern<<<grid, kGemmThreads, smem, s>>>(p);
+  // one thread per 16-element group: convert, store, sum the rounded values
+  for (int gi = threadIdx.x; gi < d / 16; gi += blockDim.x) {
+    float s = 0.f;
+    __align__(16) __half hv[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int i = gi * 16 + j;
+      const float v = gain ? __fmul_rn(__fdiv_rn(xr[i], scale), gain[i]) : xr[i];
+      hv[j] = __float2half_rn(v);
+      s += __half2float(hv[j]);
+    }
+    *reinterpret_cast<uint4*>(hr + gi * 16) = *reinterpret_cast<uint4*>(hv);
+    *reinterpret_cast<uint4*>(hr + gi * 16 + 8) = *reinterpret_cast<uint4*>(hv + 8);
+    sr[gi] = s;
+  }
+}
+
+cudaError_t launch_prep_act(const float* x, const float* gain, float eps, void* xh, long long ldxh, float* xs,
+                            long long ldxs, int n, int d, cudaStream_t s) {
+  prep_act_kernel<<<n, 256, 0, s>>>(x, gain, eps, reinterpret_cast<__half*>(xh), ldxh, xs, ldxs, d);
   return cudaGetLastError();
 }
 
-template <int WMODE, int NTC, int GKS>
+// CTAs actually launched: never more than work units, so every CTA owns at least one unit
+// and the contributors of a tile are exactly the CTAs cta_of_unit() names.
+int linear_grid_ctas(int wmode, int N, int K, int nctas) {
+  const int KCH = wmode == QS_W_F16 ? LinCfg<QS_W_F16, 1, 1>::KCH : LinCfg<QS_W_INT4, 1, 1>::KCH;
+  const long long KS = K / 16, MG = (N + 63) / 64, KC = (KS + KCH - 1) / KCH, U = MG * KC;
+  return (int)(U < nctas ? U : nctas);
+}
+
+int linear_maxc(int wmode, int N, int K, int nctas) {
+  const int KCH = wmode == QS_W_F16 ? LinCfg<QS_W_F16, 1, 1>::KCH : LinCfg<QS_W_INT4, 1, 1>::KCH;
+  const long long KS = K / 16, MG = (N + 63) / 64, KC = (KS + KCH - 1) / KCH, U = MG * KC;
+  const long long C = linear_grid_ctas(wmode, N, K, nctas);
+  int mx = 1;
+  for (long long m = 0; m < MG; ++m) {
+    const long long cf = cta_of_unit(m * KC, U, C), cl = cta_of_unit(m * KC + KC - 1, U, C);
+    if (cl - cf + 1 > mx) mx = (int)(cl - cf + 1);
+  }
+  return mx;
+}
+
+template <int WMODE, int NTC, int EPI, int GKS, int CW>
+static cudaError_t launch_lin_t(const LinearParams& p, cudaStream_t s) {
+  using C = LinCfg<WMODE, NTC, GKS>;
+  auto kern = linear_kernel<WMODE, NTC, EPI, GKS, CW>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  kern<<<linear_grid_ctas(WMODE, p.N, p.K, p.nctas), C::THREADS, C::SMEM, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int WMODE, int NTC, int GKS, int CW>
 static cudaError_t launch_lin_e(const LinearParams& p, cudaStream_t s) {
   switch (p.epi) {
-    case QS_EPI_STORE: return launch_lin_t<WMODE, NTC, QS_EPI_STORE, GKS>(p, s);
-    case QS_EPI_ADD: return launch_lin_t<WMODE, NTC, QS_EPI_ADD, GKS>(p, s);
-    case QS_EPI_QKV: return launch_lin_t<WMODE, NTC, QS_EPI_QKV, GKS>(p, s);
-    case QS_EPI_SILU_MUL: return launch_lin_t<WMODE, NTC, QS_EPI_SILU_MUL, GKS>(p, s);
+    case QS_EPI_STORE: return launch_lin_t<WMODE, NTC, QS_EPI_STORE, GKS, CW>(p, s);
+    case QS_EPI_ADD: return launch_lin_t<WMODE, NTC, QS_EPI_ADD, GKS, CW>(p, s);
+    case QS_EPI_QKV: return launch_lin_t<WMODE, NTC, QS_EPI_QKV, GKS, CW>(p, s);
+    case QS_EPI_SILU_MUL: return launch_lin_t<WMODE, NTC, QS_EPI_SILU_MUL, GKS, CW>(p, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
+// column-count dispatch; INT4 packs 8/CW weight groups into the MMA's N columns (int4_unit)
 template <int WMODE, int GKS>
 static cudaError_t launch_lin_n(const LinearParams& p, cudaStream_t s) {
-  int ntc = (p.ncols + 7) / 8;
-  if (ntc <= 1) return launch_lin_e<WMODE, 1, GKS>(p, s);
-  if (ntc <= 2) return launch_lin_e<WMODE, 2, GKS>(p, s);
-  if (ntc <= 4) return launch_lin_e<WMODE, 4, GKS>(p, s);
-  if (ntc <= 8) return launch_lin_e<WMODE, 8, GKS>(p, s);
+  if (WMODE == QS_W_INT4) {
+    if (p.ncols == 1) return launch_lin_e<WMODE, 1, GKS, 1>(p, s);
+    if (p.ncols == 2) return launch_lin_e<WMODE, 1, GKS, 2>(p, s);
+    if (p.ncols <= 4) return launch_lin_e<WMODE, 1, GKS, 4>(p, s);
+  }
+  if (p.ncols <= 8) return launch_lin_e<WMODE, 1, GKS, 8>(p, s);
+  if (p.ncols <= 16) return launch_lin_e<WMODE, 2, GKS, 8>(p, s);
   return cudaErrorInvalidValue;
 }
 
@@ -352,6 +562,32 @@ cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {
     }
   }
   return cudaErrorInvalidValue;
+}
+
+template <int WMODE, int NTC, int GKS>
+static int occ_of() {
+  using C = LinCfg<WMODE, NTC, GKS>;
+  auto kern = linear_kernel<WMODE, NTC, QS_EPI_STORE, GKS, 8>;
+  int n = 0;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, C::THREADS, C::SMEM);
+  return n;
+}
+
+template <int WMODE, int GKS>
+static int occ_n(int ncols) {
+  return ncols <= 8 ? occ_of<WMODE, 1, GKS>() : occ_of<WMODE, 2, GKS>();
+}
+
+int linear_occupancy(int wmode, int wgroup, int ncols) {
+  if (wmode == QS_W_F16) return occ_n<QS_W_F16, 1>(ncols);
+  switch (wgroup) {
+    case 16: return occ_n<QS_W_INT4, 1>(ncols);
+    case 32: return occ_n<QS_W_INT4, 2>(ncols);
+    case 64: return occ_n<QS_W_INT4, 4>(ncols);
+    case 128: return occ_n<QS_W_INT4, 8>(ncols);
+    default: return 0;
+  }
 }
 
 }  // namespace qs

@@ -263,7 +263,11 @@ __global__ void wq_fragparams_kernel(WGeom geo, const float* __restrict__ s, con
   int grp = (int)(rest % geo.gpr);
   int mt = (int)(rest / geo.gpr);
   int n0 = mt * 16 + g, n1 = n0 + 8;
-  out[i] = make_float4(s[n0 * geo.gpr + grp], z[n0 * geo.gpr + grp], s[n1 * geo.gpr + grp], z[n1 * geo.gpr + grp]);
+  // pre-folded for the offset-form MMA (qs_gemm.cu): rows g carry 1024 + c, rows g+8 carry 1024 + 16c
+  //   {S_g, Z_g - 1024 S_g, S_g8 / 16, Z_g8 - 64 S_g8}
+  const float s0 = s[n0 * geo.gpr + grp], z0 = z[n0 * geo.gpr + grp];
+  const float s1 = s[n1 * geo.gpr + grp], z1 = z[n1 * geo.gpr + grp];
+  out[i] = make_float4(s0, __fmaf_rn(-1024.f, s0, z0), __fmul_rn(s1, 0.0625f), __fmaf_rn(-64.f, s1, z1));
 }
 
 // fp16 frag layout [mt][ks][32][8 halves]

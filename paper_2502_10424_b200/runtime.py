@@ -194,21 +194,29 @@ def build_device_weights(geo: Geometry, layer_mats, embedding, final_norm, lm_he
 # ---------------------------------------------------------------------------
 
 
-def plan_linear(pl: PackedLinear, ncols: int) -> tuple[int, int]:
-    """(ksplit, krange): enough CTAs to cover the SMs twice, bounded smem."""
-    KS = pl.K // 16
-    mgroups = -(-pl.N // 64)
-    ntc = -(-ncols // 8)
-    ntc = 1 if ntc <= 1 else 2 if ntc <= 2 else 4 if ntc <= 4 else 8
-    align = 4 * max(1, pl.group // 16) if pl.wmode == _lib.W_INT4 else 1
-    max_kr = max(align, (256 // ntc) // align * align)
-    want = max(1, -(-4 * SM_COUNT // mgroups))
-    kr = -(-KS // want)
-    kr = max(kr, 16)
-    kr = min(kr, max_kr)
-    kr = -(-kr // align) * align
-    ks = -(-KS // kr)
-    return ks, kr
+_LIN_GRID: dict = {}
+
+
+def linear_grid(wmode: int, group: int = 16) -> int:
+    """Stream-K grid of the linear kernel: every resident slot, fixed per weight
+    format (never per activation-row count, so results are batch-invariant)."""
+    key = (wmode, group)
+    n = _LIN_GRID.get(key)
+    if n is None:
+        occ = _lib.load().qs_linear_occupancy(wmode, group, 1)
+        n = SM_COUNT * max(1, occ)
+        _LIN_GRID[key] = n
+    return n
+
+
+def linear_plan(pl: PackedLinear) -> tuple[int, int]:
+    """(nctas, maxc) for one packed linear layer."""
+    import ctypes
+
+    nctas = linear_grid(pl.wmode, pl.group if pl.wmode == _lib.W_INT4 else 16)
+    mx = ctypes.c_int(0)
+    _lib.call("qs_linear_plan", pl.wmode, pl.N, pl.K, nctas, ctypes.byref(mx))
+    return nctas, mx.value
 
 
 def plan_attention_splits(n_heads_total: int, max_chunks: int, ctas_per_sm: int = 2) -> int:
@@ -242,10 +250,15 @@ class Runner:
         dev = torch.device("cuda")
         d, nq = geo.hidden, geo.nq
         self.x = torch.zeros((max_cols, d), dtype=torch.float32, device=dev)
-        self.xn = torch.zeros_like(self.x)
         self.q = torch.zeros((max_cols, nq), dtype=torch.float32, device=dev)
         self.attn = torch.zeros_like(self.q)
-        self.h = torch.zeros((max_cols, geo.mlp_hidden), dtype=torch.float32, device=dev)
+        # f16 linear-layer inputs (+ 16-element sums for the INT4 zero-point term), padded rows
+        kmax = max(d, nq)
+        self.xh = torch.zeros((max_cols, (kmax + 64 + 7) // 8 * 8), dtype=torch.float16, device=dev)
+        self.xs = torch.zeros((max_cols, (kmax // 16 + 8 + 3) // 4 * 4), dtype=torch.float32, device=dev)
+        m = geo.mlp_hidden
+        self.hh = torch.zeros((max_cols, (m + 64 + 7) // 8 * 8), dtype=torch.float16, device=dev)
+        self.hs = torch.zeros((max_cols, (m // 16 + 8 + 3) // 4 * 4), dtype=torch.float32, device=dev)
         self.logits = torch.zeros((max_cols, geo.vocab), dtype=torch.float32, device=dev)
         self.tok = torch.zeros(max_cols + 1, dtype=torch.int32, device=dev)
         self.amax = torch.zeros(max_cols, dtype=torch.int32, device=dev)
@@ -274,9 +287,10 @@ class Runner:
         self.fp_cps = 0
         if self.is_fp:
             self.fp_cps = -(-self.max_chunks // self.splits_for(_lib.VIEW_FP16))
-        # linear scratch: ksplit * 64 cols * max N
+        # linear scratch: per 64-row tile, maxc partial slots of [16 cols][64 rows] (grown on demand,
+        # always before any CUDA graph is captured: the first use of a shape runs eagerly)
         nmax = max(geo.nq + 2 * geo.nk, 2 * geo.mlp_hidden, geo.vocab, geo.hidden)
-        self.work = torch.zeros(64 * 64 * nmax // 8, dtype=torch.float32, device=dev)
+        self.work = torch.zeros(1 << 16, dtype=torch.float32, device=dev)
         self.lin_counters = torch.zeros(-(-nmax // 64), dtype=torch.int32, device=dev)
         self._lin_cache: dict = {}
 
@@ -295,25 +309,34 @@ class Runner:
         return n
 
     # -- linear ---------------------------------------------------------------
-    def _linear(self, pl: PackedLinear, x, y, ncols: int, epi: int, *, ldy: int | None = None, layer: int = 0,
-                T: int = 1, row_offset: int = 0, stream: int) -> None:
+    def _linear(self, pl: PackedLinear, src, y, ncols: int, epi: int, *, ldy: int | None = None, layer: int = 0,
+                T: int = 1, row_offset: int = 0, yh=None, stream: int) -> None:
+        """One stream-K linear launch.  ``src`` = (f16 rows, 16-sums) written by
+        ``qs_prep_act`` or a SiLU epilogue; ``yh`` = (f16 rows, 16-sums) output
+        of the SiLU epilogue."""
         key = (id(pl), ncols, epi, layer, T, row_offset, self.cache.generation)
         a = self._lin_cache.get(key)
         if a is None:
             geo = self.geo
             a = _lib.LinearArgs()
             a.wmode, a.epi, a.N, a.K, a.ncols = pl.wmode, epi, pl.N, pl.K, ncols
-            a.ksplit, a.krange = plan_linear(pl, ncols)
-            ntc = -(-ncols // 8)
-            cols = 8 * (1 if ntc <= 1 else 2 if ntc <= 2 else 4 if ntc <= 4 else 8)
-            if a.ksplit * ncols * pl.N > self.work.numel():
-                raise ConfigError("linear split-K scratch too small")
-            a.wgroup = pl.group
+            a.nctas, a.maxc = linear_plan(pl)
+            need = -(-pl.N // 64) * a.maxc * 16 * 64
+            if need > self.work.numel():
+                torch = _torch()
+                self.work = torch.zeros(need, dtype=torch.float32, device=self.work.device)
+                self._relink_work()
+            a.wgroup = pl.group if pl.wmode == _lib.W_INT4 else 16
             a.w = pl.w.data_ptr()
             a.wparams = pl.params.data_ptr() if pl.params is not None else None
-            a.x = x.data_ptr()
+            xh, xs = src
+            a.xh, a.ldxh = xh.data_ptr(), xh.shape[1]
+            a.xs, a.ldxs = xs.data_ptr(), xs.shape[1]
             a.y = y.data_ptr() if y is not None else None
             a.ldy = ldy if ldy is not None else (y.shape[1] if y is not None else 0)
+            if yh is not None:
+                a.yh, a.ldyh = yh[0].data_ptr(), yh[0].shape[1]
+                a.ys, a.ldys = yh[1].data_ptr(), yh[1].shape[1]
             a.work = self.work.data_ptr()
             a.counters = self.lin_counters.data_ptr()
             if epi == _lib.EPI_QKV:
@@ -342,6 +365,17 @@ class Runner:
                     a.pos_base = c.d_pos.data_ptr()
             self._lin_cache[key] = a
         _lib.check(_lib.load().qs_linear(a, stream), "qs_linear")
+
+    def _relink_work(self) -> None:
+        for v in self._lin_cache.values():
+            if isinstance(v, _lib.LinearArgs):
+                v.work = self.work.data_ptr()
+
+    def _prep(self, x, gain, dst, ncols: int, stream: int) -> None:
+        xh, xs = dst
+        _lib.check(_lib.load().qs_prep_act(x.data_ptr(), gain.data_ptr() if gain is not None else None,
+                                           float(self.geo.norm_eps), xh.data_ptr(), xh.shape[1], xs.data_ptr(),
+                                           xs.shape[1], ncols, x.shape[1], stream), "qs_prep_act")
 
     # -- attention --------------------------------------------------------------
     def _attention(self, layer: int, view: int, T: int, row_offset: int, stream: int) -> None:
@@ -411,21 +445,20 @@ class Runner:
         tok_ptr = self.tok.data_ptr() + 4 * tok_offset
         _lib.check(lib.qs_embed(w.embedding.data_ptr(), tok_ptr, self.x.data_ptr(), ncols, d, geo.vocab,
                                 self.flags.data_ptr(), s), "qs_embed")
+        X, H = (self.xh, self.xs), (self.hh, self.hs)
         for li, lw in enumerate(w.layers):
-            _lib.check(lib.qs_rmsnorm(self.x.data_ptr(), w.attn_norms[li].data_ptr(), self.xn.data_ptr(), ncols, d,
-                                      geo.norm_eps, s), "qs_rmsnorm")
-            self._linear(lw["qkv"], self.xn, None, ncols, _lib.EPI_QKV, layer=li, T=T, row_offset=row_offset, stream=s)
+            self._prep(self.x, w.attn_norms[li], X, ncols, s)
+            self._linear(lw["qkv"], X, None, ncols, _lib.EPI_QKV, layer=li, T=T, row_offset=row_offset, stream=s)
             self._attention(li, view, T, row_offset, s)
-            self._linear(lw["o"], self.attn, self.x, ncols, _lib.EPI_ADD, stream=s)
-            _lib.check(lib.qs_rmsnorm(self.x.data_ptr(), w.mlp_norms[li].data_ptr(), self.xn.data_ptr(), ncols, d,
-                                      geo.norm_eps, s), "qs_rmsnorm")
-            self._linear(lw["gu"], self.xn, self.h, ncols, _lib.EPI_SILU_MUL, ldy=geo.mlp_hidden, stream=s)
-            self._linear(lw["down"], self.h, self.x, ncols, _lib.EPI_ADD, stream=s)
-        _lib.check(lib.qs_rmsnorm(self.x.data_ptr(), w.final_norm.data_ptr(), self.xn.data_ptr(), ncols, d,
-                                  geo.norm_eps, s), "qs_rmsnorm")
-        self._linear(w.lm_head, self.xn, self.logits, ncols, _lib.EPI_STORE, stream=s)
+            self._prep(self.attn, None, X, ncols, s)
+            self._linear(lw["o"], X, self.x, ncols, _lib.EPI_ADD, stream=s)
+            self._prep(self.x, w.mlp_norms[li], X, ncols, s)
+            self._linear(lw["gu"], X, None, ncols, _lib.EPI_SILU_MUL, yh=H, stream=s)
+            self._linear(lw["down"], H, self.x, ncols, _lib.EPI_ADD, stream=s)
+        self._prep(self.x, w.final_norm, X, ncols, s)
+        self._linear(w.lm_head, X, self.logits, ncols, _lib.EPI_STORE, stream=s)
         if argmax_to is not None:
             _lib.check(lib.qs_argmax(self.logits.data_ptr(), ncols, geo.vocab, argmax_to, 1, s), "qs_argmax")
 
     def kernel_launches_per_forward(self, nlayers: int) -> int:
-        return 1 + nlayers * 7 + 2
+        return 1 + nlayers * 8 + 3

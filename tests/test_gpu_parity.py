@@ -321,10 +321,54 @@ def test_chunked_attention_matches_monolithic():
 # ---------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("K,N,ncols", [(64, 48 * 4, 1), (4096, 4096, 1), (176, 64, 5), (4096, 11008 * 2, 9), (11008, 4096, 5)])
+def _act_buffers(x):
+    """f16 rows + 16-sums of ``x`` through qs_prep_act (the layout qs_linear reads)."""
+    n, K = x.shape
+    xh = torch.zeros(n, K + 64, dtype=torch.float16, device="cuda")
+    xs = torch.zeros(n, (K // 16 + 4 + 3) // 4 * 4, device="cuda")
+    _lib.check(_lib.load().qs_prep_act(x.data_ptr(), None, 0.0, xh.data_ptr(), xh.shape[1], xs.data_ptr(),
+                                       xs.shape[1], n, K, _lib.stream_ptr()))
+    return xh, xs
+
+
+def _run_linear(pl, x, ncols, *, epi=None, nctas=None, y=None, yh=None):
+    import ctypes
+
+    from paper_2502_10424_b200.runtime import linear_grid
+
+    xh, xs = _act_buffers(x)
+    a = _lib.LinearArgs()
+    a.wmode, a.epi, a.N, a.K, a.ncols = pl.wmode, _lib.EPI_STORE if epi is None else epi, pl.N, pl.K, ncols
+    a.nctas = nctas or linear_grid(pl.wmode, pl.group if pl.wmode == _lib.W_INT4 else 16)
+    mx = ctypes.c_int(0)
+    _lib.call("qs_linear_plan", pl.wmode, pl.N, pl.K, a.nctas, ctypes.byref(mx))
+    a.maxc = mx.value
+    a.wgroup = pl.group if pl.wmode == _lib.W_INT4 else 16
+    a.w = pl.w.data_ptr()
+    a.wparams = pl.params.data_ptr() if pl.params is not None else None
+    a.xh, a.ldxh, a.xs, a.ldxs = xh.data_ptr(), xh.shape[1], xs.data_ptr(), xs.shape[1]
+    if y is None and yh is None:
+        y = torch.zeros(ncols, pl.N, device="cuda")
+    if y is not None:
+        a.y, a.ldy = y.data_ptr(), y.shape[1]
+    if yh is not None:
+        a.yh, a.ldyh, a.ys, a.ldys = yh[0].data_ptr(), yh[0].shape[1], yh[1].data_ptr(), yh[1].shape[1]
+    mg = -(-pl.N // 64)
+    work = torch.full((mg * a.maxc * 16 * 64,), float("nan"), device="cuda")
+    cnt = torch.zeros(mg + 1, dtype=torch.int32, device="cuda")
+    a.work, a.counters = work.data_ptr(), cnt.data_ptr()
+    _lib.check(_lib.load().qs_linear(a, _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert int(cnt.sum().item()) == 0  # stream-K tile counters reset by the last contributor
+    return y
+
+
+@pytest.mark.parametrize("K,N,ncols", [(64, 48 * 4, 1), (4096, 4096, 1), (176, 64, 5), (4096, 11008 * 2, 9),
+                                       (11008, 4096, 5), (4096, 32000, 16), (1024, 576, 2), (176, 64, 3),
+                                       (11008, 128, 4), (272, 4096, 1)])
 @pytest.mark.parametrize("mode", ["f16", "int4"])
 def test_linear_vs_torch(K, N, ncols, mode):
-    from paper_2502_10424_b200.runtime import PackedLinear, plan_linear
+    from paper_2502_10424_b200.runtime import PackedLinear
 
     g = torch.Generator(device="cuda").manual_seed(K + N)
     w = torch.randn(K, N, device="cuda", generator=g) / math.sqrt(K)
@@ -336,22 +380,94 @@ def test_linear_vs_torch(K, N, ncols, mode):
         pl = PackedLinear.int4(w, 32)
         q = qs.quantize_weights(w.cpu().numpy(), 32)
         wref = torch.from_numpy(qs.dequantize_weights(q)).cuda()
-    y = torch.zeros(ncols, N, device="cuda")
-    a = _lib.LinearArgs()
-    a.wmode, a.epi, a.N, a.K, a.ncols = pl.wmode, _lib.EPI_STORE, N, K, ncols
-    a.ksplit, a.krange = plan_linear(pl, ncols)
-    a.wgroup = pl.group
-    a.w = pl.w.data_ptr()
-    a.wparams = pl.params.data_ptr() if pl.params is not None else None
-    a.x, a.y, a.ldy = x.data_ptr(), y.data_ptr(), N
-    work = torch.zeros(a.ksplit * 64 * N, device="cuda")
-    cnt = torch.zeros(N // 64 + 1, dtype=torch.int32, device="cuda")
-    a.work, a.counters = work.data_ptr(), cnt.data_ptr()
-    _lib.check(_lib.load().qs_linear(a, _lib.stream_ptr()))
+    y = _run_linear(pl, x, ncols)
     ref = x.half().float() @ wref
     err = (y - ref).abs().max().item()
     assert err <= 2e-3 * ref.abs().max().item() + 1e-4, err
-    assert int(cnt.sum().item()) == 0  # split-K semaphores reset
+
+
+@pytest.mark.parametrize("mode", ["f16", "int4"])
+@pytest.mark.parametrize("nctas", [1, 7, 148, 296, 1000])
+def test_linear_stream_k_grids(mode, nctas):
+    """Any grid size (units per CTA from <1 to whole tiles) reduces correctly."""
+    from paper_2502_10424_b200.runtime import PackedLinear
+
+    K, N, ncols = 1024, 576, 3
+    g = torch.Generator(device="cuda").manual_seed(nctas)
+    w = torch.randn(K, N, device="cuda", generator=g) / math.sqrt(K)
+    x = torch.randn(ncols, K, device="cuda", generator=g)
+    pl = PackedLinear.f16(w) if mode == "f16" else PackedLinear.int4(w, 64)
+    wref = w.half().float() if mode == "f16" else torch.from_numpy(
+        qs.dequantize_weights(qs.quantize_weights(w.cpu().numpy(), 64))).cuda()
+    y = _run_linear(pl, x, ncols, nctas=nctas)
+    ref = x.half().float() @ wref
+    assert (y - ref).abs().max().item() <= 2e-3 * ref.abs().max().item() + 1e-4
+
+
+@pytest.mark.parametrize("mode", ["f16", "int4"])
+def test_linear_batch_invariant(mode):
+    """f16 (target) weights: column c of a 9-column launch is bit-identical to a
+    1-column launch of the same row (what makes a (gamma+1)-row verify equal
+    gamma+1 AR steps).  INT4 (draft-only) weights pack weight groups into the
+    free MMA columns when few rows are active, so there the check is numeric."""
+    from paper_2502_10424_b200.runtime import PackedLinear
+
+    K, N = 4096, 4096
+    g = torch.Generator(device="cuda").manual_seed(3)
+    w = torch.randn(K, N, device="cuda", generator=g) / math.sqrt(K)
+    x = torch.randn(9, K, device="cuda", generator=g)
+    pl = PackedLinear.f16(w) if mode == "f16" else PackedLinear.int4(w, 64)
+    y9 = _run_linear(pl, x, 9)
+    for c in (0, 4, 8):
+        for n in (1, 2, 3, 6):
+            yn = _run_linear(pl, x[c:c + n].contiguous(), min(n, 9 - c))
+            if mode == "f16":
+                assert torch.equal(yn[0], y9[c])
+            else:
+                assert (yn[0] - y9[c]).abs().max().item() <= 1e-4 * y9[c].abs().max().item()
+
+
+@pytest.mark.parametrize("mode", ["f16", "int4"])
+def test_linear_silu_epilogue(mode):
+    """Fused gate/up -> SiLU(gate)*up -> f16 + 16-sums (the down projection's input)."""
+    from paper_2502_10424_b200.runtime import PackedLinear
+
+    K, M, ncols = 256, 352, 5
+    g = torch.Generator(device="cuda").manual_seed(11)
+    wg = torch.randn(K, M, device="cuda", generator=g) / math.sqrt(K)
+    wu = torch.randn(K, M, device="cuda", generator=g) / math.sqrt(K)
+    x = torch.randn(ncols, K, device="cuda", generator=g)
+    if mode == "f16":
+        pl = PackedLinear.f16_pair(wg, wu)
+        rg, ru = wg.half().float(), wu.half().float()
+    else:
+        pl = PackedLinear.int4_pair(wg, wu, 64)
+        rg, ru = (torch.from_numpy(qs.dequantize_weights(qs.quantize_weights(m.cpu().numpy(), 64))).cuda()
+                  for m in (wg, wu))
+    hh = torch.zeros(ncols, M + 64, dtype=torch.float16, device="cuda")
+    hs = torch.zeros(ncols, M // 16 + 8, device="cuda")
+    y = torch.zeros(ncols, M, device="cuda")
+    _run_linear(pl, x, ncols, epi=_lib.EPI_SILU_MUL, y=y, yh=(hh, hs))
+    xf = x.half().float()
+    a, b = xf @ rg, xf @ ru
+    ref = a / (1 + torch.exp(-a)) * b
+    assert (y - ref).abs().max().item() <= 3e-3 * ref.abs().max().item() + 1e-4
+    assert torch.equal(hh[:, :M], y.half())
+    sums = hh[:, :M].float().view(ncols, M // 16, 16).sum(-1)
+    assert torch.allclose(hs[:, :M // 16], sums, rtol=1e-5, atol=1e-4)
+
+
+def test_prep_act_rmsnorm():
+    d, n = 4096, 3
+    x = torch.randn(n, d, device="cuda")
+    gain = torch.rand(d, device="cuda") + 0.5
+    xh = torch.zeros(n, d + 64, dtype=torch.float16, device="cuda")
+    xs = torch.zeros(n, d // 16 + 4, device="cuda")
+    _lib.check(_lib.load().qs_prep_act(x.data_ptr(), gain.data_ptr(), 1e-5, xh.data_ptr(), xh.shape[1],
+                                       xs.data_ptr(), xs.shape[1], n, d, _lib.stream_ptr()))
+    ref = (x / torch.sqrt((x * x).mean(-1, keepdim=True) + 1e-5) * gain)
+    assert (xh[:, :d].float() - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
+    assert torch.allclose(xs[:, :d // 16], xh[:, :d].float().view(n, -1, 16).sum(-1), rtol=1e-5, atol=1e-4)
 
 
 # ---------------------------------------------------------------------------
