@@ -44,8 +44,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
 
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cu")]
+    headers.append(os.path.join(ROOT, "include", "quantspec_b200.h"))
+    newest_header = max(os.path.getmtime(h) for h in headers)
+
     def one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        if (not force and os.path.exists(obj) and os.path.getmtime(obj) > os.path.getmtime(os.path.join(CSRC, src))
+                and os.path.getmtime(obj) > newest_header):
+            return obj  # object is current
         cmd = [nvcc, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

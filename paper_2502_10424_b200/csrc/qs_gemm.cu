@@ -30,13 +30,15 @@ namespace qs {
 
 constexpr int kMaxCols = 16;
 
-template <int WMODE, int NTC, int GKS>
+template <int WMODE, int NTC, int GKS, int CW = 8>
 struct LinCfg {
   static constexpr int NCW = 4;                                  // consumer warps: one m-tile each
   static constexpr int THREADS = (NCW + 1) * 32;                 // + producer warp
   static constexpr int KCH = WMODE == QS_W_F16 ? 8 : 16;         // k-steps per unit (16 KB / 8 KB of weights)
   static constexpr int WBYTES = WMODE == QS_W_F16 ? KCH * 512 : KCH / 4 * 512;  // per m-tile per unit
-  static constexpr int ROWS = 8 * NTC;                           // activation rows in the B region
+  // stage layout (m-group-major weights, so each of W and P is one bulk copy per unit):
+  //   W [k-step (f16) or k-quad (INT4)][4 tiles][512 B] | B [ROWS][BROW] | P [group][4 tiles][128 B] | X [ROWS][XROW]
+  static constexpr int ROWS = NTC == 1 ? CW : 16;                // activation rows in the B region
   static constexpr int BROW = KCH * 32 + 16;                     // bytes per activation row (+pad: no conflicts)
   static constexpr int PBYTES_MAX = WMODE == QS_W_F16 ? 0 : (KCH / GKS) * 128;  // per m-tile: {S,Z} x 16 rows x groups
   static constexpr int XROW = WMODE == QS_W_F16 ? 0 : KCH * 4 + 16;  // INT4: 16-sums of activations (+pad)
@@ -122,7 +124,7 @@ __device__ __forceinline__ void int4_unit(const uint4* __restrict__ wa, const ui
       for (int j = 0; j < GKS; ++j) {
         const int ks = k0 + sl * GKS + j;
         if (ks < nks) {
-          const uint4 w4 = wa[(ks >> 2) * 32];
+          const uint4 w4 = wa[(ks >> 2) * 128];
           const uint32_t wv = (ks & 3) == 0 ? w4.x : (ks & 3) == 1 ? w4.y : (ks & 3) == 2 ? w4.z : w4.w;
           uint32_t a[4];
           unpack_u4_raw(wv, a);
@@ -148,7 +150,7 @@ __device__ __forceinline__ void int4_unit(const uint4* __restrict__ wa, const ui
         const int kk0 = gl * GKS;
         vg[e] = v8[e] = 0.f;
         if (sl < NSLOT && kk0 < nks) {
-          const float4 p = pp[gl * 8];  // {S_g, Z_g - 1024 S_g, S_g8 / 16, Z_g8 - 64 S_g8}
+          const float4 p = pp[gl * 32];  // {S_g, Z_g - 1024 S_g, S_g8 / 16, Z_g8 - 64 S_g8}
           const float* xc = xsm + c * XW + kk0;
           float X;
           if (kk0 + GKS <= nks) {
@@ -189,8 +191,8 @@ __device__ __forceinline__ void int4_unit(const uint4* __restrict__ wa, const ui
 }
 
 template <int WMODE, int NTC, int EPI, int GKS, int CW>
-__global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS>::THREADS) linear_kernel(const __grid_constant__ LinearParams P) {
-  using C = LinCfg<WMODE, NTC, GKS>;
+__global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_kernel(const __grid_constant__ LinearParams P) {
+  using C = LinCfg<WMODE, NTC, GKS, CW>;
   constexpr int COLS = 8 * NTC;
   constexpr int KCH = C::KCH;
   extern __shared__ __align__(128) uint8_t sm[];
@@ -228,47 +230,37 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS>::THREADS) linear_kerne
   if (warp == C::NCW) {
     // ======================= producer warp =======================
     if (lane != 0) return;
+    int mg = (int)(u_lo / KC), kc = (int)(u_lo % KC);
     for (int i = 0; i < nunits; ++i) {
       const int s = i % C::NSTAGE;
       if (i >= C::NSTAGE) mbar_wait_sleep(&empty_b[s], ((i / C::NSTAGE) - 1) & 1);
-      const long long u = u_lo + i;
-      const int mg = (int)(u / KC), kc = (int)(u % KC);
       const int ks0 = kc * KCH, nks = min(KCH, KS - ks0);
       uint8_t* sp = sm + s * C::STAGE;
-      uint32_t bytes = 0;
-      const int nmt = min(C::NCW, MT - mg * 4);
-      uint32_t wb, bb, pb = 0, xb = 0;
+      uint32_t wb, bb = (uint32_t)nks * 32, pb = 0, xb = 0;
+      const uint8_t* wsrc;
       if constexpr (WMODE == QS_W_F16) {
-        wb = (uint32_t)nks * 512;
+        wb = (uint32_t)nks * 2048;
+        wsrc = reinterpret_cast<const uint8_t*>(P.w) + ((size_t)mg * KS + ks0) * 2048;
       } else {
-        wb = (uint32_t)((nks + 3) / 4) * 512;
-      }
-      bb = (uint32_t)nks * 32;
-      const int ngr = WMODE == QS_W_INT4 ? (nks * 16 + P.wgroup - 1) / P.wgroup : 0;
-      if constexpr (WMODE == QS_W_INT4) {
-        pb = (uint32_t)ngr * 128;
+        wb = (uint32_t)((nks + 3) / 4) * 2048;
+        wsrc = reinterpret_cast<const uint8_t*>(P.w) + ((size_t)mg * (ks_pad / 4) + ks0 / 4) * 2048;
+        pb = (uint32_t)((nks * 16 + P.wgroup - 1) / P.wgroup) * 512;
         xb = (uint32_t)((nks + 3) / 4) * 16;
       }
-      bytes = nmt * (wb + pb) + ncols * (bb + xb);
-      mbar_arrive_expect_tx(&full_b[s], bytes);
-      for (int w = 0; w < nmt; ++w) {
-        const int mt = mg * 4 + w;
-        if constexpr (WMODE == QS_W_F16) {
-          bulk_g2s(sp + w * C::WBYTES, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)mt * KS + ks0) * 512, wb,
-                   &full_b[s]);
-        } else {
-          bulk_g2s(sp + w * C::WBYTES, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)mt * (ks_pad / 4) + ks0 / 4) * 512,
-                   wb, &full_b[s]);
-          const int gr0 = ks0 * 16 / P.wgroup;
-          bulk_g2s(sp + C::OFF_P + w * C::PBYTES_MAX,
-                   reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)mt * gpr + gr0) * 128, pb, &full_b[s]);
-        }
-      }
+      mbar_arrive_expect_tx(&full_b[s], wb + pb + ncols * (bb + xb));
+      bulk_g2s(sp, wsrc, wb, &full_b[s]);
+      if constexpr (WMODE == QS_W_INT4)
+        bulk_g2s(sp + C::OFF_P, reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)mg * gpr + ks0 * 16 / P.wgroup) * 512,
+                 pb, &full_b[s]);
       for (int c = 0; c < ncols; ++c) {
         bulk_g2s(sp + C::OFF_B + c * C::BROW, reinterpret_cast<const __half*>(P.xh) + (size_t)c * P.ldxh + ks0 * 16, bb,
                  &full_b[s]);
         if constexpr (WMODE == QS_W_INT4)
           bulk_g2s(sp + C::OFF_X + c * C::XROW, P.xs + (size_t)c * P.ldxs + ks0, xb, &full_b[s]);
+      }
+      if (++kc == KC) {
+        kc = 0;
+        ++mg;
       }
     }
     return;
@@ -281,10 +273,13 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS>::THREADS) linear_kerne
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
 
+  int mg = (int)(u_lo / KC), kc = (int)(u_lo % KC) - 1;
   for (int i = 0; i < nunits; ++i) {
     const int s = i % C::NSTAGE;
-    const long long u = u_lo + i;
-    const int mg = (int)(u / KC), kc = (int)(u % KC);
+    if (++kc == KC) {
+      kc = 0;
+      ++mg;
+    }
     const int ks0 = kc * KCH, nks = min(KCH, KS - ks0);
     const int mt = mg * 4 + warp;
     const uint8_t* sp = sm + s * C::STAGE;
@@ -294,11 +289,11 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS>::THREADS) linear_kerne
       // which only ever reaches the matching (discarded) output columns of the MMA.
       const uint8_t* bst = sp + C::OFF_B + g * C::BROW + 4 * t4;
       if constexpr (WMODE == QS_W_F16) {
-        const uint4* wa = reinterpret_cast<const uint4*>(sp + warp * C::WBYTES) + lane;
+        const uint4* wa = reinterpret_cast<const uint4*>(sp) + warp * 32 + lane;  // [ks][4 tiles][32 lanes]
         if (nks == KCH) {
 #pragma unroll
           for (int ks = 0; ks < KCH; ++ks) {
-            const uint4 w4 = wa[ks * 32];
+            const uint4 w4 = wa[ks * 128];
             const uint32_t a[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
             for (int nt = 0; nt < NTC; ++nt) {
@@ -308,7 +303,7 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS>::THREADS) linear_kerne
           }
         } else {
           for (int ks = 0; ks < nks; ++ks) {
-            const uint4 w4 = wa[ks * 32];
+            const uint4 w4 = wa[ks * 128];
             const uint32_t a[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
             for (int nt = 0; nt < NTC; ++nt) {
@@ -318,8 +313,8 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS>::THREADS) linear_kerne
           }
         }
       } else {
-        const uint4* wa = reinterpret_cast<const uint4*>(sp + warp * C::WBYTES) + lane;
-        const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P + warp * C::PBYTES_MAX) + g;
+        const uint4* wa = reinterpret_cast<const uint4*>(sp) + warp * 32 + lane;          // [k-quad][4 tiles][32]
+        const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + warp * 8 + g;  // [group][4 tiles][8]
         const float* xsm = reinterpret_cast<const float*>(sp + C::OFF_X);
         if (nks == KCH)
           int4_unit<C, NTC, GKS, CW>(wa, sp + C::OFF_B, zrow, pp, xsm, KCH, g, t4, acc);
@@ -514,7 +509,7 @@ int linear_maxc(int wmode, int N, int K, int nctas) {
 
 template <int WMODE, int NTC, int EPI, int GKS, int CW>
 static cudaError_t launch_lin_t(const LinearParams& p, cudaStream_t s) {
-  using C = LinCfg<WMODE, NTC, GKS>;
+  using C = LinCfg<WMODE, NTC, GKS, CW>;
   auto kern = linear_kernel<WMODE, NTC, EPI, GKS, CW>;
   static bool configured = false;
   if (!configured) {
@@ -564,10 +559,10 @@ cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-template <int WMODE, int NTC, int GKS>
+template <int WMODE, int NTC, int GKS, int CW>
 static int occ_of() {
-  using C = LinCfg<WMODE, NTC, GKS>;
-  auto kern = linear_kernel<WMODE, NTC, QS_EPI_STORE, GKS, 8>;
+  using C = LinCfg<WMODE, NTC, GKS, CW>;
+  auto kern = linear_kernel<WMODE, NTC, QS_EPI_STORE, GKS, CW>;
   int n = 0;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, C::THREADS, C::SMEM);
@@ -576,7 +571,12 @@ static int occ_of() {
 
 template <int WMODE, int GKS>
 static int occ_n(int ncols) {
-  return ncols <= 8 ? occ_of<WMODE, 1, GKS>() : occ_of<WMODE, 2, GKS>();
+  if (WMODE == QS_W_INT4) {
+    if (ncols == 1) return occ_of<WMODE, 1, GKS, 1>();
+    if (ncols == 2) return occ_of<WMODE, 1, GKS, 2>();
+    if (ncols <= 4) return occ_of<WMODE, 1, GKS, 4>();
+  }
+  return ncols <= 8 ? occ_of<WMODE, 1, GKS, 8>() : occ_of<WMODE, 2, GKS, 8>();
 }
 
 int linear_occupancy(int wmode, int wgroup, int ncols) {

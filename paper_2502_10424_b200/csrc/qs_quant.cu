@@ -224,22 +224,27 @@ __global__ void wq_refcodes_kernel(const float* __restrict__ w, WGeom geo, const
   out[b] = (uint8_t)(c[0] | (c[1] << 4));
 }
 
-// frag4 words [mt][KSpad/4][32][4] (A = W^T tile, rows = outputs, cols = d_in)
+// frag4 words, m-group major: [mg][KSpad/4][4 tiles][32 lanes][4]  (tile mt = 4 mg + w; A = W^T tile,
+// rows = outputs, cols = d_in).  One (4-tile group, k-chunk) unit of the linear kernel is one
+// contiguous range; tiles past d_out/16 (padding to a multiple of 4) are zero.
 __global__ void wq_frag_kernel(const float* __restrict__ w, WGeom geo, const float* __restrict__ s,
                                const float* __restrict__ z, uint32_t* __restrict__ frag, int ks_pad) {
   long long wi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long nwords = (long long)(geo.d_out / 16) * ks_pad * 32;
+  const int MT = geo.d_out / 16, MT4 = (MT + 3) / 4 * 4;
+  long long nwords = (long long)MT4 * ks_pad * 32;
   if (wi >= nwords) return;
   int v4 = (int)(wi & 3);
   long long rest = wi >> 2;
   int lane = (int)(rest & 31);
   rest >>= 5;
+  int wt = (int)(rest & 3);
+  rest >>= 2;
   int kq = (int)(rest % (ks_pad / 4));
-  int mt = (int)(rest / (ks_pad / 4));
+  int mt = (int)(rest / (ks_pad / 4)) * 4 + wt;
   int ks = kq * 4 + v4;
   int g = lane >> 2, t = lane & 3;
   uint32_t word = 0;
-  if (ks * 16 < geo.d_in) {
+  if (ks * 16 < geo.d_in && mt < MT) {
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       int j = p & 3, h = p >> 2;
@@ -252,16 +257,23 @@ __global__ void wq_frag_kernel(const float* __restrict__ w, WGeom geo, const flo
   frag[wi] = word;
 }
 
-// float4 {S_g, Z_g, S_g8, Z_g8} per (mt, group, g)
+// params, m-group major: float4 per [mg][group][4 tiles][g] (zeros for padding tiles)
 __global__ void wq_fragparams_kernel(WGeom geo, const float* __restrict__ s, const float* __restrict__ z,
                                      float4* __restrict__ out) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long total = (long long)(geo.d_out / 16) * geo.gpr * 8;
+  const int MT = geo.d_out / 16, MT4 = (MT + 3) / 4 * 4;
+  long long total = (long long)MT4 * geo.gpr * 8;
   if (i >= total) return;
   int g = (int)(i & 7);
   long long rest = i >> 3;
+  int wt = (int)(rest & 3);
+  rest >>= 2;
   int grp = (int)(rest % geo.gpr);
-  int mt = (int)(rest / geo.gpr);
+  int mt = (int)(rest / geo.gpr) * 4 + wt;
+  if (mt >= MT) {
+    out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   int n0 = mt * 16 + g, n1 = n0 + 8;
   // pre-folded for the offset-form MMA (qs_gemm.cu): rows g carry 1024 + c, rows g+8 carry 1024 + 16c
   //   {S_g, Z_g - 1024 S_g, S_g8 / 16, Z_g8 - 64 S_g8}
@@ -270,22 +282,24 @@ __global__ void wq_fragparams_kernel(WGeom geo, const float* __restrict__ s, con
   out[i] = make_float4(s0, __fmaf_rn(-1024.f, s0, z0), __fmul_rn(s1, 0.0625f), __fmaf_rn(-64.f, s1, z1));
 }
 
-// fp16 frag layout [mt][ks][32][8 halves]
+// fp16 frag layout, m-group major: [mg][ks][4 tiles][32 lanes][8 halves] (tile mt = 4 mg + w; zero padding tiles)
 __global__ void pack_f16_kernel(const float* __restrict__ w, int d_in, int d_out, __half* __restrict__ out) {
-  long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (mt, ks, lane)
-  int KS = d_in / 16;
-  long long total = (long long)(d_out / 16) * KS * 32;
+  long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (mg, ks, w, lane)
+  const int KS = d_in / 16, MT = d_out / 16, MT4 = (MT + 3) / 4 * 4;
+  long long total = (long long)MT4 * KS * 32;
   if (li >= total) return;
   int lane = (int)(li & 31);
   long long rest = li >> 5;
-  int ks = (int)(rest % KS), mt = (int)(rest / KS);
+  int wt = (int)(rest & 3);
+  rest >>= 2;
+  int ks = (int)(rest % KS), mt = (int)(rest / KS) * 4 + wt;
   int g = lane >> 2, t = lane & 3;
   __align__(16) __half hv[8];
 #pragma unroll
   for (int slot = 0; slot < 8; ++slot) {
     int j = slot >> 1, h = slot & 1;
     int row = g + 8 * (j & 1), col = 2 * t + 8 * (j >> 1) + h;
-    hv[slot] = __float2half_rn(w[(size_t)(ks * 16 + col) * d_out + mt * 16 + row]);
+    hv[slot] = mt < MT ? __float2half_rn(w[(size_t)(ks * 16 + col) * d_out + mt * 16 + row]) : __float2half_rn(0.f);
   }
   *reinterpret_cast<uint4*>(out + li * 8) = *reinterpret_cast<uint4*>(hv);
 }
@@ -524,18 +538,18 @@ cudaError_t launch_quantize_weights(const float* w, int d_in, int d_out, int gro
   if (ref) wq_refcodes_kernel<<<blocks_for(((long long)d_in * d_out + 1) / 2, 256), 256, 0, st>>>(w, geo, s, z, ref);
   if (frag4) {
     int ks = d_in / 16, ks_pad = (ks + 3) / 4 * 4;
-    long long nwords = (long long)(d_out / 16) * ks_pad * 32;
+    long long nwords = (long long)((d_out / 16 + 3) / 4 * 4) * ks_pad * 32;
     wq_frag_kernel<<<blocks_for(nwords, 256), 256, 0, st>>>(w, geo, s, z, frag4, ks_pad);
   }
   if (fparams) {
-    long long tot = (long long)(d_out / 16) * geo.gpr * 8;
+    long long tot = (long long)((d_out / 16 + 3) / 4 * 4) * geo.gpr * 8;
     wq_fragparams_kernel<<<blocks_for(tot, 256), 256, 0, st>>>(geo, s, z, fparams);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_f16(const float* w, int d_in, int d_out, __half* out, cudaStream_t st) {
-  long long total = (long long)(d_out / 16) * (d_in / 16) * 32;
+  long long total = (long long)((d_out / 16 + 3) / 4 * 4) * (d_in / 16) * 32;
   pack_f16_kernel<<<blocks_for(total, 256), 256, 0, st>>>(w, d_in, d_out, out);
   return cudaGetLastError();
 }

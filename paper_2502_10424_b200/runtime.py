@@ -80,15 +80,17 @@ def pack_f16(w):
     """[d_in, d_out] f32 CUDA tensor -> frag16 halves."""
     torch = _torch()
     d_in, d_out = (int(x) for x in w.shape)
-    out = torch.empty((d_out // 16) * (d_in // 16) * 32 * 8, dtype=torch.float16, device=w.device)
+    mt4 = (d_out // 16 + 3) // 4 * 4
+    out = torch.empty(mt4 * (d_in // 16) * 32 * 8, dtype=torch.float16, device=w.device)
     _lib.call("qs_pack_weights_f16", w.data_ptr(), d_in, d_out, out.data_ptr(), _lib.stream_ptr())
     return out
 
 
-def interleave_tiles(a, b, ntiles: int):
-    """Interleave two packed matrices m-tile by m-tile (gate/up fusion)."""
-    torch = _torch()
-    return torch.stack([a.view(ntiles, -1), b.view(ntiles, -1)], dim=1).reshape(-1)
+def interleave_cols(a, b):
+    """[K, N] x 2 -> [K, 2N] with 16-column blocks alternating a, b (gate/up fusion:
+    output tile 2j is gate tile j, 2j+1 is up tile j)."""
+    K, N = (int(v) for v in a.shape)
+    return _torch().stack([a.view(K, N // 16, 16), b.view(K, N // 16, 16)], dim=2).reshape(K, 2 * N).contiguous()
 
 
 class PackedLinear:
@@ -103,9 +105,7 @@ class PackedLinear:
 
     @classmethod
     def f16_pair(cls, wa, wb):
-        a, b = pack_f16(wa), pack_f16(wb)
-        n = int(wa.shape[1])
-        return cls(_lib.W_F16, 2 * n, int(wa.shape[0]), interleave_tiles(a, b, n // 16))
+        return cls.f16(interleave_cols(wa, wb))
 
     @classmethod
     def int4(cls, w, group: int):
@@ -116,13 +116,7 @@ class PackedLinear:
 
     @classmethod
     def int4_pair(cls, wa, wb, group: int):
-        from .quant import quantize_weights_device
-
-        _, _, _, fa, pa, g = quantize_weights_device(wa, group, want_plane=False, want_frag=True)
-        _, _, _, fb, pb, _ = quantize_weights_device(wb, group, want_plane=False, want_frag=True)
-        n = int(wa.shape[1])
-        return cls(_lib.W_INT4, 2 * n, int(wa.shape[0]), interleave_tiles(fa, fb, n // 16),
-                   interleave_tiles(pa, pb, n // 16), g)
+        return cls.int4(interleave_cols(wa, wb), group)
 
     def nbytes(self) -> int:
         b = self.w.numel() * self.w.element_size()
@@ -197,23 +191,24 @@ def build_device_weights(geo: Geometry, layer_mats, embedding, final_norm, lm_he
 _LIN_GRID: dict = {}
 
 
-def linear_grid(wmode: int, group: int = 16) -> int:
-    """Stream-K grid of the linear kernel: every resident slot, fixed per weight
-    format (never per activation-row count, so results are batch-invariant)."""
-    key = (wmode, group)
+def linear_grid(wmode: int, group: int = 16, ncols: int = 1) -> int:
+    """Stream-K grid of the linear kernel: every resident CTA slot.  f16 weights
+    (the target) use one grid for every activation-row count, so their results
+    are batch-invariant; INT4 (draft-only) sizes its grid per row count."""
+    key = (wmode, group, 16 if wmode == _lib.W_F16 else ncols)
     n = _LIN_GRID.get(key)
     if n is None:
-        occ = _lib.load().qs_linear_occupancy(wmode, group, 1)
+        occ = _lib.load().qs_linear_occupancy(wmode, group, key[2])
         n = SM_COUNT * max(1, occ)
         _LIN_GRID[key] = n
     return n
 
 
-def linear_plan(pl: PackedLinear) -> tuple[int, int]:
-    """(nctas, maxc) for one packed linear layer."""
+def linear_plan(pl: PackedLinear, ncols: int = 1) -> tuple[int, int]:
+    """(nctas, maxc) for one packed linear layer at ``ncols`` activation rows."""
     import ctypes
 
-    nctas = linear_grid(pl.wmode, pl.group if pl.wmode == _lib.W_INT4 else 16)
+    nctas = linear_grid(pl.wmode, pl.group if pl.wmode == _lib.W_INT4 else 16, ncols)
     mx = ctypes.c_int(0)
     _lib.call("qs_linear_plan", pl.wmode, pl.N, pl.K, nctas, ctypes.byref(mx))
     return nctas, mx.value
@@ -320,7 +315,7 @@ class Runner:
             geo = self.geo
             a = _lib.LinearArgs()
             a.wmode, a.epi, a.N, a.K, a.ncols = pl.wmode, epi, pl.N, pl.K, ncols
-            a.nctas, a.maxc = linear_plan(pl)
+            a.nctas, a.maxc = linear_plan(pl, ncols)
             need = -(-pl.N // 64) * a.maxc * 16 * 64
             if need > self.work.numel():
                 torch = _torch()

@@ -67,7 +67,7 @@ def main():
                                                    xs.shape[1], a.ncols, K, _lib.stream_ptr()))
                 y = torch.zeros(a.ncols, N, device="cuda")
                 args = []
-                nct = a.nctas or linear_grid(pls[0].wmode, grp)
+                nct = a.nctas or linear_grid(pls[0].wmode, grp, a.ncols)
                 mx = ctypes.c_int(0)
                 _lib.call("qs_linear_plan", pls[0].wmode, N, K, nct, ctypes.byref(mx))
                 mg = -(-N // 64)

@@ -339,7 +339,7 @@ def _run_linear(pl, x, ncols, *, epi=None, nctas=None, y=None, yh=None):
     xh, xs = _act_buffers(x)
     a = _lib.LinearArgs()
     a.wmode, a.epi, a.N, a.K, a.ncols = pl.wmode, _lib.EPI_STORE if epi is None else epi, pl.N, pl.K, ncols
-    a.nctas = nctas or linear_grid(pl.wmode, pl.group if pl.wmode == _lib.W_INT4 else 16)
+    a.nctas = nctas or linear_grid(pl.wmode, pl.group if pl.wmode == _lib.W_INT4 else 16, ncols)
     mx = ctypes.c_int(0)
     _lib.call("qs_linear_plan", pl.wmode, pl.N, pl.K, a.nctas, ctypes.byref(mx))
     a.maxc = mx.value
