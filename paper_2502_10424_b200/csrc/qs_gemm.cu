@@ -48,7 +48,8 @@ struct LinCfg {
   static constexpr int STAGE = (OFF_X + ROWS * XROW + 127) / 128 * 128;
   static constexpr int NSTAGE = 4;
   static constexpr int ZROW = WMODE == QS_W_F16 ? 0 : BROW;      // zero B row (INT4 group slots)
-  static constexpr int SMEM = NSTAGE * STAGE + 64 * ROWS * 4 + ZROW + 2 * NSTAGE * 8 + 16;
+  static constexpr int YCOLS = 8 * NTC;                          // ysm tile [64][YCOLS] f32 (all MMA columns)
+  static constexpr int SMEM = NSTAGE * STAGE + 64 * YCOLS * 4 + ZROW + 2 * NSTAGE * 8 + 16;
 };
 
 // mma.sync without `volatile` (pure: lets ptxas interleave the group's MMAs with unpacking)
