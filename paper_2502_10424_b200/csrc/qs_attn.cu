@@ -77,9 +77,8 @@ struct AttnCfg {
   static constexpr int BQF_WORDS = KS * NT * 64;          // raw-query fragments for fp16 chunks
   static constexpr int PW_HALVES = NT * 8 * PSTRIDE;
   static constexpr int VPAD = 2 * NQ <= 8 ? 8 : 2 * NQ <= 16 ? 16 : 32;      // reduce-scatter width
-  static constexpr int PSCR_FLOATS = 2 * 8 * VPAD * (NPW > 0 ? NPW : 1);    // producer partial sums
   static constexpr int SMEM =
-      REGION + BQF_WORDS * 4 + NQ * HD * 4 + NCW * PW_HALVES * 2 + PSCR_FLOATS * 4 + 3 * 8 * 8 + 16;
+      REGION + BQF_WORDS * 4 + NQ * HD * 4 + NCW * PW_HALVES * 2 + 3 * 8 * 8 + 16;
 };
 
 __device__ __forceinline__ int swz16(int chunk, int row, int nchunk) {
@@ -289,7 +288,7 @@ __device__ __forceinline__ void fp16_region(uint8_t* region, uint32_t* bqf, cons
 // quantised region: producer warp + 8 consumer warps
 // ---------------------------------------------------------------------------
 template <typename C, int HD, int NT, int MODE>
-__device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, const float* q_s, __half* pw, float* pscr, int nq,
+__device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, const float* q_s, __half* pw, int nq,
                                              int seq, int head, int n_tok, int c_begin, int c_end,
                                              const AttnParams& P, Softmax (&st)[NT], float (&acc)[C::KS][NT][4]) {
   constexpr int KS = C::KS, NQ = C::NQ, S = C::NSTAGE;
@@ -334,34 +333,34 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       bulk_g2s(sp + C::KP_OFF, kp + (size_t)b0 * HD, kpb, &tma_b[s]);
       bulk_g2s(sp + C::VP_OFF, vp + (size_t)b0 * G, vpb, &tma_b[s]);
     };
-    // the channel pairs this lane folds: cp = pwid*32 + lane + 32*NPW*k; query values kept in registers
+    // Producer warp p folds whole chunks j = p (mod NPW) on its own (no inter-warp
+    // synchronisation: the per-chunk fold is a latency chain, so independent warps
+    // overlap it), then refills the stage of its previous chunk once the consumers
+    // have released it.  Lane l folds channel pairs cp = l + 32 k.
     constexpr int NPW = C::NPW;
-    constexpr int CPL = (HD / 2 + 32 * NPW - 1) / (32 * NPW);
-    constexpr bool QREG = NQ <= 8;  // wide launches re-read shared memory instead (registers)
+    constexpr int CPL = (HD / 2 + 31) / 32;
+    constexpr bool QREG = false;  // queries re-read from shared memory (keeps the 2-CTA/SM register budget)
     float2 qr[QREG ? NQ : 1][CPL];
     if constexpr (QREG) {
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
-          const int cp = pwid * 32 + lane + 32 * NPW * k;
+          const int cp = lane + 32 * k;
           qr[q][k] = cp < HD / 2 ? *reinterpret_cast<const float2*>(q_s + q * HD + 2 * cp) : make_float2(0.f, 0.f);
         }
     }
     if (pwid == 0 && lane == 0)
       for (int i = 0; i < S && i < nchunk; ++i) issue(i);
-    // chunk j is prepared (B fragments + biases) while the consumers work on
-    // chunk j-1; then the stage of chunk j-1 is refilled with chunk j-1+S
-    for (int j = 0; j < nchunk; ++j) {
+    for (int j = pwid; j < nchunk; j += NPW) {
       const int s = j % S;
       uint8_t* sp = stage_ptr(s);
-      mbar_wait_sleep(&tma_b[s], (j / S) & 1);
+      mbar_wait(&tma_b[s], (j / S) & 1);
       const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + j) * QS_CHUNK_Q);
       const int nbl = (ntok_chunk + G - 1) >> lgG;
       const float2* kps = reinterpret_cast<const float2*>(sp + C::KP_OFF);
       uint32_t* bqb = reinterpret_cast<uint32_t*>(sp + C::BQ_OFF);
       float* bias = reinterpret_cast<float*>(sp + C::BIAS_OFF);
-      float* scr = pscr + (j & 1) * (NPW * 8 * C::VPAD);  // per-warp partial sums (double-buffered)
       // q'_c = q_c * S_c as f16 hi/lo B fragments; per (block, query): bias = sum q Z - offset * sum(q').
       // All queries are processed together so the warp reductions overlap (ILP), not serialise.
       for (int bl = 0; bl < ((P.dbg & 2) ? 0 : nbl); ++bl) {
@@ -370,7 +369,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         for (int q = 0; q < NQ; ++q) zs[q] = bs[q] = 0.f;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
-          const int cp = pwid * 32 + lane + 32 * NPW * k;
+          const int cp = lane + 32 * k;
           if (cp < HD / 2) {
             const float4 pz = *reinterpret_cast<const float4*>(kps + bl * HD + 2 * cp);  // (S0, Z0, S1, Z1)
             const float s0 = pz.x * kvs, s1 = pz.z * kvs;
@@ -420,33 +419,24 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         float tot = vals[0];
 #pragma unroll
         for (int o = 16 >> LV; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        const int idx = (lane >> (5 - LV)) & (V - 1);  // which of the 2*NQ sums this lane holds
-        if ((lane & ((1 << (5 - LV)) - 1)) == 0) scr[(pwid * 8 + bl) * V + idx] = tot;
-        if constexpr (NPW > 1) {
-          // all producer warps: partial sums written (and fragments stored) before warp 0 combines
-          asm volatile("bar.sync 1, %0;" ::"n"(NPW * 32));
-        } else {
-          __syncwarp();
-        }
-        if (pwid == 0 && lane < nq) {
-          float z = 0.f, b = 0.f;
-#pragma unroll
-          for (int w = 0; w < NPW; ++w) {
-            z += scr[(w * 8 + bl) * V + lane];
-            b += scr[(w * 8 + bl) * V + NQ + lane];
-          }
-          // draft rows g carry 1024 + c, rows g+8 carry (1024 + 16c) (scaled by 1/16 after the MMA);
-          // target rows carry 1032 + (16 c_u + c_l)
+        // lanes [idx << (5-LV), (idx+1) << (5-LV)) now hold sum idx (idx < NQ: zs, else bs)
+        const int qq = lane < nq ? lane : 0;
+        const float z = __shfl_sync(0xffffffffu, tot, qq << (5 - LV));
+        const float b = __shfl_sync(0xffffffffu, tot, (NQ + qq) << (5 - LV));
+        // draft rows g carry 1024 + c, rows g+8 carry (1024 + 16c) (scaled by 1/16 after the MMA);
+        // target rows carry 1032 + (16 c_u + c_l)
+        if (lane < nq) {
           bias[(bl * NQ + lane) * 2 + 0] = z - (TGT ? 1032.f : 1024.f) * b;
           bias[(bl * NQ + lane) * 2 + 1] = z - (TGT ? 1032.f : 64.f) * b;
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_b[s]);  // full barrier counts one arrival per producer warp
-      // refill the stage consumed by chunk j-1
-      if (pwid == 0 && j >= 1 && j - 1 + S < nchunk) {
-        mbar_wait_sleep(&empty_b[(j - 1) % S], ((j - 1) / S) & 1);
-        if (lane == 0) issue(j - 1 + S);
+      if (lane == 0) mbar_arrive(&full_b[s]);
+      // refill the stage of this warp's previous chunk (every chunk >= S is issued exactly once)
+      const int jp = j - NPW;
+      if (jp >= 0 && jp + S < nchunk) {
+        mbar_wait(&empty_b[jp % S], (jp / S) & 1);
+        if (lane == 0) issue(jp + S);
       }
     }
     return;
@@ -458,7 +448,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   for (int i = 0; i < nchunk; ++i) {
     const int s = i % S;
     const uint8_t* sp = stage_ptr(s);
-    mbar_wait_sleep(&full_b[s], (i / S) & 1);
+    mbar_wait(&full_b[s], (i / S) & 1);
     const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
     const bool live = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
     if (live) {
@@ -544,8 +534,7 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
   uint32_t* bqf = reinterpret_cast<uint32_t*>(smem + C::REGION);      // [KS][NT][32][2]
   float* q_s = reinterpret_cast<float*>(bqf + C::BQF_WORDS);          // [NQ][HD]
   __half* pw_all = reinterpret_cast<__half*>(q_s + NQ * HD);           // [NCW][PW_HALVES]
-  float* pscr = reinterpret_cast<float*>(pw_all + NCW * C::PW_HALVES);  // producer partial sums
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pscr + C::PSCR_FLOATS);  // tma[8] full[8] empty[8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pw_all + NCW * C::PW_HALVES);  // tma[8] full[8] empty[8]
   int* ticket_s = reinterpret_cast<int*>(bars + 24);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -578,7 +567,7 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
   if (tid == 0) {
     for (int i = 0; i < 8; ++i) {
       mbar_init(&bars[i], 1);         // TMA transactions
-      mbar_init(&bars[8 + i], C::NPW > 0 ? C::NPW : 1);  // producers -> consumers
+      mbar_init(&bars[8 + i], 1);     // producer (one warp per chunk) -> consumers
       mbar_init(&bars[16 + i], NCW);  // consumers -> producer
     }
     fence_mbar_init();
@@ -644,7 +633,7 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
   bool offset_pv = false;
   if (region_kind == 0) {
     if constexpr (C::QUANT) {
-      if (c_end > c_begin) quant_region<C, HD, NT, MODE>(region, bars, q_s, pw, pscr, nq, seq, head, n_tok, c_begin, c_end, P, st, acc);
+      if (c_end > c_begin) quant_region<C, HD, NT, MODE>(region, bars, q_s, pw, nq, seq, head, n_tok, c_begin, c_end, P, st, acc);
       offset_pv = true;
     }
   } else if (c_end > c_begin) {
