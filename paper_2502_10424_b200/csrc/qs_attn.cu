@@ -284,6 +284,36 @@ __device__ __forceinline__ void fp16_region(uint8_t* region, uint32_t* bqf, cons
   cp_async_wait<0>();
 }
 
+// TMA bulk copies of quantised chunk i of this CTA's range (planes + key/value params)
+// into ring stage i % NSTAGE; completion is counted on tma_b[stage].  Reads only
+// blocks below n_blocks, which no kernel of a decode forward modifies, so the
+// first NSTAGE chunks are issued before the grid dependency resolves (PDL).
+template <typename C, int HD, int MODE>
+__device__ __forceinline__ void quant_issue(const AttnParams& P, uint8_t* region, uint64_t* tma_b, int seq, int head,
+                                            int n_blocks, int c_begin, int i) {
+  constexpr bool TGT = MODE == MODE_QTARGET;
+  const int G = P.G;
+  const int bpc = QS_CHUNK_Q / G;
+  const size_t plane_blk = (size_t)G * HD / 2;
+  const size_t ph = ((size_t)seq * P.plane_seq_stride) + (size_t)head * P.plane_head_stride;
+  const float2* kp = reinterpret_cast<const float2*>(P.kp) + (size_t)seq * P.kp_seq_stride + (size_t)head * P.kp_head_stride;
+  const float2* vp = reinterpret_cast<const float2*>(P.vp) + (size_t)seq * P.vp_seq_stride + (size_t)head * P.vp_head_stride;
+  const int c = c_begin + i, s = i % C::NSTAGE;
+  uint8_t* sp = region + s * C::QSTAGE;
+  const int b0 = c * bpc, nb = min(bpc, n_blocks - b0);
+  const uint32_t pbytes = (uint32_t)(nb * plane_blk);
+  const uint32_t kpb = (uint32_t)(nb * HD * 8), vpb = (uint32_t)(nb * G * 8);
+  mbar_arrive_expect_tx(&tma_b[s], pbytes * C::NPLANE + kpb + vpb);
+  bulk_g2s(sp, P.ku + ph + b0 * plane_blk, pbytes, &tma_b[s]);
+  bulk_g2s(sp + C::PLANE_CHUNK, P.vu + ph + b0 * plane_blk, pbytes, &tma_b[s]);
+  if constexpr (TGT) {
+    bulk_g2s(sp + 2 * C::PLANE_CHUNK, P.kl + ph + b0 * plane_blk, pbytes, &tma_b[s]);
+    bulk_g2s(sp + 3 * C::PLANE_CHUNK, P.vl + ph + b0 * plane_blk, pbytes, &tma_b[s]);
+  }
+  bulk_g2s(sp + C::KP_OFF, kp + (size_t)b0 * HD, kpb, &tma_b[s]);
+  bulk_g2s(sp + C::VP_OFF, vp + (size_t)b0 * G, vpb, &tma_b[s]);
+}
+
 // ---------------------------------------------------------------------------
 // quantised region: producer warp + 8 consumer warps
 // ---------------------------------------------------------------------------
@@ -310,29 +340,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   if (warp >= C::NCW) {
     // ======================= producer warps (NPW) =======================
     const int pwid = warp - C::NCW;
-    const size_t ph = ((size_t)seq * P.plane_seq_stride) + (size_t)head * P.plane_head_stride;
-    const uint8_t* ku = P.ku + ph;
-    const uint8_t* vu = P.vu + ph;
-    const uint8_t* kl = TGT ? P.kl + ph : nullptr;
-    const uint8_t* vl = TGT ? P.vl + ph : nullptr;
-    const float2* kp = reinterpret_cast<const float2*>(P.kp) + (size_t)seq * P.kp_seq_stride + (size_t)head * P.kp_head_stride;
-    const float2* vp = reinterpret_cast<const float2*>(P.vp) + (size_t)seq * P.vp_seq_stride + (size_t)head * P.vp_head_stride;
-    auto issue = [&](int i) {
-      const int c = c_begin + i, s = i % S;
-      uint8_t* sp = stage_ptr(s);
-      const int b0 = c * bpc, nb = min(bpc, n_blocks - b0);
-      const uint32_t pbytes = (uint32_t)(nb * plane_blk);
-      const uint32_t kpb = (uint32_t)(nb * HD * 8), vpb = (uint32_t)(nb * G * 8);
-      mbar_arrive_expect_tx(&tma_b[s], pbytes * C::NPLANE + kpb + vpb);
-      bulk_g2s(sp, ku + b0 * plane_blk, pbytes, &tma_b[s]);
-      bulk_g2s(sp + C::PLANE_CHUNK, vu + b0 * plane_blk, pbytes, &tma_b[s]);
-      if constexpr (TGT) {
-        bulk_g2s(sp + 2 * C::PLANE_CHUNK, kl + b0 * plane_blk, pbytes, &tma_b[s]);
-        bulk_g2s(sp + 3 * C::PLANE_CHUNK, vl + b0 * plane_blk, pbytes, &tma_b[s]);
-      }
-      bulk_g2s(sp + C::KP_OFF, kp + (size_t)b0 * HD, kpb, &tma_b[s]);
-      bulk_g2s(sp + C::VP_OFF, vp + (size_t)b0 * G, vpb, &tma_b[s]);
-    };
+    auto issue = [&](int i) { quant_issue<C, HD, MODE>(P, region, tma_b, seq, head, n_blocks, c_begin, i); };
     // Producer warp p folds whole chunks j = p (mod NPW) on its own (no inter-warp
     // synchronisation: the per-chunk fold is a latency chain, so independent warps
     // overlap it), then refills the stage of its previous chunk once the consumers
@@ -350,8 +358,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
           qr[q][k] = cp < HD / 2 ? *reinterpret_cast<const float2*>(q_s + q * HD + 2 * cp) : make_float2(0.f, 0.f);
         }
     }
-    if (pwid == 0 && lane == 0)
-      for (int i = 0; i < S && i < nchunk; ++i) issue(i);
+    // chunks 0..S-1 were issued by the kernel prologue (before pdl_wait)
     for (int j = pwid; j < nchunk; j += NPW) {
       const int s = j % S;
       uint8_t* sp = stage_ptr(s);
@@ -547,16 +554,6 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
   const int nq = min(NQ, P.n_queries - qg * NQ);
   __half* pw = pw_all + min(warp, NCW - 1) * C::PW_HALVES;
 
-  for (int i = tid; i < NQ * HD; i += NTH) {
-    const int q = i / HD, c = i % HD;
-    float v = 0.f;
-    if (q < nq) {
-      const int qgl = qg * NQ + q;
-      const int t = qgl / P.r, j = qgl - t * P.r;
-      v = P.q[((size_t)seq * P.T + t) * P.q_row_stride + (size_t)(head * P.r + j) * HD + c];
-    }
-    q_s[i] = v;
-  }
   if constexpr (C::QUANT) {
     // per-stage B fragment buffers: the unused query columns stay zero
     for (int s = 0; s < C::NSTAGE; ++s) {
@@ -572,9 +569,8 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
     }
     fence_mbar_init();
   }
-  __syncthreads();
 
-  // ---- region of this CTA ----
+  // ---- region of this CTA (lengths are not written by the previous kernel: QKV linear) ----
   const int fp1_len = P.fp1_len ? P.fp1_len[seq] : 0;
   const int fp2_base = P.fp2_len ? P.fp2_len[seq] + P.row_offset : 0;
   int region_kind;  // 0 quant, 1 fp16 main, 2 fp1, 3 fp2
@@ -618,6 +614,27 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
     c_begin = 0;
     c_end = fk ? (n_tok + C::CF - 1) / C::CF : 0;
   }
+
+  __syncthreads();  // barriers initialised, fragment buffers zeroed
+  if constexpr (C::QUANT) {
+    // PDL: the first ring stages of packed planes stream in before the grid dependency resolves
+    if (region_kind == 0 && warp == NCW && lane == 0)
+      for (int i = 0; i < C::NSTAGE && i < c_end - c_begin; ++i)
+        quant_issue<C, HD, MODE>(P, region, bars, seq, head, P.n_blocks[seq], c_begin, i);
+  }
+  pdl_wait();
+  pdl_trigger();
+  for (int i = tid; i < NQ * HD; i += NTH) {
+    const int q = i / HD, c = i % HD;
+    float v = 0.f;
+    if (q < nq) {
+      const int qgl = qg * NQ + q;
+      const int t = qgl / P.r, j = qgl - t * P.r;
+      v = P.q[((size_t)seq * P.T + t) * P.q_row_stride + (size_t)(head * P.r + j) * HD + c];
+    }
+    q_s[i] = v;
+  }
+  __syncthreads();
 
   Softmax st[NT];
 #pragma unroll
@@ -732,8 +749,7 @@ static cudaError_t launch_attn_t(const AttnParams& p, cudaStream_t stream) {
     configured = true;
   }
   dim3 grid(p.Hkv * p.n_qgroups, p.n_main + 2, p.B);
-  kern<<<grid, C::THREADS, C::SMEM, stream>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, dim3(C::THREADS), C::SMEM, stream, p);
 }
 
 template <int HD, int MODE>

@@ -2,6 +2,7 @@
 // mirrors the reference's typed errors, then stream-ordered kernel launches.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "qs_api_internal.h"

@@ -201,6 +201,37 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// programmatic dependent launch (PDL).  Every hot-loop kernel is launched with
+// programmatic stream serialisation: its CTAs may start while the previous
+// kernel is still running.  Protocol (keeps the overlap window one kernel deep):
+//   1. before pdl_wait(): only shared-memory setup and reads of data no kernel
+//      on the decode path writes (weights, quantised blocks below n_blocks);
+//   2. pdl_wait() in every thread (returns once the previous grid completed and
+//      its memory is visible);
+//   3. pdl_trigger() right after: lets the next kernel's CTAs be scheduled.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+bool pdl_enabled();  // QS_PDL=0 in the environment disables it (A/B measurements)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -47,9 +47,8 @@ struct LinCfg {
   static constexpr int OFF_X = OFF_P + NCW * PBYTES_MAX;
   static constexpr int STAGE = (OFF_X + ROWS * XROW + 127) / 128 * 128;
   static constexpr int NSTAGE = 4;
-  static constexpr int ZROW = WMODE == QS_W_F16 ? 0 : BROW;      // zero B row (INT4 group slots)
   static constexpr int YCOLS = 8 * NTC;                          // ysm tile [64][YCOLS] f32 (all MMA columns)
-  static constexpr int SMEM = NSTAGE * STAGE + 64 * YCOLS * 4 + ZROW + 2 * NSTAGE * 8 + 16;
+  static constexpr int SMEM = NSTAGE * STAGE + 64 * YCOLS * 4 + 2 * NSTAGE * 8 + 16;
 };
 
 // mma.sync without `volatile` (pure: lets ptxas interleave the group's MMAs with unpacking)
@@ -100,7 +99,7 @@ __host__ __device__ __forceinline__ long long cta_of_unit(long long u, long long
 // accumulator thus carries 8/CW groups, and the scale/zero-point epilogue runs once per window
 // of 8/CW groups instead of once per group; the slot partials are then summed across the quad.
 template <class C, int NTC, int GKS, int CW>
-__device__ __forceinline__ void int4_unit(const uint4* __restrict__ wa, const uint8_t* bbase, const uint8_t* zrow,
+__device__ __forceinline__ void int4_unit(const uint4* __restrict__ wa, const uint8_t* bbase,
                                           const float4* pp, const float* xsm, const int nks, const int g,
                                           const int t4, float (&acc)[NTC][4]) {
   static_assert(NTC == 1 || CW == 8, "two n-tiles only with one group per window");
@@ -114,13 +113,21 @@ __device__ __forceinline__ void int4_unit(const uint4* __restrict__ wa, const ui
   for (int w = 0; w < KCH / WIN; ++w) {
     const int k0 = w * WIN;
     if (k0 >= nks) break;
-    float D[NTC][4];
+    // two accumulator chains (even / odd k-steps of the window) halve the dependent-MMA depth
+    float D2[2][NTC][4];
 #pragma unroll
-    for (int sl = 0; sl < NSLOT; ++sl) {
-      const uint8_t* brow[NTC];
+    for (int c2 = 0; c2 < 2; ++c2)
 #pragma unroll
       for (int nt = 0; nt < NTC; ++nt)
-        brow[nt] = (my_slot == sl ? bbase + (nt * 8 + g % CW) * C::BROW : zrow) + 4 * t4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) D2[c2][nt][e] = 0.f;
+#pragma unroll
+    for (int sl = 0; sl < NSLOT; ++sl) {
+      // lanes of other slots feed zeros (no load: a shared zero row would bank-conflict with the activations)
+      const bool mine = my_slot == sl;
+      const uint8_t* brow[NTC];
+#pragma unroll
+      for (int nt = 0; nt < NTC; ++nt) brow[nt] = bbase + (nt * 8 + g % CW) * C::BROW + 4 * t4;
 #pragma unroll
       for (int j = 0; j < GKS; ++j) {
         const int ks = k0 + sl * GKS + j;
@@ -131,15 +138,22 @@ __device__ __forceinline__ void int4_unit(const uint4* __restrict__ wa, const ui
           unpack_u4_raw(wv, a);
 #pragma unroll
           for (int nt = 0; nt < NTC; ++nt) {
-            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32);
-            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32 + 16);
-            if (sl == 0 && j == 0) mma_zc(D[nt], a, b0, b1);
-            else mma_acc(D[nt], a, b0, b1);
+            uint32_t b0 = 0u, b1 = 0u;
+            if (mine) {
+              b0 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32);
+              b1 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32 + 16);
+            }
+            mma_acc(D2[(sl * GKS + j) & 1][nt], a, b0, b1);
           }
         }
       }
     }
     // ---- window epilogue: scale + zero point per (row, column) ----
+    float D[NTC][4];
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) D[nt][e] = __fadd_rn(D2[0][nt][e], D2[1][nt][e]);
 #pragma unroll
     for (int nt = 0; nt < NTC; ++nt) {
       float vg[2], v8[2];
@@ -198,8 +212,7 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
   constexpr int KCH = C::KCH;
   extern __shared__ __align__(128) uint8_t sm[];
   float* ysm = reinterpret_cast<float*>(sm + C::NSTAGE * C::STAGE);  // [64][COLS]
-  uint8_t* zrow = reinterpret_cast<uint8_t*>(ysm + 64 * COLS);  // INT4: zero B row (C::ZROW bytes)
-  uint64_t* full_b = reinterpret_cast<uint64_t*>(zrow + C::ZROW);
+  uint64_t* full_b = reinterpret_cast<uint64_t*>(ysm + 64 * COLS);
   uint64_t* empty_b = full_b + C::NSTAGE;
   int* flag = reinterpret_cast<int*>(empty_b + C::NSTAGE);
 
@@ -217,7 +230,6 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
   const int gpr = WMODE == QS_W_INT4 ? (P.K + P.wgroup - 1) / P.wgroup : 1;
   const int ks_pad = (KS + 3) / 4 * 4;
 
-  for (int i = tid; i < C::ZROW / 4; i += C::THREADS) reinterpret_cast<uint32_t*>(zrow)[i] = 0u;
   if (tid == 0) {
     for (int s = 0; s < C::NSTAGE; ++s) {
       mbar_init(&full_b[s], 1);
@@ -226,15 +238,22 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
     fence_mbar_init();
   }
   __syncthreads();
-  if (nunits <= 0) return;
+  if (nunits <= 0) {
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
 
   if (warp == C::NCW) {
     // ======================= producer warp =======================
-    if (lane != 0) return;
-    int mg = (int)(u_lo / KC), kc = (int)(u_lo % KC);
-    for (int i = 0; i < nunits; ++i) {
+    if (lane != 0) {
+      pdl_wait();
+      pdl_trigger();
+      return;
+    }
+    // weights (+ INT4 params) of unit i -> stage i % NSTAGE; expects the activation bytes too
+    auto issue_static = [&](int i, int mg, int kc) {
       const int s = i % C::NSTAGE;
-      if (i >= C::NSTAGE) mbar_wait_sleep(&empty_b[s], ((i / C::NSTAGE) - 1) & 1);
       const int ks0 = kc * KCH, nks = min(KCH, KS - ks0);
       uint8_t* sp = sm + s * C::STAGE;
       uint32_t wb, bb = (uint32_t)nks * 32, pb = 0, xb = 0;
@@ -253,12 +272,41 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
       if constexpr (WMODE == QS_W_INT4)
         bulk_g2s(sp + C::OFF_P, reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)mg * gpr + ks0 * 16 / P.wgroup) * 512,
                  pb, &full_b[s]);
+    };
+    // activation rows (+ INT4 16-sums) of unit i: written by the previous kernel
+    auto issue_act = [&](int i, int kc) {
+      const int s = i % C::NSTAGE;
+      const int ks0 = kc * KCH, nks = min(KCH, KS - ks0);
+      uint8_t* sp = sm + s * C::STAGE;
+      const uint32_t bb = (uint32_t)nks * 32, xb = (uint32_t)((nks + 3) / 4) * 16;
       for (int c = 0; c < ncols; ++c) {
         bulk_g2s(sp + C::OFF_B + c * C::BROW, reinterpret_cast<const __half*>(P.xh) + (size_t)c * P.ldxh + ks0 * 16, bb,
                  &full_b[s]);
         if constexpr (WMODE == QS_W_INT4)
           bulk_g2s(sp + C::OFF_X + c * C::XROW, P.xs + (size_t)c * P.ldxs + ks0, xb, &full_b[s]);
       }
+    };
+    // the first NSTAGE units' weights stream in while the previous kernel finishes (PDL)
+    const int npre = min(nunits, C::NSTAGE);
+    {
+      int mg = (int)(u_lo / KC), kc = (int)(u_lo % KC);
+      for (int i = 0; i < npre; ++i) {
+        issue_static(i, mg, kc);
+        if (++kc == KC) {
+          kc = 0;
+          ++mg;
+        }
+      }
+    }
+    pdl_wait();
+    pdl_trigger();
+    int mg = (int)(u_lo / KC), kc = (int)(u_lo % KC);
+    for (int i = 0; i < nunits; ++i) {
+      if (i >= npre) {
+        mbar_wait(&empty_b[i % C::NSTAGE], ((i / C::NSTAGE) - 1) & 1);
+        issue_static(i, mg, kc);
+      }
+      issue_act(i, kc);
       if (++kc == KC) {
         kc = 0;
         ++mg;
@@ -266,13 +314,15 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
     }
     return;
   }
+  pdl_wait();
+  pdl_trigger();
 
   // ======================= consumer warps =======================
-  float acc[NTC][4];
+  float acc[NTC][4], acc1[NTC][4];  // f16: even / odd k-step chains (halves the dependent-MMA depth)
 #pragma unroll
   for (int nt = 0; nt < NTC; ++nt)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+    for (int e = 0; e < 4; ++e) acc[nt][e] = acc1[nt][e] = 0.f;
 
   int mg = (int)(u_lo / KC), kc = (int)(u_lo % KC) - 1;
   for (int i = 0; i < nunits; ++i) {
@@ -284,7 +334,7 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
     const int ks0 = kc * KCH, nks = min(KCH, KS - ks0);
     const int mt = mg * 4 + warp;
     const uint8_t* sp = sm + s * C::STAGE;
-    mbar_wait_sleep(&full_b[s], (i / C::NSTAGE) & 1);
+    mbar_wait(&full_b[s], (i / C::NSTAGE) & 1);
     if (mt < MT) {
       // B fragments: row r = activation column; columns >= ncols read stale shared memory,
       // which only ever reaches the matching (discarded) output columns of the MMA.
@@ -299,7 +349,8 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
 #pragma unroll
             for (int nt = 0; nt < NTC; ++nt) {
               const uint8_t* row = bst + nt * 8 * C::BROW + ks * 32;
-              mma_acc(acc[nt], a, *reinterpret_cast<const uint32_t*>(row), *reinterpret_cast<const uint32_t*>(row + 16));
+              mma_acc((ks & 1) ? acc1[nt] : acc[nt], a, *reinterpret_cast<const uint32_t*>(row),
+                      *reinterpret_cast<const uint32_t*>(row + 16));
             }
           }
         } else {
@@ -318,9 +369,9 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
         const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + warp * 8 + g;  // [group][4 tiles][8]
         const float* xsm = reinterpret_cast<const float*>(sp + C::OFF_X);
         if (nks == KCH)
-          int4_unit<C, NTC, GKS, CW>(wa, sp + C::OFF_B, zrow, pp, xsm, KCH, g, t4, acc);
+          int4_unit<C, NTC, GKS, CW>(wa, sp + C::OFF_B, pp, xsm, KCH, g, t4, acc);
         else
-          int4_unit<C, NTC, GKS, CW>(wa, sp + C::OFF_B, zrow, pp, xsm, nks, g, t4, acc);
+          int4_unit<C, NTC, GKS, CW>(wa, sp + C::OFF_B, pp, xsm, nks, g, t4, acc);
       }
     }
     __syncwarp();
@@ -337,6 +388,11 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
     if (mt < MT) {
 #pragma unroll
       for (int nt = 0; nt < NTC; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          acc[nt][e] = __fadd_rn(acc[nt][e], acc1[nt][e]);
+          acc1[nt][e] = 0.f;
+        }
         const int c0 = nt * 8 + 2 * t4;
         const int r = warp * 16 + g;
         if (c0 < ncols) {
@@ -445,15 +501,31 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
 __global__ void prep_act_kernel(const float* __restrict__ x, const float* __restrict__ gain, float eps,
                                 __half* __restrict__ xh, long long ldxh, float* __restrict__ xs, long long ldxs,
                                 int d) {
+  pdl_wait();
+  pdl_trigger();
   const float* xr = x + (size_t)blockIdx.x * d;
   __half* hr = xh + (size_t)blockIdx.x * ldxh;
   float* sr = xs + (size_t)blockIdx.x * ldxs;
   __shared__ float red[32];
   __shared__ float s_inv;
+  const int ng = d / 16;
   float scale = 1.f;
   if (gain) {
+    // one thread per 16-element group, four 16-byte loads in flight per group
     float a = 0.f;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) a += __fmul_rn(xr[i], xr[i]);
+    for (int gi = threadIdx.x; gi < ng; gi += blockDim.x) {
+      const float4* p = reinterpret_cast<const float4*>(xr + gi * 16);
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = p[j];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a += __fmul_rn(v[j].x, v[j].x);
+        a += __fmul_rn(v[j].y, v[j].y);
+        a += __fmul_rn(v[j].z, v[j].z);
+        a += __fmul_rn(v[j].w, v[j].w);
+      }
+    }
     a = warp_sum(a);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
     __syncthreads();
@@ -466,13 +538,27 @@ __global__ void prep_act_kernel(const float* __restrict__ x, const float* __rest
     scale = s_inv;
   }
   // one thread per 16-element group: convert, store, sum the rounded values
-  for (int gi = threadIdx.x; gi < d / 16; gi += blockDim.x) {
+  for (int gi = threadIdx.x; gi < ng; gi += blockDim.x) {
+    float xv[16], gv[16];
+    const float4* p = reinterpret_cast<const float4*>(xr + gi * 16);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 v = p[j];
+      xv[4 * j] = v.x; xv[4 * j + 1] = v.y; xv[4 * j + 2] = v.z; xv[4 * j + 3] = v.w;
+    }
+    if (gain) {
+      const float4* gp = reinterpret_cast<const float4*>(gain + gi * 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 v = gp[j];
+        gv[4 * j] = v.x; gv[4 * j + 1] = v.y; gv[4 * j + 2] = v.z; gv[4 * j + 3] = v.w;
+      }
+    }
     float s = 0.f;
     __align__(16) __half hv[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const int i = gi * 16 + j;
-      const float v = gain ? __fmul_rn(__fdiv_rn(xr[i], scale), gain[i]) : xr[i];
+      const float v = gain ? __fmul_rn(__fdiv_rn(xv[j], scale), gv[j]) : xv[j];
       hv[j] = __float2half_rn(v);
       s += __half2float(hv[j]);
     }
@@ -484,8 +570,7 @@ __global__ void prep_act_kernel(const float* __restrict__ x, const float* __rest
 
 cudaError_t launch_prep_act(const float* x, const float* gain, float eps, void* xh, long long ldxh, float* xs,
                             long long ldxs, int n, int d, cudaStream_t s) {
-  prep_act_kernel<<<n, 256, 0, s>>>(x, gain, eps, reinterpret_cast<__half*>(xh), ldxh, xs, ldxs, d);
-  return cudaGetLastError();
+  return launch_pdl(prep_act_kernel, dim3(n), dim3(256), 0, s, x, gain, eps, reinterpret_cast<__half*>(xh), ldxh, xs, ldxs, d);
 }
 
 // CTAs actually launched: never more than work units, so every CTA owns at least one unit
@@ -518,8 +603,7 @@ static cudaError_t launch_lin_t(const LinearParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  kern<<<linear_grid_ctas(WMODE, p.N, p.K, p.nctas), C::THREADS, C::SMEM, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(linear_grid_ctas(WMODE, p.N, p.K, p.nctas)), dim3(C::THREADS), C::SMEM, s, p);
 }
 
 template <int WMODE, int NTC, int GKS, int CW>

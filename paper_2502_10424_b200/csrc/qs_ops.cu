@@ -5,14 +5,27 @@
 //   argmax selection /root/reference/pkg/src/quantspec/specdec.py:209-212
 //   greedy verify    /root/reference/pkg/src/quantspec/specdec.py:276-299
 #include <math.h>
+#include <stdlib.h>
 
 #include "qs_common.cuh"
 #include "qs_api_internal.h"
 
 namespace qs {
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("QS_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ gain, float* __restrict__ out,
                                int d, float eps) {
+  pdl_wait();
+  pdl_trigger();
   const float* xr = x + (size_t)blockIdx.x * d;
   float* orow = out + (size_t)blockIdx.x * d;
   __shared__ float red[32];
@@ -34,6 +47,8 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restr
 
 __global__ void embed_kernel(const float* __restrict__ table, const int* __restrict__ tok, float* __restrict__ out,
                              int d, int vocab, int* flags) {
+  pdl_wait();
+  pdl_trigger();
   int t = tok[blockIdx.x];
   if (t < 0 || t >= vocab) {
     if (threadIdx.x == 0 && flags) atomicOr(flags, 2);
@@ -58,6 +73,8 @@ __device__ __forceinline__ bool better(float va, int ia, float vb, int ib) {
 }
 
 __global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int* __restrict__ out, int out_stride) {
+  pdl_wait();
+  pdl_trigger();
   const float* row = logits + (size_t)blockIdx.x * vocab;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
@@ -98,6 +115,8 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int* 
 // tgt[i] = argmax of target row i.  Greedy rule of Q/specdec.py:279-298.
 __global__ void greedy_accept_kernel(const int* __restrict__ drafts, const int* __restrict__ tgt, int gamma,
                                      int* __restrict__ res, int* __restrict__ next_tok, int* bump0, int* bump1) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x != 0) return;
   int v = 0;
   while (v < gamma && drafts[v] == tgt[v]) ++v;
@@ -110,31 +129,28 @@ __global__ void greedy_accept_kernel(const int* __restrict__ drafts, const int* 
 }
 
 __global__ void add_int_kernel(int* p, int n, int delta) {
+  pdl_wait();
+  pdl_trigger();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] += delta;
 }
 
 cudaError_t launch_rmsnorm(const float* x, const float* gain, float* out, int n, int d, float eps, cudaStream_t s) {
-  rmsnorm_kernel<<<n, 256, 0, s>>>(x, gain, out, d, eps);
-  return cudaGetLastError();
+  return launch_pdl(rmsnorm_kernel, dim3(n), dim3(256), 0, s, x, gain, out, d, eps);
 }
 cudaError_t launch_embed(const float* table, const int* tok, float* out, int n, int d, int vocab, int* flags,
                          cudaStream_t s) {
-  embed_kernel<<<n, 256, 0, s>>>(table, tok, out, d, vocab, flags);
-  return cudaGetLastError();
+  return launch_pdl(embed_kernel, dim3(n), dim3(256), 0, s, table, tok, out, d, vocab, flags);
 }
 cudaError_t launch_argmax(const float* logits, int n, int vocab, int* out, int out_stride, cudaStream_t s) {
-  argmax_kernel<<<n, 512, 0, s>>>(logits, vocab, out, out_stride);
-  return cudaGetLastError();
+  return launch_pdl(argmax_kernel, dim3(n), dim3(512), 0, s, logits, vocab, out, out_stride);
 }
 cudaError_t launch_greedy_accept(const int* drafts, const int* tgt, int gamma, int* res, int* next_tok, int* b0,
                                  int* b1, cudaStream_t s) {
-  greedy_accept_kernel<<<1, 32, 0, s>>>(drafts, tgt, gamma, res, next_tok, b0, b1);
-  return cudaGetLastError();
+  return launch_pdl(greedy_accept_kernel, dim3(1), dim3(32), 0, s, drafts, tgt, gamma, res, next_tok, b0, b1);
 }
 cudaError_t launch_add_int(int* p, int n, int delta, cudaStream_t s) {
-  add_int_kernel<<<(n + 127) / 128, 128, 0, s>>>(p, n, delta);
-  return cudaGetLastError();
+  return launch_pdl(add_int_kernel, dim3((n + 127) / 128), dim3(128), 0, s, p, n, delta);
 }
 
 }  // namespace qs
