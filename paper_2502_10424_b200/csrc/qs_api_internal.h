@@ -8,8 +8,17 @@ using AttnParams = qs_attn_args;
 using LinearParams = qs_linear_args;
 
 cudaError_t launch_attention(const AttnParams& p, int mode, cudaStream_t s);
-int attention_smem_bytes(int hd, int nt, int mode);
-int attention_occupancy(int hd, int nt, int mode);
+// query tiles per CTA for `per` query columns: the target view runs 8 queries per MMA tile
+// (hi/lo on the M rows), the draft and fp16 views 4 (hi/lo column pairs); queries per CTA = nt * that
+inline int attention_nt(int per, int mode) {
+  const int w = mode == QS_VIEW_TARGET ? 8 : 4;
+  const int nt = (per + w - 1) / w;
+  return nt < 1 ? 1 : nt;
+}
+inline int attention_queries_per_cta(int per, int mode) {
+  return attention_nt(per, mode) * (mode == QS_VIEW_TARGET ? 8 : 4);
+}
+int attention_occupancy(int hd, int per, int mode);
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s);
 int linear_maxc(int wmode, int N, int K, int nctas);
 int linear_occupancy(int wmode, int wgroup, int ncols);

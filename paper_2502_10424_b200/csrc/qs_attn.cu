@@ -39,46 +39,68 @@ enum { MODE_QDRAFT = 0, MODE_QTARGET = 1, MODE_FP16 = 2 };
 
 #define kNegInf (-__int_as_float(0x7f800000))
 
+// mma.sync without `volatile`: pure, so ptxas may interleave it with the nibble unpacking
+__device__ __forceinline__ void mma_nv(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
 constexpr int PSTRIDE = 24;  // halves per P row (16 tokens + pad: conflict-free transposes)
 
-template <int HD, int NT, int MODE>
+// NT: quantised modes -> query tiles of 8 queries (QK runs queries on the MMA M rows:
+// hi parts in rows 0-7, lo parts in rows 8-15); fp16 mode -> n-tiles of 4 queries
+// (hi/lo column pairs).  The fp16 tails inside a quantised launch use NTO = NQ/4 of the latter.
+// NT: quantised modes -> query tiles of 8 queries (QK runs queries on the MMA M rows:
+// hi parts in rows 0-7, lo parts in rows 8-15); fp16 mode -> n-tiles of 4 queries
+// (hi/lo column pairs).  QR (quantised, NT == 1): query rows actually stored in the
+// q' fragment buffers (the MHA draft has one query per KV head: QR = 1 keeps the stage small).
+template <int HD, int NT, int MODE, int QR = 8>
 struct AttnCfg {
   static constexpr bool QUANT = MODE != MODE_FP16;
   static constexpr int NCW = QUANT ? 8 : 4;            // compute warps
-  static constexpr int NPW = QUANT ? 2 : 0;            // producer warps (TMA issue + query-scale fold)
-  static constexpr int NWARPS = NCW + NPW;
-  static constexpr int THREADS = NWARPS * 32;
   static constexpr int KS = HD / 16;
-  static constexpr int NQ = NT * 4;                      // queries (hi/lo column pairs) per CTA
-  // ---- quantised stage: planes | key params | value params | Bq fragments | biases ----
+  // target view: queries on the QK M rows (ROWQ); draft and fp16 views: hi/lo column pairs
+  static constexpr bool ROWQ = MODE == MODE_QTARGET;
+  static constexpr int NQ = ROWQ ? NT * 8 : NT * 4;      // queries per CTA
+  static constexpr int NTO = NQ / 4;                     // hi/lo column-pair n-tiles of the fp16 path
+  static constexpr int AQ = QR * 16;                     // words per (k-tile, query tile) of q' A fragments
+  // ---- quantised stage: planes | key params | value params | Aq fragments | biases ----
   static constexpr int PLANE_CHUNK = HD * QS_CHUNK_Q / 2;
   static constexpr int NPLANE = (MODE == MODE_QTARGET) ? 4 : 2;
   static constexpr int KP_OFF = NPLANE * PLANE_CHUNK;
   static constexpr int VP_OFF = KP_OFF + QS_CHUNK_Q * 8;  // (128/G)*HD <= 128 key params (G >= HD)
   static constexpr int BQ_OFF = VP_OFF + QS_CHUNK_Q * 8;
-  static constexpr int BQ_WORDS = 8 * NT * 64;            // (128/G)*KS <= 8 B-fragment tiles
+  // ROWQ: A fragments [(128/G)*KS <= 8 k-tiles][NT][QR*4 lanes][a0..a3]; else B fragments [k-tile][NT][lane][b0 b1]
+  static constexpr int BQ_WORDS = ROWQ ? 8 * NT * AQ : 8 * NT * 64;
   static constexpr int BIAS_OFF = BQ_OFF + BQ_WORDS * 4;
-  static constexpr int BIAS_FLOATS = 8 * NQ * 2;          // [block][q][row g | row g+8]
+  static constexpr int BIAS_FLOATS = 8 * NQ * 2;          // [block][q][x1 tokens | x16 tokens]
   static constexpr int QSTAGE = (BIAS_OFF + BIAS_FLOATS * 4 + 127) / 128 * 128;
-  // deep TMA ring: ~4 chunks in flight per CTA (the loaded HBM latency is a few microseconds)
-  static constexpr int NSTAGE = NT <= 2 ? 5 : 4;
-  // resident CTAs per SM the register budget targets (wide verify launches keep 1 to avoid spills)
-  static constexpr int MIN_BLOCKS = QUANT ? ((MODE == MODE_QDRAFT && NT == 1) ? 2 : 1) : 3;
   // ---- fp16 chunks: 64 tokens in the fp16 kernel, 32 in the quantised kernel's tails ----
   static constexpr int CF = QUANT ? 32 : 64;
   static constexpr int FSTAGE = 2 * CF * HD * 2;
   static constexpr int NSTAGE_F = 2;
-  static constexpr int REGION_Q = QUANT ? NSTAGE * QSTAGE : 0;
   static constexpr int REGION_F = NSTAGE_F * FSTAGE;
   static constexpr int MS = HD + 4;
   static constexpr int MERGE_BYTES = NCW * NQ * MS * 4;
+  static constexpr int BQF_WORDS = ROWQ ? KS * NT * AQ : KS * NTO * 64;  // query fragments of fp16 chunks
+  static constexpr int PW_HALVES = NTO * 8 * PSTRIDE;
+  static constexpr int FIXED = BQF_WORDS * 4 + NQ * HD * 4 + (ROWQ ? 0 : NCW * PW_HALVES * 2) + 3 * 8 * 8 + 16;
+  // TMA ring: two CTAs per SM when at least 4 stages fit each (of 228 KB, 1 KB reserved per CTA),
+  // else one CTA with the deepest ring that fits; at most 6 stages
+  static constexpr int S2 = (233472 / 2 - 1024 - FIXED) / QSTAGE;
+  static constexpr int S1 = (232448 - FIXED) / QSTAGE;
+  static constexpr int MIN_BLOCKS = QUANT ? ((NT == 1 && S2 >= 4) ? 2 : 1) : 3;  // wide launches: registers
+  static constexpr int NSTAGE = QUANT ? (MIN_BLOCKS == 2 ? (S2 < 6 ? S2 : 6) : (S1 < 6 ? S1 : 6)) : 1;
+  // producer warps (TMA issue + query-scale fold); each folds whole chunks, NPW < NSTAGE
+  static constexpr int NPW = QUANT ? (NSTAGE > 2 ? 2 : 1) : 0;
+  static constexpr int NWARPS = NCW + NPW;
+  static constexpr int THREADS = NWARPS * 32;
+  static constexpr int REGION_Q = QUANT ? NSTAGE * QSTAGE : 0;
   static constexpr int R0 = REGION_Q > REGION_F ? REGION_Q : REGION_F;
   static constexpr int REGION = R0 > MERGE_BYTES ? R0 : MERGE_BYTES;
-  static constexpr int BQF_WORDS = KS * NT * 64;          // raw-query fragments for fp16 chunks
-  static constexpr int PW_HALVES = NT * 8 * PSTRIDE;
   static constexpr int VPAD = 2 * NQ <= 8 ? 8 : 2 * NQ <= 16 ? 16 : 32;      // reduce-scatter width
-  static constexpr int SMEM =
-      REGION + BQF_WORDS * 4 + NQ * HD * 4 + NCW * PW_HALVES * 2 + 3 * 8 * 8 + 16;
+  static constexpr int SMEM = REGION + FIXED;
 };
 
 __device__ __forceinline__ int swz16(int chunk, int row, int nchunk) {
@@ -314,6 +336,157 @@ __device__ __forceinline__ void quant_issue(const AttnParams& P, uint8_t* region
   bulk_g2s(sp + C::VP_OFF, vp + (size_t)b0 * G, vpb, &tma_b[s]);
 }
 
+// fp16 tails of a quantised launch (fp1 / fp2 recent-token buffers) in the quantised
+// path's register layout: queries on the MMA M rows (hi rows g, lo rows g+8), tokens on N,
+// so P feeds P.V straight from registers and the merge is shared with quant_region.
+template <typename C, int HD, int NT>
+__device__ __forceinline__ void fp16_region_q(uint8_t* region, uint32_t* aqf, const float* q_s, int nq,
+                                              const __half* fk, const __half* fv, int n_tok, int c_begin, int c_end,
+                                              int causal, int qg, const AttnParams& P, Softmax (&st)[NT],
+                                              float (&acc)[C::KS][NT][4]) {
+  constexpr int KS = C::KS, NQ = C::NQ, NTH = C::THREADS, CF = C::CF;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const float sl2 = P.sm_scale_log2;
+  for (int i = tid; i < C::BQF_WORDS; i += NTH) aqf[i] = 0u;
+  __syncthreads();
+  // A fragments of the raw queries: [k-tile][query tile][lane][a0..a3]
+  for (int j = tid; j < (HD / 2) * nq; j += NTH) {
+    const int cp = j % (HD / 2), q = j / (HD / 2);
+    const float2 qv = *reinterpret_cast<const float2*>(q_s + q * HD + 2 * cp);
+    const __half2 hi = __floats2half2_rn(qv.x, qv.y);
+    const float2 hf = __half22float2(hi);
+    const __half2 lo = __floats2half2_rn(qv.x - hf.x, qv.y - hf.y);
+    const int jj = cp & 7;
+    uint32_t* bb = aqf + (size_t)((cp >> 3) * NT + (q >> 3)) * C::AQ + (q & 7) * 16 + (jj & 3) * 4 + 2 * (jj >> 2);
+    bb[0] = h2_as_u32(hi);
+    bb[1] = h2_as_u32(lo);
+  }
+  const int nchunk = c_end - c_begin;
+  constexpr int NCH16 = HD / 8;
+  auto fstage = [&](int s) { return reinterpret_cast<__half*>(region + s * C::FSTAGE); };
+  auto issue_f = [&](int i) {
+    if (i < nchunk) {
+      int c = c_begin + i;
+      __half* ks_ = fstage(i % C::NSTAGE_F);
+      __half* vs_ = ks_ + CF * HD;
+      for (int idx = tid; idx < CF * NCH16; idx += NTH) {
+        int row = idx / NCH16, ch = idx % NCH16;
+        int tok = c * CF + row;
+        bool ok = tok < n_tok;
+        int tk = ok ? tok : 0;
+        int pc = swz16(ch, row, NCH16);
+        cp_async16(smem_u32(ks_ + row * HD + pc * 8), fk + (size_t)tk * HD + ch * 8, ok);
+        cp_async16(smem_u32(vs_ + row * HD + pc * 8), fv + (size_t)tk * HD + ch * 8, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  for (int i = 0; i < C::NSTAGE_F - 1; ++i) issue_f(i);
+  const int mt = warp;
+  const bool has_tile = mt * 16 < CF && warp < C::NCW;
+  const int ii = lane >> 3, rr = lane & 7;
+  for (int i = 0; i < nchunk; ++i) {
+    cp_async_wait<C::NSTAGE_F - 2>();
+    __syncthreads();
+    issue_f(i + C::NSTAGE_F - 1);
+    if (!has_tile) continue;
+    const int c = c_begin + i;
+    const __half* ks_ = fstage(i % C::NSTAGE_F);
+    const __half* vs_ = ks_ + CF * HD;
+    const int tok_base = c * CF + mt * 16;
+    if (tok_base < n_tok) {
+      float d[2][NT][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) d[j][nt][e] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        // x4: (tokens 0-7 | 8-15) x (channels lo | hi) of the k-tile = B fragments of both token n-tiles
+        const int row = mt * 16 + (ii & 1) * 8 + rr;
+        const int ch = ks * 2 + (ii >> 1);
+        uint32_t b[4];
+        ldmatrix_x4(b, smem_u32(ks_ + row * HD + swz16(ch, row, NCH16) * 8));
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const uint4 a4 = lane < C::AQ / 4 ? reinterpret_cast<const uint4*>(aqf)[(ks * NT + nt) * (C::AQ / 4) + lane]
+                                          : make_uint4(0u, 0u, 0u, 0u);
+          const uint32_t af[4] = {a4.x, a4.y, a4.z, a4.w};
+          mma_nv(d[0][nt], af, b[0], b[2]);
+          mma_nv(d[1][nt], af, b[1], b[3]);
+        }
+      }
+      uint32_t bph[NT][2], bpl[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        int lim = n_tok;
+        if (causal) {
+          const int qgl = qg * NQ + nt * 8 + g;
+          const int t = min(qgl / P.r, P.T - 1);
+          lim = n_tok - (P.T - 1 - t);
+        }
+        float sv[2][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int tok = tok_base + 8 * j + 2 * t4 + e;
+            sv[j][e] = tok < lim ? (d[j][nt][e] + d[j][nt][e + 2]) * sl2 : kNegInf;
+          }
+        float mx = fmaxf(fmaxf(sv[0][0], sv[0][1]), fmaxf(sv[1][0], sv[1][1]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        float alpha = 1.0f;
+        if (mx > st[nt].m) {
+          alpha = exp2f(st[nt].m - mx);
+          st[nt].l *= alpha;
+          st[nt].m = mx;
+        }
+        if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+          const float a0 = __shfl_sync(0xffffffffu, alpha, 8 * t4);
+          const float a1 = __shfl_sync(0xffffffffu, alpha, 8 * t4 + 4);
+#pragma unroll
+          for (int cm = 0; cm < KS; ++cm) {
+            acc[cm][nt][0] *= a0;
+            acc[cm][nt][1] *= a1;
+            acc[cm][nt][2] *= a0;
+            acc[cm][nt][3] *= a1;
+          }
+        }
+        const float m = st[nt].m;
+        float p[2][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) p[j][e] = sv[j][e] == kNegInf ? 0.f : exp2f(sv[j][e] - m);
+        st[nt].l += (p[0][0] + p[0][1]) + (p[1][0] + p[1][1]);
+        const __half2 h0 = __floats2half2_rn(p[0][0], p[0][1]), h1 = __floats2half2_rn(p[1][0], p[1][1]);
+        const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+        bph[nt][0] = h2_as_u32(h0);
+        bph[nt][1] = h2_as_u32(h1);
+        bpl[nt][0] = h2_as_u32(__floats2half2_rn(p[0][0] - f0.x, p[0][1] - f0.y));
+        bpl[nt][1] = h2_as_u32(__floats2half2_rn(p[1][0] - f1.x, p[1][1] - f1.y));
+      }
+#pragma unroll
+      for (int cm = 0; cm < KS; ++cm) {
+        const int row = mt * 16 + (ii >> 1) * 8 + rr;
+        const int ch = cm * 2 + (ii & 1);
+        uint32_t a[4];
+        ldmatrix_x4_trans(a, smem_u32(vs_ + row * HD + swz16(ch, row, NCH16) * 8));
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mma_nv(acc[cm][nt], a, bph[nt][0], bph[nt][1]);
+          mma_nv(acc[cm][nt], a, bpl[nt][0], bpl[nt][1]);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // ---------------------------------------------------------------------------
 // quantised region: producer warp + 8 consumer warps
 // ---------------------------------------------------------------------------
@@ -380,8 +553,11 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
           if (cp < HD / 2) {
             const float4 pz = *reinterpret_cast<const float4*>(kps + bl * HD + 2 * cp);  // (S0, Z0, S1, Z1)
             const float s0 = pz.x * kvs, s1 = pz.z * kvs;
+            // ROWQ: A fragment of k-tile cp/8, lane (q%8)*4 + (cp%4), register 2*((cp/4)%2) (+1 for lo);
+            // else B fragment (columns 2q = hi, 2q+1 = lo), lane (col%8)*4 + cp%4, register (cp/4)%2
             const int jj = cp & 7;
-            uint32_t* tb = bqb + (size_t)(bl * KS + (cp >> 3)) * NT * 64 + (jj & 3) * 2 + (jj >> 2);
+            uint32_t* tb = C::ROWQ ? bqb + (size_t)(bl * KS + (cp >> 3)) * NT * C::AQ + (jj & 3) * 4 + 2 * (jj >> 2)
+                                   : bqb + (size_t)(bl * KS + (cp >> 3)) * NT * 64 + (jj & 3) * 2 + (jj >> 2);
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
               if (q < nq) {
@@ -391,9 +567,15 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
                 const float2 hf = __half22float2(hi);
                 const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
                 const float2 lf = __half22float2(lo);
-                uint32_t* bb = tb + ((2 * q) >> 3) * 64 + ((2 * q) & 7) * 8;
-                bb[0] = h2_as_u32(hi);
-                bb[8] = h2_as_u32(lo);
+                if constexpr (C::ROWQ) {
+                  uint32_t* bb = tb + (q >> 3) * C::AQ + (q & 7) * 16;
+                  bb[0] = h2_as_u32(hi);
+                  bb[1] = h2_as_u32(lo);
+                } else {
+                  uint32_t* bb = tb + ((2 * q) >> 3) * 64 + ((2 * q) & 7) * 8;
+                  bb[0] = h2_as_u32(hi);
+                  bb[8] = h2_as_u32(lo);
+                }
                 zs[q] += qv.x * pz.y + qv.y * pz.w;
                 bs[q] += (hf.x + hf.y) + (lf.x + lf.y);
               }
@@ -430,8 +612,8 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         const int qq = lane < nq ? lane : 0;
         const float z = __shfl_sync(0xffffffffu, tot, qq << (5 - LV));
         const float b = __shfl_sync(0xffffffffu, tot, (NQ + qq) << (5 - LV));
-        // draft rows g carry 1024 + c, rows g+8 carry (1024 + 16c) (scaled by 1/16 after the MMA);
-        // target rows carry 1032 + (16 c_u + c_l)
+        // draft tokens g of a 16-token tile carry 1024 + c, tokens g+8 carry (1024 + 16c) (scaled
+        // by 1/16 after the MMA); target tokens carry 1032 + (16 c_u + c_l)
         if (lane < nq) {
           bias[(bl * NQ + lane) * 2 + 0] = z - (TGT ? 1032.f : 1024.f) * b;
           bias[(bl * NQ + lane) * 2 + 1] = z - (TGT ? 1032.f : 64.f) * b;
@@ -449,6 +631,127 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
     return;
   }
 
+  if constexpr (C::ROWQ) {
+  // ======================= consumer warps =======================
+  // Warp mt owns token tile mt (16 tokens) of every chunk.
+  //   Q.K^T (queries on M): A = q' fragments (rows g: hi, rows g+8: lo of query g), B = the
+  //   tile's K codes as two n-tiles (tokens g | g+8: the frag4 word of an A tile K[token][ch]
+  //   is exactly the B fragment pair of K^T), so each lane ends up with the scores of query g
+  //   for tokens 2t, 2t+1, 2t+8, 2t+9 -- already the B-fragment layout of P for P.V.
+  //   P.V (channels on M): A = V^T codes, B = p' = p * S_v (hi, and lo for the target).
+  const float sl2 = P.sm_scale_log2;
+  const int mt = warp;
+  for (int i = 0; i < nchunk; ++i) {
+    const int s = i % S;
+    const uint8_t* sp = stage_ptr(s);
+    mbar_wait(&full_b[s], (i / S) & 1);
+    const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
+    const bool live = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
+    if (live) {
+      const int bl = (mt * 16) >> lgG;
+      const uint4* aq = reinterpret_cast<const uint4*>(sp + C::BQ_OFF) + (size_t)bl * KS * NT * (C::AQ / 4) + lane;
+      const float* bias = reinterpret_cast<const float*>(sp + C::BIAS_OFF);
+      const float4* vps4 = reinterpret_cast<const float4*>(sp + C::VP_OFF);  // (S, Z) of tokens 2k, 2k+1
+      uint32_t wu[KS], wl[KS];
+      load_words<KS>(reinterpret_cast<const uint32_t*>(sp), mt, lane, wu);
+      if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp + 2 * C::PLANE_CHUNK), mt, lane, wl);
+      float d[2][NT][4];  // [token half][query tile]: two independent MMA chains
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) d[j][nt][e] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        uint32_t r[4];
+        if constexpr (TGT) unpack_u4l4_raw(wu[ks], wl[ks], r);
+        else unpack_u4_raw(wu[ks], r);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const uint4 a4 = lane < C::AQ / 4 ? aq[(ks * NT + nt) * (C::AQ / 4)] : make_uint4(0u, 0u, 0u, 0u);
+          const uint32_t af[4] = {a4.x, a4.y, a4.z, a4.w};
+          mma_nv(d[0][nt], af, r[0], r[2]);  // tokens g     (draft: 1024 + c)
+          mma_nv(d[1][nt], af, r[1], r[3]);  // tokens g + 8 (draft: 1024 + 16 c)
+        }
+      }
+      const float4 vz0 = vps4[mt * 8 + t4], vz1 = vps4[mt * 8 + 4 + t4];
+      uint32_t bph[NT][2], bpl[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const float2 bb = *reinterpret_cast<const float2*>(bias + (bl * NQ + nt * 8 + g) * 2);
+        float sv[2][2];  // [token half][token 2t + e]
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float raw = d[j][nt][e] + d[j][nt][e + 2];  // rows g (hi) + g+8 (lo) of query g
+            sv[j][e] = (TGT || j == 0) ? (raw + bb.x) * sl2 : fmaf(raw, 0.0625f, bb.y) * sl2;
+          }
+        float mx = fmaxf(fmaxf(sv[0][0], sv[0][1]), fmaxf(sv[1][0], sv[1][1]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        float alpha = 1.0f;
+        if (mx > st[nt].m) {
+          alpha = exp2f(st[nt].m - mx);  // st.m == -inf -> 0
+          st[nt].l *= alpha;
+          st[nt].z *= alpha;
+          st[nt].ps *= alpha;
+          st[nt].m = mx;
+        }
+        // the accumulator columns of query q = nt*8 + 2t + e live in this lane; its alpha in lanes g = q
+        if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+          const float a0 = __shfl_sync(0xffffffffu, alpha, 8 * t4);
+          const float a1 = __shfl_sync(0xffffffffu, alpha, 8 * t4 + 4);
+#pragma unroll
+          for (int cm = 0; cm < KS; ++cm) {
+            acc[cm][nt][0] *= a0;
+            acc[cm][nt][1] *= a1;
+            acc[cm][nt][2] *= a0;
+            acc[cm][nt][3] *= a1;
+          }
+        }
+        const float m = st[nt].m;
+        const float p00 = exp2f(sv[0][0] - m), p01 = exp2f(sv[0][1] - m);
+        const float p10 = exp2f(sv[1][0] - m), p11 = exp2f(sv[1][1] - m);
+        st[nt].l += (p00 + p01) + (p10 + p11);
+        st[nt].z += (p00 * vz0.y + p01 * vz0.w) + (p10 * vz1.y + p11 * vz1.w);
+        const float v00 = p00 * (vz0.x * kvs), v01 = p01 * (vz0.z * kvs);
+        const float v10 = p10 * (vz1.x * kvs), v11 = p11 * (vz1.z * kvs);
+        const __half2 h0 = __floats2half2_rn(v00, v01), h1 = __floats2half2_rn(v10, v11);
+        const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+        float psum = (f0.x + f0.y) + (f1.x + f1.y);
+        bph[nt][0] = h2_as_u32(h0);
+        bph[nt][1] = h2_as_u32(h1);
+        if constexpr (TGT) {
+          const __half2 l0 = __floats2half2_rn(v00 - f0.x, v01 - f0.y), l1 = __floats2half2_rn(v10 - f1.x, v11 - f1.y);
+          const float2 g0 = __half22float2(l0), g1 = __half22float2(l1);
+          psum += (g0.x + g0.y) + (g1.x + g1.y);
+          bpl[nt][0] = h2_as_u32(l0);
+          bpl[nt][1] = h2_as_u32(l1);
+        }
+        st[nt].ps += psum;
+      }
+      // ---- P.V: A = V^T codes [channels x tokens] of this token tile ----
+      uint32_t vw[KS], vwl[KS];
+      load_words<KS>(reinterpret_cast<const uint32_t*>(sp + C::PLANE_CHUNK), mt, lane, vw);
+      if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp + 3 * C::PLANE_CHUNK), mt, lane, vwl);
+#pragma unroll
+      for (int cm = 0; cm < KS; ++cm) {
+        uint32_t a[4];
+        if constexpr (TGT) unpack_u4l4_raw(vw[cm], vwl[cm], a);
+        else unpack_u4_raw(vw[cm], a);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mma_nv(acc[cm][nt], a, bph[nt][0], bph[nt][1]);
+          if constexpr (TGT) mma_nv(acc[cm][nt], a, bpl[nt][0], bpl[nt][1]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_b[s]);
+  }
+  } else {
   // ======================= consumer warps =======================
   const float sl2 = P.sm_scale_log2;
   const int mt = warp;  // this warp's 16-token tile of every chunk
@@ -527,21 +830,103 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_b[s]);
   }
+  }
+}
+
+// Per-warp merge rows of the quantised path (query q = nt*8 + g holds the softmax state;
+// accumulator columns are queries nt*8 + 2t + e).  P.V offsets: draft rows g carried
+// (1024 + c) p' and rows g+8 (1024 + 16c) p'; target rows carried (1032 + 16 c_u + c_l) p'.
+template <typename C, int HD, int NT, int MODE>
+__device__ __forceinline__ void merge_rows_quant(float* mrg, const Softmax (&st)[NT], const float (&acc)[C::KS][NT][4],
+                                                 bool offsets) {
+  constexpr int KS = C::KS, NQ = C::NQ, MS = C::MS;
+  constexpr bool TGT = MODE == MODE_QTARGET;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    float l = st[nt].l, z = st[nt].z, ps = st[nt].ps;
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      l += __shfl_xor_sync(0xffffffffu, l, o);
+      z += __shfl_xor_sync(0xffffffffu, z, o);
+      ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    }
+    float* row = mrg + (warp * NQ + nt * 8 + g) * MS;
+    if (t4 == 0) {
+      row[0] = st[nt].m;
+      row[1] = l;
+      row[2] = z;
+      row[3] = ps;
+    }
+  }
+  __syncwarp();
+  // (fp16 tails: plain values, no offsets)
+  const float og = offsets ? (TGT ? 1032.f : 1024.f) : 0.f, og8 = offsets ? (TGT ? 1032.f : 64.f) : 0.f;
+  const float sc8 = (offsets && !TGT) ? 0.0625f : 1.0f;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      float* row = mrg + (warp * NQ + nt * 8 + 2 * t4 + e) * MS;
+      const float z = row[2], ps = row[3];
+#pragma unroll
+      for (int cm = 0; cm < KS; ++cm) {
+        row[4 + cm * 16 + g] = (acc[cm][nt][e] - og * ps) + z;
+        row[4 + cm * 16 + g + 8] = fmaf(acc[cm][nt][e + 2], sc8, -og8 * ps) + z;
+      }
+    }
+}
+
+// per-warp merge rows of the hi/lo column-pair layout (query q = nt*4 + t): the fp16
+// regions, and the draft's quantised region with its P.V offsets (rows g carried
+// (1024 + c) p', rows g+8 (1024 + 16c) p')
+template <typename C, int HD, int NTO, int MODE>
+__device__ __forceinline__ void merge_rows_fp(float* mrg, const Softmax (&st)[NTO], const float (&acc)[C::KS][NTO][4],
+                                              bool offsets) {
+  constexpr int KS = C::KS, NQ = C::NQ, MS = C::MS;
+  constexpr bool TGT = MODE == MODE_QTARGET;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int nt = 0; nt < NTO; ++nt) {
+    float l = st[nt].l, z = st[nt].z, ps = st[nt].ps;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l += __shfl_xor_sync(0xffffffffu, l, o);
+      z += __shfl_xor_sync(0xffffffffu, z, o);
+      ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    }
+    float* row = mrg + (warp * NQ + nt * 4 + t4) * MS;
+    if (g == 0) {
+      row[0] = st[nt].m;
+      row[1] = l;
+    }
+    const float off_g = offsets ? (TGT ? 1032.f : 1024.f) * ps : 0.f;
+    const float off_g8 = offsets ? (TGT ? 1032.f : 64.f) * ps : 0.f;
+    const float sc8 = (offsets && !TGT) ? 0.0625f : 1.0f;
+#pragma unroll
+    for (int cm = 0; cm < KS; ++cm) {
+      row[4 + cm * 16 + g] = ((acc[cm][nt][0] + acc[cm][nt][1]) - off_g) + z;
+      row[4 + cm * 16 + g + 8] = fmaf(acc[cm][nt][2] + acc[cm][nt][3], sc8, -off_g8) + z;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int HD, int NT, int MODE>
-__global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT, MODE>::MIN_BLOCKS) attn_kernel(const __grid_constant__ AttnParams P) {
-  using C = AttnCfg<HD, NT, MODE>;
+template <int HD, int NT, int MODE, int QR>
+__global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD, NT, MODE, QR>::MIN_BLOCKS) attn_kernel(const __grid_constant__ AttnParams P) {
+  using C = AttnCfg<HD, NT, MODE, QR>;
   constexpr int KS = C::KS, NQ = C::NQ, NCW = C::NCW, NTH = C::THREADS;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* region = smem;
   uint32_t* bqf = reinterpret_cast<uint32_t*>(smem + C::REGION);      // [KS][NT][32][2]
   float* q_s = reinterpret_cast<float*>(bqf + C::BQF_WORDS);          // [NQ][HD]
   __half* pw_all = reinterpret_cast<__half*>(q_s + NQ * HD);           // [NCW][PW_HALVES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pw_all + NCW * C::PW_HALVES);  // tma[8] full[8] empty[8]
+  // tma[8] full[8] empty[8] (the row-query kernels have no P transpose buffers)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(C::ROWQ ? reinterpret_cast<__half*>(q_s + NQ * HD) : pw_all + NCW * C::PW_HALVES);
   int* ticket_s = reinterpret_cast<int*>(bars + 24);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -636,59 +1021,56 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
   }
   __syncthreads();
 
-  Softmax st[NT];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) st[nt] = {kNegInf, 0.f, 0.f, 0.f};
-  float acc[KS][NT][4];
-#pragma unroll
-  for (int a = 0; a < KS; ++a)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[a][nt][e] = 0.f;
-
-  bool offset_pv = false;
+  constexpr int MS = C::MS;
+  float* mrg = reinterpret_cast<float*>(region);  // [NCW][NQ][MS]: m, l, z, ps, acc[HD]  (after the regions)
   if (region_kind == 0) {
     if constexpr (C::QUANT) {
+      Softmax st[NT];
+      float acc[KS][NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        st[nt] = {kNegInf, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int a = 0; a < KS; ++a)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[a][nt][e] = 0.f;
+      }
       if (c_end > c_begin) quant_region<C, HD, NT, MODE>(region, bars, q_s, pw, nq, seq, head, n_tok, c_begin, c_end, P, st, acc);
-      offset_pv = true;
+      __syncthreads();
+      if (warp < NCW) {
+        if constexpr (C::ROWQ) merge_rows_quant<C, HD, NT, MODE>(mrg, st, acc, true);
+        else merge_rows_fp<C, HD, NT, MODE>(mrg, st, acc, true);
+      }
     }
-  } else if (c_end > c_begin) {
-    fp16_region<C, HD, NT>(region, bqf, q_s, pw, nq, fk, fv, n_tok, c_begin, c_end, causal, qg, P, st, acc);
-  }
-
-  // ===================== merge the compute warps of this CTA =====================
-  __syncthreads();
-  constexpr int MS = C::MS;
-  float* mrg = reinterpret_cast<float*>(region);  // [NCW][NQ][MS]: m, l, -, -, acc[HD]
-  if (warp < NCW) {
+  } else if constexpr (C::ROWQ) {
+    Softmax st[NT];
+    float acc[KS][NT][4];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      float l = st[nt].l, z = st[nt].z, ps = st[nt].ps;
+      st[nt] = {kNegInf, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        l += __shfl_xor_sync(0xffffffffu, l, o);
-        z += __shfl_xor_sync(0xffffffffu, z, o);
-        ps += __shfl_xor_sync(0xffffffffu, ps, o);
-      }
-      const int q = nt * 4 + t4;
-      float* row = mrg + (warp * NQ + q) * MS;
-      if (g == 0) {
-        row[0] = st[nt].m;
-        row[1] = l;
-      }
-      // P.V offsets of the quantised path: draft rows g carried (1024 + c) p' and rows g+8
-      // (1024 + 16c) p'; target rows carried (1032 + 16 c_u + c_l) p'
-      constexpr bool TGTM = MODE == MODE_QTARGET;
-      const float off_g = offset_pv ? (TGTM ? 1032.f : 1024.f) * ps : 0.f;
-      const float off_g8 = offset_pv ? (TGTM ? 1032.f : 64.f) * ps : 0.f;
-      const float sc8 = (offset_pv && !TGTM) ? 0.0625f : 1.0f;
+      for (int a = 0; a < KS; ++a)
 #pragma unroll
-      for (int cm = 0; cm < KS; ++cm) {
-        row[4 + cm * 16 + g] = ((acc[cm][nt][0] + acc[cm][nt][1]) - off_g) + z;
-        row[4 + cm * 16 + g + 8] = fmaf(acc[cm][nt][2] + acc[cm][nt][3], sc8, -off_g8) + z;
-      }
+        for (int e = 0; e < 4; ++e) acc[a][nt][e] = 0.f;
     }
+    if (c_end > c_begin) fp16_region_q<C, HD, NT>(region, bqf, q_s, nq, fk, fv, n_tok, c_begin, c_end, causal, qg, P, st, acc);
+    __syncthreads();
+    if (warp < NCW) merge_rows_quant<C, HD, NT, MODE>(mrg, st, acc, false);
+  } else {
+    constexpr int NTO = C::NTO;
+    Softmax st[NTO];
+    float acc[KS][NTO][4];
+#pragma unroll
+    for (int nt = 0; nt < NTO; ++nt) {
+      st[nt] = {kNegInf, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int a = 0; a < KS; ++a)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[a][nt][e] = 0.f;
+    }
+    if (c_end > c_begin) fp16_region<C, HD, NTO>(region, bqf, q_s, pw, nq, fk, fv, n_tok, c_begin, c_end, causal, qg, P, st, acc);
+    __syncthreads();
+    if (warp < NCW) merge_rows_fp<C, HD, NTO, MODE>(mrg, st, acc, false);
   }
   __syncthreads();
   const size_t hidx = ((size_t)seq * P.Hkv + head) * P.n_qgroups + qg;
@@ -738,10 +1120,10 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE>::THREADS, AttnCfg<HD, NT
   if (tid == 0) P.counters[hidx] = 0;
 }
 
-template <int HD, int NT, int MODE>
+template <int HD, int NT, int MODE, int QR>
 static cudaError_t launch_attn_t(const AttnParams& p, cudaStream_t stream) {
-  using C = AttnCfg<HD, NT, MODE>;
-  auto kern = attn_kernel<HD, NT, MODE>;
+  using C = AttnCfg<HD, NT, MODE, QR>;
+  auto kern = attn_kernel<HD, NT, MODE, QR>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -752,74 +1134,104 @@ static cudaError_t launch_attn_t(const AttnParams& p, cudaStream_t stream) {
   return launch_pdl(kern, grid, dim3(C::THREADS), C::SMEM, stream, p);
 }
 
+// query rows stored per CTA for `per` query columns (quantised, one query tile)
+static inline int attn_qr(int per) { return per <= 1 ? 1 : per <= 2 ? 2 : per <= 4 ? 4 : 8; }
+
 template <int HD, int MODE>
-static cudaError_t launch_attn_nt(const AttnParams& p, int nt, cudaStream_t s) {
-  switch (nt) {
-    case 1: return launch_attn_t<HD, 1, MODE>(p, s);
-    case 2: return launch_attn_t<HD, 2, MODE>(p, s);
-    case 3: return launch_attn_t<HD, 3, MODE>(p, s);
-    default: return cudaErrorInvalidValue;
+static cudaError_t launch_attn_nt(const AttnParams& p, int nt, int per, cudaStream_t s) {
+  if constexpr (MODE == MODE_FP16) {
+    switch (nt) {
+      case 1: return launch_attn_t<HD, 1, MODE, 8>(p, s);
+      case 2: return launch_attn_t<HD, 2, MODE, 8>(p, s);
+      case 3: return launch_attn_t<HD, 3, MODE, 8>(p, s);
+      default: return cudaErrorInvalidValue;
+    }
+  } else if constexpr (MODE == MODE_QDRAFT) {
+    switch (nt) {
+      case 1: return launch_attn_t<HD, 1, MODE, 8>(p, s);
+      case 2: return launch_attn_t<HD, 2, MODE, 8>(p, s);
+      case 3: return launch_attn_t<HD, 3, MODE, 8>(p, s);
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    if (nt == 2) return launch_attn_t<HD, 2, MODE, 8>(p, s);
+    if (nt != 1) return cudaErrorInvalidValue;
+    switch (attn_qr(per)) {
+      case 1: return launch_attn_t<HD, 1, MODE, 1>(p, s);
+      case 2: return launch_attn_t<HD, 1, MODE, 2>(p, s);
+      case 4: return launch_attn_t<HD, 1, MODE, 4>(p, s);
+      default: return launch_attn_t<HD, 1, MODE, 8>(p, s);
+    }
   }
 }
 
 template <int MODE>
-static cudaError_t launch_attn_hd(const AttnParams& p, int nt, cudaStream_t s) {
+static cudaError_t launch_attn_hd(const AttnParams& p, int nt, int per, cudaStream_t s) {
   switch (p.hd) {
-    case 16: return launch_attn_nt<16, MODE>(p, nt, s);
-    case 32: return launch_attn_nt<32, MODE>(p, nt, s);
-    case 64: return launch_attn_nt<64, MODE>(p, nt, s);
-    case 128: return launch_attn_nt<128, MODE>(p, nt, s);
+    case 16: return launch_attn_nt<16, MODE>(p, nt, per, s);
+    case 32: return launch_attn_nt<32, MODE>(p, nt, per, s);
+    case 64: return launch_attn_nt<64, MODE>(p, nt, per, s);
+    case 128: return launch_attn_nt<128, MODE>(p, nt, per, s);
     default: return cudaErrorInvalidValue;
   }
-}
-
-static int attn_nt(const AttnParams& p) {
-  int per = (p.n_queries + p.n_qgroups - 1) / p.n_qgroups;
-  int nt = (per + 3) / 4;
-  return nt < 1 ? 1 : nt;
 }
 
 cudaError_t launch_attention(const AttnParams& p, int mode, cudaStream_t s) {
-  const int nt = attn_nt(p);
+  const int per = (p.n_queries + p.n_qgroups - 1) / p.n_qgroups;
+  const int nt = attention_nt(per, mode);
   switch (mode) {
-    case MODE_QDRAFT: return launch_attn_hd<MODE_QDRAFT>(p, nt, s);
-    case MODE_QTARGET: return launch_attn_hd<MODE_QTARGET>(p, nt, s);
-    case MODE_FP16: return launch_attn_hd<MODE_FP16>(p, nt, s);
+    case MODE_QDRAFT: return launch_attn_hd<MODE_QDRAFT>(p, nt, per, s);
+    case MODE_QTARGET: return launch_attn_hd<MODE_QTARGET>(p, nt, per, s);
+    case MODE_FP16: return launch_attn_hd<MODE_FP16>(p, nt, per, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
-template <int HD, int NT, int MODE>
+template <int HD, int NT, int MODE, int QR>
 static int occ_t() {
-  using C = AttnCfg<HD, NT, MODE>;
-  auto kern = attn_kernel<HD, NT, MODE>;
+  using C = AttnCfg<HD, NT, MODE, QR>;
+  auto kern = attn_kernel<HD, NT, MODE, QR>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess) return -1;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, C::THREADS, C::SMEM) != cudaSuccess) return -1;
   return n;
 }
 
-#define QS_FOR_CFGS(X)                                                                                          \
-  X(16, 1, 0) X(16, 2, 0) X(16, 3, 0) X(32, 1, 0) X(32, 2, 0) X(32, 3, 0) X(64, 1, 0) X(64, 2, 0) X(64, 3, 0)    \
-  X(128, 1, 0) X(128, 2, 0) X(128, 3, 0) X(16, 1, 1) X(16, 2, 1) X(16, 3, 1) X(32, 1, 1) X(32, 2, 1) X(32, 3, 1) \
-  X(64, 1, 1) X(64, 2, 1) X(64, 3, 1) X(128, 1, 1) X(128, 2, 1) X(128, 3, 1) X(16, 1, 2) X(16, 2, 2)            \
-  X(16, 3, 2) X(32, 1, 2) X(32, 2, 2) X(32, 3, 2) X(64, 1, 2) X(64, 2, 2) X(64, 3, 2) X(128, 1, 2) X(128, 2, 2) \
-  X(128, 3, 2)
-
-int attention_occupancy(int hd, int nt, int mode) {
-#define QS_OC(H, N, M) \
-  if (hd == H && nt == N && mode == M) return occ_t<H, N, M>();
-  QS_FOR_CFGS(QS_OC)
-#undef QS_OC
-  return -1;
+template <int HD, int MODE>
+static int occ_h(int per) {
+  const int nt = attention_nt(per, MODE);
+  if constexpr (MODE != MODE_QTARGET) {
+    return nt == 1 ? occ_t<HD, 1, MODE, 8>() : nt == 2 ? occ_t<HD, 2, MODE, 8>() : occ_t<HD, 3, MODE, 8>();
+  } else {
+    if (nt == 2) return occ_t<HD, 2, MODE, 8>();
+    switch (attn_qr(per)) {
+      case 1: return occ_t<HD, 1, MODE, 1>();
+      case 2: return occ_t<HD, 1, MODE, 2>();
+      case 4: return occ_t<HD, 1, MODE, 4>();
+      default: return occ_t<HD, 1, MODE, 8>();
+    }
+  }
 }
 
-int attention_smem_bytes(int hd, int nt, int mode) {
-#define QS_SM(H, N, M) \
-  if (hd == H && nt == N && mode == M) return AttnCfg<H, N, M>::SMEM;
-  QS_FOR_CFGS(QS_SM)
-#undef QS_SM
-  return -1;
+template <int MODE>
+static int occ_m(int hd, int per) {
+  switch (hd) {
+    case 16: return occ_h<16, MODE>(per);
+    case 32: return occ_h<32, MODE>(per);
+    case 64: return occ_h<64, MODE>(per);
+    case 128: return occ_h<128, MODE>(per);
+    default: return -1;
+  }
+}
+
+// resident CTAs per SM of the launch serving `per` query columns per CTA
+int attention_occupancy(int hd, int per, int mode) {
+  switch (mode) {
+    case MODE_QDRAFT: return occ_m<MODE_QDRAFT>(hd, per);
+    case MODE_QTARGET: return occ_m<MODE_QTARGET>(hd, per);
+    case MODE_FP16: return occ_m<MODE_FP16>(hd, per);
+    default: return -1;
+  }
 }
 
 }  // namespace qs

@@ -174,16 +174,15 @@ qs_status qs_kv_dequant_view(const qs_kv_store* st, int seq, int layer, int nblk
 
 int qs_attn_partials_floats(const qs_attn_args* a) {
   int per = (a->n_queries + a->n_qgroups - 1) / a->n_qgroups;
-  int nt = (per + 3) / 4;
-  if (nt < 1) nt = 1;
-  return a->B * a->Hkv * a->n_qgroups * (a->n_main + 2) * nt * 4 * (a->hd + 2);
+  int nq = 0;
+  for (int m = 0; m < 3; ++m) {  // one scratch layout serves every view
+    int v = qs::attention_queries_per_cta(per, m);
+    if (v > nq) nq = v;
+  }
+  return a->B * a->Hkv * a->n_qgroups * (a->n_main + 2) * nq * (a->hd + 2);
 }
 
-int qs_attn_occupancy(int hd, int n_query_cols, int mode) {
-  int nt = (n_query_cols + 3) / 4;
-  if (nt < 1) nt = 1;
-  return qs::attention_occupancy(hd, nt, mode);
-}
+int qs_attn_occupancy(int hd, int n_query_cols, int mode) { return qs::attention_occupancy(hd, n_query_cols, mode); }
 
 qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream) {
   if (!a) QS_FAIL(QS_ERR_CONFIG, "null args");

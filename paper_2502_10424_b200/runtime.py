@@ -274,9 +274,10 @@ class Runner:
         ncols_q = self.max_T * r
         self.n_qgroups_max = max(1, -(-ncols_q // 12))
         per = -(-ncols_q // self.n_qgroups_max)
-        nt = max(1, -(-per // 4))
+        # queries per CTA: 8 per tile in the quantised views, 4 in the fp16 view (qs_attn_partials_floats)
+        nq_cta = max(8 * max(1, -(-per // 8)), 4 * max(1, -(-per // 4)))
         max_splits = attn_splits or max(1, min(self.max_chunks, 4 * SM_COUNT))
-        nparts = self.B * geo.num_kv_heads * self.n_qgroups_max * (max_splits + 2) * nt * 4 * (geo.head_dim + 2)
+        nparts = self.B * geo.num_kv_heads * self.n_qgroups_max * (max_splits + 2) * nq_cta * (geo.head_dim + 2)
         self.partials = torch.zeros(nparts, dtype=torch.float32, device=dev)
         self.attn_counters = torch.zeros(self.B * geo.num_kv_heads * self.n_qgroups_max, dtype=torch.int32, device=dev)
         self.fp_cps = 0
