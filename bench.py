@@ -447,16 +447,18 @@ def main():
         barrier()
         wall = time.time() - t_all
     head = res.get("both") or res.get("kv_only")
-    # max over ranks of the per-step time -> whole-job throughput
-    vals = torch.tensor([head["ms_per_step"], head["tok_s"], head["e2e_tok_s"]], dtype=torch.float64, device="cuda")
+    # whole-job throughput: tokens emitted on all ranks / the slowest rank's device time
+    emitted = head["tok_s"] * head["ms_per_step"] * args.steps / 1e3
+    e2e_s = emitted / head["e2e_tok_s"]
+    vals = torch.tensor([head["ms_per_step"], e2e_s, emitted], dtype=torch.float64, device="cuda")
     if world > 1:
         t = vals.clone()
-        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[:2], op=dist.ReduceOp.MAX)
         s2 = vals.clone()
         dist.all_reduce(s2, op=dist.ReduceOp.SUM)
         ms = float(t[0])
-        value = float(s2[1])
-        e2e = float(s2[2])
+        value = float(s2[2]) / (ms * args.steps / 1e3)
+        e2e = float(s2[2]) / float(t[1])
     else:
         ms, value, e2e = head["ms_per_step"], head["tok_s"], head["e2e_tok_s"]
     if rank != 0:
