@@ -115,6 +115,7 @@ typedef struct {
   const int* pos_base;/* [B] position of row_base (seq_len)         */
   const void* rope;   /* float2 [max_pos][hd/2] (cos, sin)           */
   int max_pos;
+  int dbg;            /* 0; diagnostic bits (1: consumers skip the MMA work, 2: no tile reduction) */
 } qs_linear_args;
 
 /* KV store descriptor (device pointers + geometry), Q/cache.py:42-133 */

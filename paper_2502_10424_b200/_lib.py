@@ -13,7 +13,7 @@ import os
 from . import errors
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libqsb200.so")
+LIB_PATH = os.environ.get("QS_LIB") or os.path.join(_PKG, "libqsb200.so")  # QS_LIB: A/B builds
 
 VIEW_DRAFT, VIEW_TARGET, VIEW_FP16 = 0, 1, 2
 EPI_STORE, EPI_ADD, EPI_QKV, EPI_SILU_MUL = 0, 1, 2, 3
@@ -51,7 +51,7 @@ class LinearArgs(C.Structure):
         ("work", vp), ("counters", vp),
         ("Nq", i32), ("Nk", i32), ("hd", i32), ("T", i32),
         ("q_out", vp), ("k_dst", vp), ("v_dst", vp), ("kv_seq_stride", i64), ("kv_head_stride", i64),
-        ("row_base", vp), ("row_offset", i32), ("pos_base", vp), ("rope", vp), ("max_pos", i32),
+        ("row_base", vp), ("row_offset", i32), ("pos_base", vp), ("rope", vp), ("max_pos", i32), ("dbg", i32),
     ]
 
 

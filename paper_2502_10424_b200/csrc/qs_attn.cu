@@ -1092,12 +1092,10 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
     }
     part[i] = v;
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) *ticket_s = atomicAdd(&P.counters[hidx], 1);
+  __syncthreads();  // every partial store before thread 0's release-acquire ticket (cumulative)
+  if (tid == 0) *ticket_s = atom_add_acq_rel_gpu(&P.counters[hidx], 1);
   __syncthreads();
   if (*ticket_s != n_split_tot - 1) return;
-  __threadfence();
   // ===================== last CTA of the head: merge splits in fixed order =====================
   const float* allp = P.partials + hidx * n_split_tot * (size_t)NQ * (HD + 2);
   for (int i = tid; i < nq * HD; i += NTH) {

@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
     const int mt = mg * 4 + warp;
     const uint8_t* sp = sm + s * C::STAGE;
     mbar_wait(&full_b[s], (i / C::NSTAGE) & 1);
-    if (mt < MT) {
+    if (mt < MT && !(P.dbg & 1)) {
       // B fragments: row r = activation column; columns >= ncols read stale shared memory,
       // which only ever reaches the matching (discarded) output columns of the MMA.
       const uint8_t* bst = sp + C::OFF_B + g * C::BROW + 4 * t4;
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
 
     // ---- tile boundary: publish this CTA's partial of 64-row tile mg ----
     const bool last_unit_of_tile = (kc == KC - 1) || (i == nunits - 1);
-    if (!last_unit_of_tile) continue;
+    if (!last_unit_of_tile || (P.dbg & 2)) continue;
     const long long cf = cta_of_unit((long long)mg * KC, U, Cn);
     const long long cl = cta_of_unit((long long)mg * KC + KC - 1, U, Cn);
     const int ncontrib = (int)(cl - cf + 1);
@@ -406,12 +406,12 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
         acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
       }
     }
-    __threadfence();
+    // the CTA barrier orders every consumer thread's partial before thread 0's release-acquire
+    // ticket (cumulative), and the winner's acquire before the other threads' reads
     asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
-    if (tid == 0) *flag = atomicAdd(&P.counters[mg], 1) == ncontrib - 1;
+    if (tid == 0) *flag = atom_add_acq_rel_gpu(&P.counters[mg], 1) == ncontrib - 1;
     asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
     if (!*flag) continue;
-    __threadfence();
     const int row0 = mg * 64;
     const int nthr = C::NCW * 32;
     for (int e = tid; e < 64 * ncols; e += nthr) {

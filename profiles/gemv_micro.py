@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--nctas", type=int, default=0)
     ap.add_argument("--modes", default="f16,int4")
     ap.add_argument("--copies", type=int, default=4, help="distinct weight copies rotated (defeats L2)")
+    ap.add_argument("--dbg", type=int, default=0, help="diagnostic bits (1: consumers skip the MMA work)")
     a = ap.parse_args()
     peak = 6542.1
     for mode in a.modes.split(","):
@@ -83,6 +84,7 @@ def main():
                     ar.xh, ar.ldxh, ar.xs, ar.ldxs = xh.data_ptr(), xh.shape[1], xs.data_ptr(), xs.shape[1]
                     ar.y, ar.ldy = y.data_ptr(), N
                     ar.work, ar.counters = work.data_ptr(), cnt.data_ptr()
+                    ar.dbg = a.dbg
                     args.append(ar)
                 lib = _lib.load()
                 it = [0]
