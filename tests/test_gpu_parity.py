@@ -268,6 +268,32 @@ def test_attention_vs_oracle(H, hd, G, n_prompt, view, T):
         assert err <= 2e-3 * vmax, (t, err)
 
 
+@pytest.mark.parametrize("view", ["draft", "target"])
+@pytest.mark.parametrize("T", [1, 2, 5])
+def test_attention_gqa_vs_oracle(view, T):
+    """GQA (config 4 shape class): r query heads share one KV head.  The oracle has no GQA
+    model; it is restated by repeating each KV head r times.  Covers the
+    query-row variants of the target kernel (1-8 rows per CTA and two query tiles) and
+    the draft's 1-3 column tiles."""
+    H, hd, G, r = 2, 128, 128, 4
+    cache, orc, rk, rv, rng = _attn_setup(H, hd, G, 3 * 128 + 70, T, seed=40 + T, r=r)
+    base = cache.fp2_len
+    for t in range(T):
+        cache.fp_k[0, 0, 1, :, base + t] = torch.from_numpy(rk[t]).cuda().half().reshape(H, hd)
+        cache.fp_v[0, 0, 1, :, base + t] = torch.from_numpy(rv[t]).cuda().half().reshape(H, hd)
+    q = (rng.standard_normal((T, H * r, hd)) * 2.0).astype(np.float32)
+    got = _run_attention(cache, q, _lib.VIEW_DRAFT if view == "draft" else _lib.VIEW_TARGET, T)
+    for t in range(T):
+        orc.append_decode_token(0, rk[t], rv[t])
+        vw = orc.view(0, view)
+        segs = [(np.repeat(k.reshape(-1, H, hd), r, axis=1), np.repeat(v.reshape(-1, H, hd), r, axis=1))
+                for k, v in vw.segments]
+        want = O.merged_attention(q[t], segs, 1.0 / np.sqrt(hd))
+        vmax = float(np.abs(vw.v).max())
+        err = np.abs(got[t].reshape(H * r, hd) - want).max()
+        assert err <= 2e-3 * vmax, (t, err)
+
+
 def test_attention_batch_invariance_bit_exact():
     """Row t of a T-row launch == the same row launched alone at its position."""
     H, hd, G = 4, 128, 128
