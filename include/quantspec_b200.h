@@ -78,6 +78,12 @@ typedef struct {
   float* partials;       /* scratch */
   int* counters;         /* [B*Hkv*n_qgroups] zero-initialised */
   int dbg;               /* 0; diagnostic bits (1: skip consumer math, 2: skip producer fold) */
+  /* optional fused hand-off to the output projection (the qs_prep_act layout, no norm):
+   * f16 copy [B*T][ld_out_h] and f32 sums of every 16 f16 values [B*T][ld_out_s]; NULL = off */
+  void* out_h;
+  int64_t ld_out_h;
+  float* out_s;
+  int64_t ld_out_s;
 } qs_attn_args;
 
 /* x @ W with fused epilogue.  Replaces the fp32 `h @ W` products of

@@ -39,6 +39,7 @@ class AttnArgs(C.Structure):
         ("main_k", vp), ("main_v", vp), ("main_seq_stride", i64), ("main_head_stride", i64),
         ("fp1_k", vp), ("fp1_v", vp), ("fp2_k", vp), ("fp2_v", vp), ("fp_seq_stride", i64),
         ("partials", vp), ("counters", vp), ("dbg", i32),
+        ("out_h", vp), ("ld_out_h", i64), ("out_s", vp), ("ld_out_s", i64),
     ]
 
 

@@ -1098,22 +1098,42 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
   if (*ticket_s != n_split_tot - 1) return;
   // ===================== last CTA of the head: merge splits in fixed order =====================
   const float* allp = P.partials + hidx * n_split_tot * (size_t)NQ * (HD + 2);
-  for (int i = tid; i < nq * HD; i += NTH) {
-    const int q = i / HD, c = i % HD;
-    float mx = kNegInf;
-    for (int s = 0; s < n_split_tot; ++s) mx = fmaxf(mx, __ldcg(allp + ((size_t)s * NQ + q) * (HD + 2)));
-    float num = 0.f, den = 0.f;
-    if (mx != kNegInf) {
-      for (int s = 0; s < n_split_tot; ++s) {
-        const float* pr = allp + ((size_t)s * NQ + q) * (HD + 2);
-        const float f = exp2f(__ldcg(pr) - mx);
-        den += f * __ldcg(pr + 1);
-        num += f * __ldcg(pr + 2 + c);
+  // all lanes run every round (whole 16-channel groups are valid or not together) so the
+  // optional f16 copy + 16-sums for the output projection can reduce with shuffles
+  for (int base = 0; base < nq * HD; base += NTH) {
+    const int i = base + tid;
+    const bool valid = i < nq * HD;
+    const int q = valid ? i / HD : 0, c = i % HD;
+    float o = 0.f;
+    if (valid) {
+      float mx = kNegInf;
+      for (int s = 0; s < n_split_tot; ++s) mx = fmaxf(mx, __ldcg(allp + ((size_t)s * NQ + q) * (HD + 2)));
+      float num = 0.f, den = 0.f;
+      if (mx != kNegInf) {
+        for (int s = 0; s < n_split_tot; ++s) {
+          const float* pr = allp + ((size_t)s * NQ + q) * (HD + 2);
+          const float f = exp2f(__ldcg(pr) - mx);
+          den += f * __ldcg(pr + 1);
+          num += f * __ldcg(pr + 2 + c);
+        }
       }
+      o = den > 0.f ? num / den : 0.f;
     }
     const int qgl = qg * NQ + q;
     const int t = qgl / P.r, j = qgl - t * P.r;
-    P.out[((size_t)seq * P.T + t) * P.q_row_stride + (size_t)(head * P.r + j) * HD + c] = den > 0.f ? num / den : 0.f;
+    const size_t row = (size_t)seq * P.T + t;
+    const size_t col = (size_t)(head * P.r + j) * HD + c;
+    if (valid) P.out[row * P.q_row_stride + col] = o;
+    if (P.out_h) {
+      const __half h = __float2half_rn(o);
+      float sm16 = __half2float(h);
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) sm16 += __shfl_xor_sync(0xffffffffu, sm16, off);
+      if (valid) {
+        reinterpret_cast<__half*>(P.out_h)[row * P.ld_out_h + col] = h;
+        if ((c & 15) == 0) P.out_s[row * P.ld_out_s + col / 16] = sm16;
+      }
+    }
   }
   if (tid == 0) P.counters[hidx] = 0;
 }

@@ -388,6 +388,9 @@ class Runner:
             a.sm_scale_log2 = float(1.4426950408889634 / math.sqrt(geo.head_dim))
             a.q, a.out, a.q_row_stride = self.q.data_ptr(), self.attn.data_ptr(), geo.nq
             a.partials, a.counters = self.partials.data_ptr(), self.attn_counters.data_ptr()
+            # fused hand-off: the merge writes the O projection's f16 input + 16-sums (no prep launch)
+            a.out_h, a.ld_out_h = self.xh.data_ptr(), self.xh.shape[1]
+            a.out_s, a.ld_out_s = self.xs.data_ptr(), self.xs.shape[1]
             if self.is_fp:
                 a.G = 64
                 a.fp_len = c.d_len.data_ptr()
@@ -445,8 +448,7 @@ class Runner:
         for li, lw in enumerate(w.layers):
             self._prep(self.x, w.attn_norms[li], X, ncols, s)
             self._linear(lw["qkv"], X, None, ncols, _lib.EPI_QKV, layer=li, T=T, row_offset=row_offset, stream=s)
-            self._attention(li, view, T, row_offset, s)
-            self._prep(self.attn, None, X, ncols, s)
+            self._attention(li, view, T, row_offset, s)  # also writes X = (f16, 16-sums) of its output
             self._linear(lw["o"], X, self.x, ncols, _lib.EPI_ADD, stream=s)
             self._prep(self.x, w.mlp_norms[li], X, ncols, s)
             self._linear(lw["gu"], X, None, ncols, _lib.EPI_SILU_MUL, yh=H, stream=s)
@@ -457,4 +459,4 @@ class Runner:
             _lib.check(lib.qs_argmax(self.logits.data_ptr(), ncols, geo.vocab, argmax_to, 1, s), "qs_argmax")
 
     def kernel_launches_per_forward(self, nlayers: int) -> int:
-        return 1 + nlayers * 8 + 3
+        return 1 + nlayers * 7 + 3
