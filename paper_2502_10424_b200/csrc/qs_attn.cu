@@ -91,10 +91,16 @@ struct AttnCfg {
   static constexpr int S2 = (233472 / 2 - 1024 - FIXED) / QSTAGE;
   static constexpr int S1 = (232448 - FIXED) / QSTAGE;
   static constexpr int MIN_BLOCKS = QUANT ? ((NT == 1 && S2 >= 4) ? 2 : 1) : 3;  // wide launches: registers
-  static constexpr int NSTAGE = QUANT ? (MIN_BLOCKS == 2 ? (S2 < 6 ? S2 : 6) : (S1 < 6 ? S1 : 6)) : 1;
-  // producer warps (TMA issue + query-scale fold); each folds whole chunks, NPW < NSTAGE
-  static constexpr int NPW = QUANT ? (NSTAGE > 2 ? 2 : 1) : 0;
-  static constexpr int NWARPS = NCW + NPW;
+  // TMAW (one CTA per SM, the target's wide fold): a dedicated TMA warp refills each stage as
+  // soon as the consumers release it, and NPW = NSTAGE fold warps each own one stage -- every
+  // mbarrier's phases are then waited in order by a single warp, so a parity wait can never
+  // run a phase ahead.  Otherwise (two CTAs per SM, or the draft's cheap fold) two fold warps
+  // alternate chunks and refill the ring themselves behind the consumers.
+  static constexpr bool TMAW = ROWQ && MIN_BLOCKS == 1;
+  static constexpr int NSTAGE =
+      QUANT ? (MIN_BLOCKS == 2 ? (S2 < 6 ? S2 : 6) : TMAW ? (S1 < 4 ? S1 : 4) : (S1 < 6 ? S1 : 6)) : 1;
+  static constexpr int NPW = QUANT ? (TMAW ? NSTAGE : (NSTAGE > 2 ? 2 : 1)) : 0;
+  static constexpr int NWARPS = NCW + (TMAW ? 1 : 0) + NPW;
   static constexpr int THREADS = NWARPS * 32;
   static constexpr int REGION_Q = QUANT ? NSTAGE * QSTAGE : 0;
   static constexpr int R0 = REGION_Q > REGION_F ? REGION_Q : REGION_F;
@@ -512,8 +518,20 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
 
   if (warp >= C::NCW) {
     // ======================= producer warps (NPW) =======================
-    const int pwid = warp - C::NCW;
     auto issue = [&](int i) { quant_issue<C, HD, MODE>(P, region, tma_b, seq, head, n_blocks, c_begin, i); };
+    if constexpr (C::TMAW) {
+      if (warp == C::NCW) {
+        // dedicated TMA warp: chunk c >= S goes into the stage chunk c - S vacated (whole warp
+        // loops, lane 0 issues, so it reaches the kernel's CTA barriers converged)
+        for (int c = S; c < nchunk; ++c) {
+          mbar_wait(&empty_b[c % S], ((c - S) / S) & 1);
+          if (lane == 0) issue(c);
+          __syncwarp();
+        }
+        return;
+      }
+    }
+    const int pwid = warp - C::NCW - (C::TMAW ? 1 : 0);
     // Producer warp p folds whole chunks j = p (mod NPW) on its own (no inter-warp
     // synchronisation: the per-chunk fold is a latency chain, so independent warps
     // overlap it), then refills the stage of its previous chunk once the consumers
@@ -623,7 +641,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       if (lane == 0) mbar_arrive(&full_b[s]);
       // refill the stage of this warp's previous chunk (every chunk >= S is issued exactly once)
       const int jp = j - NPW;
-      if (jp >= 0 && jp + S < nchunk) {
+      if (!C::TMAW && jp >= 0 && jp + S < nchunk) {
         mbar_wait(&empty_b[jp % S], (jp / S) & 1);
         if (lane == 0) issue(jp + S);
       }
