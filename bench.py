@@ -186,20 +186,23 @@ def build_workload(args, dev_index: int):
     return geo, fw, qw, hcache, fcache, first, setup_s
 
 
-def time_kernel(fn, iters: int = 20):
-    """Average device time of fn() over iters launches (CUDA events on the launching stream)."""
+def time_kernel(fn, iters: int = 21):
+    """Median device time of fn() (CUDA events around each launch on the launching stream;
+    the event between launches also keeps consecutive launches from overlapping via PDL)."""
+    import statistics
+
     import torch
 
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(iters):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for s, e in ev:
+        s.record()
         fn()
-    e.record()
+        e.record()
     torch.cuda.synchronize()
-    return s.elapsed_time(e) / iters / 1e3
+    return statistics.median(s.elapsed_time(e) for s, e in ev) / 1e3
 
 
 def kernel_roofline(geo, fw, qw, hcache, fcache, peak):

@@ -1132,15 +1132,37 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
     const int q = valid ? i / HD : 0, c = i % HD;
     float o = 0.f;
     if (valid) {
+      // every split's (m, l, acc[c]) requested at once, 16 splits per round (one L2 round trip
+      // per round instead of one per split); combined in split order
       float mx = kNegInf;
-      for (int s = 0; s < n_split_tot; ++s) mx = fmaxf(mx, __ldcg(allp + ((size_t)s * NQ + q) * (HD + 2)));
+      for (int s0 = 0; s0 < n_split_tot; s0 += 16) {
+        float mv[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          mv[j] = s0 + j < n_split_tot ? __ldcg(allp + ((size_t)(s0 + j) * NQ + q) * (HD + 2)) : kNegInf;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mx = fmaxf(mx, mv[j]);
+      }
       float num = 0.f, den = 0.f;
       if (mx != kNegInf) {
-        for (int s = 0; s < n_split_tot; ++s) {
-          const float* pr = allp + ((size_t)s * NQ + q) * (HD + 2);
-          const float f = exp2f(__ldcg(pr) - mx);
-          den += f * __ldcg(pr + 1);
-          num += f * __ldcg(pr + 2 + c);
+        for (int s0 = 0; s0 < n_split_tot; s0 += 16) {
+          float mv[16], lv[16], av[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const bool ok = s0 + j < n_split_tot;
+            const float* pr = allp + ((size_t)(s0 + j) * NQ + q) * (HD + 2);
+            mv[j] = ok ? __ldcg(pr) : kNegInf;
+            lv[j] = ok ? __ldcg(pr + 1) : 0.f;
+            av[j] = ok ? __ldcg(pr + 2 + c) : 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (s0 + j < n_split_tot) {
+              const float f = exp2f(mv[j] - mx);
+              den += f * lv[j];
+              num += f * av[j];
+            }
+          }
         }
       }
       o = den > 0.f ? num / den : 0.f;

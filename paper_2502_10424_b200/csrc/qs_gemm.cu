@@ -416,8 +416,17 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
     const int nthr = C::NCW * 32;
     for (int e = tid; e < 64 * ncols; e += nthr) {
       const int r = e % 64, c = e / 64;
+      const float* src = P.work + ((size_t)mg * P.maxc * kMaxCols + c) * 64 + r;
+      // all partials in flight at once (one L2 round trip, not ncontrib), summed in slot order
       float a = 0.f;
-      for (int q = 0; q < ncontrib; ++q) a = a + __ldcg(P.work + (((size_t)mg * P.maxc + q) * kMaxCols + c) * 64 + r);
+      for (int q0 = 0; q0 < ncontrib; q0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = q0 + j < ncontrib ? __ldcg(src + (size_t)(q0 + j) * kMaxCols * 64) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (q0 + j < ncontrib) a = a + v[j];
+      }
       ysm[r * COLS + c] = a;
     }
     asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
