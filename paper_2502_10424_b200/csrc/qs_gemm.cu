@@ -205,6 +205,82 @@ __device__ __forceinline__ void int4_unit(const uint4* __restrict__ wa, const ui
   }
 }
 
+// Fused epilogue over an nrows x ncols tile of results (ysm[r * COLS + c]) starting at output row
+// row0, run by the NTH consumer threads: store / residual add / SiLU*up -> f16 + 16-sums
+// (16-row tiles interleaved gate, up) / q,k RoPE + q store + k,v append.
+template <int EPI, int COLS, int NTH>
+__device__ __forceinline__ void linear_epilogue(const LinearParams& P, float* ysm, int row0, int nrows, int tid,
+                                                int ncols) {
+  constexpr int nthr = NTH;
+  if constexpr (EPI == QS_EPI_STORE || EPI == QS_EPI_ADD) {
+    for (int e = tid; e < nrows * ncols; e += nthr) {
+      const int r = e % nrows, c = e / nrows;
+      const int n = row0 + r;
+      if (n >= P.N) continue;
+      const float v = ysm[r * COLS + c];
+      float* dst = P.y + (size_t)c * P.ldy + n;
+      if (EPI == QS_EPI_ADD) *dst = __fadd_rn(*dst, v);
+      else *dst = v;
+    }
+  } else if constexpr (EPI == QS_EPI_SILU_MUL) {
+    // 16-row tiles interleaved: local tiles (2p, 2p+1) = (gate, up) of output tile row0/32 + p;
+    // output: f16 input of the down projection + its 16-sums (one sum per output tile)
+    for (int e = tid; e < (nrows / 2) * ncols; e += nthr) {
+      const int rr = e % (nrows / 2), c = e / (nrows / 2);
+      const int pair = rr / 16, r16 = rr % 16;
+      const int rg = pair * 32 + r16, ru = rg + 16;
+      if (row0 + rg >= P.N) continue;
+      const int n = (row0 / 32 + pair) * 16 + r16;
+      const float h = __fmul_rn(silu_f32(ysm[rg * COLS + c]), ysm[ru * COLS + c]);
+      const __half hh = __float2half_rn(h);
+      reinterpret_cast<__half*>(P.yh)[(size_t)c * P.ldyh + n] = hh;
+      if (P.y) P.y[(size_t)c * P.ldy + n] = h;
+      ysm[rg * COLS + c] = __half2float(hh);  // gate slot now holds the f16-rounded output
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(NTH));
+    for (int e = tid; e < (nrows / 32) * ncols; e += nthr) {
+      const int pair = e % (nrows / 32), c = e / (nrows / 32);
+      if (row0 + pair * 32 >= P.N) continue;
+      float a = 0.f;
+      for (int r16 = 0; r16 < 16; ++r16) a += ysm[(pair * 32 + r16) * COLS + c];
+      P.ys[(size_t)c * P.ldys + row0 / 32 + pair] = a;
+    }
+  } else if constexpr (EPI == QS_EPI_QKV) {
+    const float2* rope = reinterpret_cast<const float2*>(P.rope);
+    const int hd = P.hd;
+    for (int e = tid; e < (nrows / 2) * ncols; e += nthr) {
+      const int pr = e % (nrows / 2), c = e / (nrows / 2);
+      const int r = 2 * pr;
+      const int n = row0 + r;
+      if (n >= P.N) continue;
+      const int sq = c / P.T, t = c % P.T;
+      float ev = ysm[r * COLS + c], ov = ysm[(r + 1) * COLS + c];
+      if (n < P.Nq + P.Nk) {
+        const int nn = n < P.Nq ? n : n - P.Nq;
+        const int d = nn % hd;
+        const int pos = P.pos_base[sq] + P.row_offset + t;
+        const float2 cs = rope[(size_t)pos * (hd / 2) + d / 2];
+        const float e2 = __fsub_rn(__fmul_rn(ev, cs.x), __fmul_rn(ov, cs.y));
+        const float o2 = __fadd_rn(__fmul_rn(ev, cs.y), __fmul_rn(ov, cs.x));
+        ev = e2;
+        ov = o2;
+      }
+      if (n < P.Nq) {
+        P.q_out[(size_t)c * P.Nq + n] = ev;
+        P.q_out[(size_t)c * P.Nq + n + 1] = ov;
+      } else {
+        const bool isk = n < P.Nq + P.Nk;
+        const int nn = isk ? n - P.Nq : n - P.Nq - P.Nk;
+        const int head = nn / hd, d = nn % hd;
+        const int row = P.row_base[sq] + P.row_offset + t;
+        __half* dst = reinterpret_cast<__half*>(isk ? P.k_dst : P.v_dst) + (size_t)sq * P.kv_seq_stride +
+                      (size_t)head * P.kv_head_stride + (size_t)row * hd + d;
+        *reinterpret_cast<__half2*>(dst) = __floats2half2_rn(ev, ov);
+      }
+    }
+  }
+}
+
 template <int WMODE, int NTC, int EPI, int GKS, int CW>
 __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_kernel(const __grid_constant__ LinearParams P) {
   using C = LinCfg<WMODE, NTC, GKS, CW>;
@@ -433,75 +509,305 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
     if (tid == 0) P.counters[mg] = 0;
 
     // ---- fused epilogue over the 64 x ncols tile ----
-    if constexpr (EPI == QS_EPI_STORE || EPI == QS_EPI_ADD) {
-      for (int e = tid; e < 64 * ncols; e += nthr) {
-        const int r = e % 64, c = e / 64;
-        const int n = row0 + r;
-        if (n >= P.N) continue;
-        const float v = ysm[r * COLS + c];
-        float* dst = P.y + (size_t)c * P.ldy + n;
-        if (EPI == QS_EPI_ADD) *dst = __fadd_rn(*dst, v);
-        else *dst = v;
-      }
-    } else if constexpr (EPI == QS_EPI_SILU_MUL) {
-      // m-tiles interleaved: local tiles (0,1) = (gate, up) of output tile 2*mg, (2,3) of 2*mg+1;
-      // output: f16 input of the down projection + its 16-sums (one sum per output tile)
-      for (int e = tid; e < 32 * ncols; e += nthr) {
-        const int rr = e % 32, c = e / 32;
-        const int pair = rr / 16, r16 = rr % 16;
-        const int rg = pair * 32 + r16, ru = rg + 16;
-        if (row0 + rg >= P.N) continue;
-        const int n = (mg * 2 + pair) * 16 + r16;
-        const float h = __fmul_rn(silu_f32(ysm[rg * COLS + c]), ysm[ru * COLS + c]);
-        const __half hh = __float2half_rn(h);
-        reinterpret_cast<__half*>(P.yh)[(size_t)c * P.ldyh + n] = hh;
-        if (P.y) P.y[(size_t)c * P.ldy + n] = h;
-        ysm[rg * COLS + c] = __half2float(hh);  // gate slot now holds the f16-rounded output
-      }
-      asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
-      for (int e = tid; e < 2 * ncols; e += nthr) {
-        const int pair = e % 2, c = e / 2;
-        if (row0 + pair * 32 >= P.N) continue;
-        float a = 0.f;
-        for (int r16 = 0; r16 < 16; ++r16) a += ysm[(pair * 32 + r16) * COLS + c];
-        P.ys[(size_t)c * P.ldys + mg * 2 + pair] = a;
-      }
-    } else if constexpr (EPI == QS_EPI_QKV) {
-      const float2* rope = reinterpret_cast<const float2*>(P.rope);
-      const int hd = P.hd;
-      for (int e = tid; e < 32 * ncols; e += nthr) {
-        const int pr = e % 32, c = e / 32;
-        const int r = 2 * pr;
-        const int n = row0 + r;
-        if (n >= P.N) continue;
-        const int sq = c / P.T, t = c % P.T;
-        float ev = ysm[r * COLS + c], ov = ysm[(r + 1) * COLS + c];
-        if (n < P.Nq + P.Nk) {
-          const int nn = n < P.Nq ? n : n - P.Nq;
-          const int d = nn % hd;
-          const int pos = P.pos_base[sq] + P.row_offset + t;
-          const float2 cs = rope[(size_t)pos * (hd / 2) + d / 2];
-          const float e2 = __fsub_rn(__fmul_rn(ev, cs.x), __fmul_rn(ov, cs.y));
-          const float o2 = __fadd_rn(__fmul_rn(ev, cs.y), __fmul_rn(ov, cs.x));
-          ev = e2;
-          ov = o2;
-        }
-        if (n < P.Nq) {
-          P.q_out[(size_t)c * P.Nq + n] = ev;
-          P.q_out[(size_t)c * P.Nq + n + 1] = ov;
-        } else {
-          const bool isk = n < P.Nq + P.Nk;
-          const int nn = isk ? n - P.Nq : n - P.Nq - P.Nk;
-          const int head = nn / hd, d = nn % hd;
-          const int row = P.row_base[sq] + P.row_offset + t;
-          __half* dst = reinterpret_cast<__half*>(isk ? P.k_dst : P.v_dst) + (size_t)sq * P.kv_seq_stride +
-                        (size_t)head * P.kv_head_stride + (size_t)row * hd + d;
-          *reinterpret_cast<__half2*>(dst) = __floats2half2_rn(ev, ov);
+    linear_epilogue<EPI, COLS, C::NCW * 32>(P, ysm, row0, 64, tid, ncols);
+    asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));  // ysm reuse by the next tile
+  }
+}
+
+// ---------------------------------------------------------------------------
+// INT4 W4A16 GEMV/GEMM without cross-CTA reduction (the draft's weights).
+//
+// One CTA owns a pair of 16-row tiles (32 output rows; for the gate/up projection exactly
+// the (gate, up) rows of one output tile) over the FULL K range, so no tile spans CTAs:
+// the stream-K fix-up (partials through L2, a ticket, the last CTA's reduction) was the
+// limiter of these short INT4 launches.  Weights are stored pair-major
+// ([pair][k-quad][2 tiles][32 lanes][16 B], params [pair][group][2 tiles][8][float4]), so
+// a 64-k-step stage of a pair is one contiguous bulk copy of codes and one of params.
+// Warps 0-3: tile w&1, k-half w>>1 of every stage; the two k-halves of a tile are summed
+// through shared memory at the end (fixed order).  Grid = N/32 CTAs: small CTAs keep the
+// SMs balanced, and PDL overlaps each CTA's first weight stages with the previous kernel.
+// ---------------------------------------------------------------------------
+template <int NTC, int GKS, int CW>
+struct I4Cfg {
+  static constexpr int NCW = 4;
+  static constexpr int THREADS = (NCW + 1) * 32;
+  static constexpr int KCH = 64;                                  // k-steps per stage
+  static constexpr int HKS = KCH / 2;                             // k-steps per consumer warp per stage
+  static constexpr int WBYTES = (KCH / 4) * 2 * 512;              // codes of both tiles
+  static constexpr int ROWS = NTC == 1 ? CW : 16;
+  static constexpr int BROW = KCH * 32 + 16;
+  static constexpr int PBYTES = (KCH / GKS) * 2 * 128;            // {S,Z} x 16 rows x 2 tiles per group
+  static constexpr int XROW = KCH * 4 + 16;
+  static constexpr int OFF_B = WBYTES;
+  static constexpr int OFF_P = OFF_B + ROWS * BROW;
+  static constexpr int OFF_X = OFF_P + PBYTES;
+  static constexpr int STAGE = (OFF_X + ROWS * XROW + 127) / 128 * 128;
+  static constexpr int NSTAGE = 3;
+  static constexpr int YCOLS = 8 * NTC;
+  static constexpr int SMEM = NSTAGE * STAGE + 2 * 32 * YCOLS * 4 + 2 * NSTAGE * 8 + 16;
+};
+
+// HKS k-steps of one 16-row tile for one consumer warp (window / group-slot scheme of
+// int4_unit; pair-major strides).  wa: this lane's first uint4 of the k-range; bbase: B rows
+// at the k-range; pp: float4 params of the first group (this tile, row g); xsm: 16-sums.
+template <class C, int NTC, int GKS, int CW>
+__device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uint8_t* bbase, const float4* pp,
+                                         const float* xsm, const int nks, const int g, const int t4,
+                                         float (&acc)[NTC][4]) {
+  constexpr int G8 = 8 / CW;
+  constexpr int WIN = (G8 * GKS < C::HKS) ? G8 * GKS : C::HKS;  // k-steps per window
+  constexpr int NSLOT = WIN / GKS;
+  constexpr int XW = C::XROW / 4;
+  const int my_slot = g / CW;
+#pragma unroll
+  for (int w = 0; w < C::HKS / WIN; ++w) {
+    const int k0 = w * WIN;
+    if (k0 >= nks) break;
+    float D2[2][NTC][4];
+#pragma unroll
+    for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+      for (int nt = 0; nt < NTC; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) D2[c2][nt][e] = 0.f;
+#pragma unroll
+    for (int sl = 0; sl < NSLOT; ++sl) {
+      const bool mine = my_slot == sl;
+      const uint8_t* brow[NTC];
+#pragma unroll
+      for (int nt = 0; nt < NTC; ++nt) brow[nt] = bbase + (nt * 8 + g % CW) * C::BROW + 4 * t4;
+#pragma unroll
+      for (int j = 0; j < GKS; ++j) {
+        const int ks = k0 + sl * GKS + j;
+        if (ks < nks) {
+          const uint4 w4 = wa[(ks >> 2) * 64];
+          const uint32_t wv = (ks & 3) == 0 ? w4.x : (ks & 3) == 1 ? w4.y : (ks & 3) == 2 ? w4.z : w4.w;
+          uint32_t a[4];
+          unpack_u4_raw(wv, a);
+#pragma unroll
+          for (int nt = 0; nt < NTC; ++nt) {
+            uint32_t b0 = 0u, b1 = 0u;
+            if (mine) {
+              b0 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32);
+              b1 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32 + 16);
+            }
+            mma_acc(D2[(sl * GKS + j) & 1][nt], a, b0, b1);
+          }
         }
       }
     }
-    asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));  // ysm reuse by the next tile
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt) {
+      float D[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) D[e] = __fadd_rn(D2[0][nt][e], D2[1][nt][e]);
+      float vg[2], v8[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 2 * t4 + e;
+        const int sl = n / CW, c = nt * 8 + n % CW;
+        const int gl = k0 / GKS + sl;
+        const int kk0 = gl * GKS;
+        vg[e] = v8[e] = 0.f;
+        if (sl < NSLOT && kk0 < nks) {
+          const float4 p = pp[gl * 16];  // {S_g, Z_g - 1024 S_g, S_g8 / 16, Z_g8 - 64 S_g8}
+          const float* xc = xsm + c * XW + kk0;
+          float X;
+          if (kk0 + GKS <= nks) {
+            X = sum_n<GKS>(xc);
+          } else {
+            X = 0.f;
+            for (int q = 0; q < nks - kk0; ++q) X = __fadd_rn(X, xc[q]);
+          }
+          vg[e] = __fmaf_rn(p.x, D[e], __fmul_rn(p.y, X));
+          v8[e] = __fmaf_rn(p.z, D[e + 2], __fmul_rn(p.w, X));
+        }
+      }
+      if constexpr (CW == 1) {
+        float r0 = __fadd_rn(vg[0], vg[1]), r2 = __fadd_rn(v8[0], v8[1]);
+        r0 = __fadd_rn(r0, __shfl_xor_sync(0xffffffffu, r0, 1));
+        r2 = __fadd_rn(r2, __shfl_xor_sync(0xffffffffu, r2, 1));
+        r0 = __fadd_rn(r0, __shfl_xor_sync(0xffffffffu, r0, 2));
+        r2 = __fadd_rn(r2, __shfl_xor_sync(0xffffffffu, r2, 2));
+        acc[nt][0] = __fadd_rn(acc[nt][0], r0);
+        acc[nt][2] = __fadd_rn(acc[nt][2], r2);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if constexpr (CW == 2) {
+            vg[e] = __fadd_rn(vg[e], __shfl_xor_sync(0xffffffffu, vg[e], 1));
+            v8[e] = __fadd_rn(v8[e], __shfl_xor_sync(0xffffffffu, v8[e], 1));
+          }
+          if constexpr (CW <= 4) {
+            vg[e] = __fadd_rn(vg[e], __shfl_xor_sync(0xffffffffu, vg[e], 2));
+            v8[e] = __fadd_rn(v8[e], __shfl_xor_sync(0xffffffffu, v8[e], 2));
+          }
+          acc[nt][e] = __fadd_rn(acc[nt][e], vg[e]);
+          acc[nt][e + 2] = __fadd_rn(acc[nt][e + 2], v8[e]);
+        }
+      }
+    }
   }
+}
+
+template <int NTC, int EPI, int GKS, int CW>
+__global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel(const __grid_constant__ LinearParams P) {
+  using C = I4Cfg<NTC, GKS, CW>;
+  constexpr int COLS = 8 * NTC;
+  constexpr int KCH = C::KCH;
+  extern __shared__ __align__(128) uint8_t sm[];
+  float* ysm = reinterpret_cast<float*>(sm + C::NSTAGE * C::STAGE);  // [32][COLS] results
+  float* hsm = ysm + 32 * COLS;                                       // [32][COLS] k-half 1 partials
+  uint64_t* full_b = reinterpret_cast<uint64_t*>(hsm + 32 * COLS);
+  uint64_t* empty_b = full_b + C::NSTAGE;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int KS = P.K / 16;
+  const int ks_pad = (KS + 3) / 4 * 4;
+  const int gpr = (P.K + P.wgroup - 1) / P.wgroup;
+  const int tp = blockIdx.x;                     // tile pair
+  const int nst = (KS + KCH - 1) / KCH;          // stages of the full K range
+  const int ncols = P.ncols;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::NSTAGE; ++s) {
+      mbar_init(&full_b[s], 1);
+      mbar_init(&empty_b[s], C::NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == C::NCW) {
+    // ======================= producer warp (lane 0 issues) =======================
+    auto issue_static = [&](int u) {
+      const int s = u % C::NSTAGE;
+      const int ks0 = u * KCH, nks = min(KCH, KS - ks0);
+      uint8_t* sp = sm + s * C::STAGE;
+      const uint32_t wb = (uint32_t)((nks + 3) / 4) * 1024;
+      const uint32_t pb = (uint32_t)((nks * 16 + P.wgroup - 1) / P.wgroup) * 256;
+      const uint32_t bb = (uint32_t)nks * 32, xb = (uint32_t)((nks + 3) / 4) * 16;
+      mbar_arrive_expect_tx(&full_b[s], wb + pb + ncols * (bb + xb));
+      bulk_g2s(sp, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)tp * (ks_pad / 4) + ks0 / 4) * 1024, wb, &full_b[s]);
+      bulk_g2s(sp + C::OFF_P, reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)tp * gpr + ks0 * 16 / P.wgroup) * 256,
+               pb, &full_b[s]);
+    };
+    auto issue_act = [&](int u) {
+      const int s = u % C::NSTAGE;
+      const int ks0 = u * KCH, nks = min(KCH, KS - ks0);
+      uint8_t* sp = sm + s * C::STAGE;
+      const uint32_t bb = (uint32_t)nks * 32, xb = (uint32_t)((nks + 3) / 4) * 16;
+      for (int c = 0; c < ncols; ++c) {
+        bulk_g2s(sp + C::OFF_B + c * C::BROW, reinterpret_cast<const __half*>(P.xh) + (size_t)c * P.ldxh + ks0 * 16, bb,
+                 &full_b[s]);
+        bulk_g2s(sp + C::OFF_X + c * C::XROW, P.xs + (size_t)c * P.ldxs + ks0, xb, &full_b[s]);
+      }
+    };
+    const int npre = min(nst, C::NSTAGE);
+    if (lane == 0)
+      for (int u = 0; u < npre; ++u) issue_static(u);  // weights stream in before the dependency resolves
+    pdl_wait();
+    pdl_trigger();
+    if (lane == 0) {
+      for (int u = 0; u < nst; ++u) {
+        if (u >= npre) {
+          mbar_wait(&empty_b[u % C::NSTAGE], ((u / C::NSTAGE) - 1) & 1);
+          issue_static(u);
+        }
+        issue_act(u);
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  pdl_wait();
+  pdl_trigger();
+
+  // ======================= consumer warps =======================
+  const int tile = warp & 1, kh = warp >> 1;
+  float acc[NTC][4];
+#pragma unroll
+  for (int nt = 0; nt < NTC; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+  for (int u = 0, s = 0, ph = 0; u < nst; ++u) {
+    mbar_wait(&full_b[s], ph);
+    const int nks = min(KCH, KS - u * KCH) - kh * C::HKS;  // this warp's k-steps of the stage
+    if (nks > 0 && !(P.dbg & 1)) {
+      const uint8_t* sp = sm + s * C::STAGE;
+      const int ko = kh * C::HKS;
+      const uint4* wa = reinterpret_cast<const uint4*>(sp) + (ko / 4) * 64 + tile * 32 + lane;
+      const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + (ko * 16 / P.wgroup) * 16 + tile * 8 + g;
+      const float* xsm = reinterpret_cast<const float*>(sp + C::OFF_X) + ko;
+      const uint8_t* bb = sp + C::OFF_B + ko * 32;
+      if (nks >= C::HKS)
+        i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, C::HKS, g, t4, acc);
+      else
+        i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, nks, g, t4, acc);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_b[s]);
+    if (++s == C::NSTAGE) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+  // ---- sum the two k-halves of each tile (k-half 0 + k-half 1), then the epilogue ----
+  const int rr = tile * 16 + g;
+  if (kh == 1) {
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) hsm[(rr + (e >> 1) * 8) * COLS + nt * 8 + 2 * t4 + (e & 1)] = acc[nt][e];
+  }
+  asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
+  if (kh == 0) {
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int idx = (rr + (e >> 1) * 8) * COLS + nt * 8 + 2 * t4 + (e & 1);
+        ysm[idx] = __fadd_rn(acc[nt][e], hsm[idx]);
+      }
+  }
+  asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
+  linear_epilogue<EPI, COLS, C::NCW * 32>(P, ysm, tp * 32, 32, tid, ncols);
+}
+
+template <int NTC, int EPI, int GKS, int CW>
+static cudaError_t launch_i4_t(const LinearParams& p, cudaStream_t s) {
+  using C = I4Cfg<NTC, GKS, CW>;
+  auto kern = linear_i4_kernel<NTC, EPI, GKS, CW>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int pairs = (p.N / 16 + 1) / 2;
+  return launch_pdl(kern, dim3(pairs), dim3(C::THREADS), C::SMEM, s, p);
+}
+
+template <int NTC, int GKS, int CW>
+static cudaError_t launch_i4_e(const LinearParams& p, cudaStream_t s) {
+  switch (p.epi) {
+    case QS_EPI_STORE: return launch_i4_t<NTC, QS_EPI_STORE, GKS, CW>(p, s);
+    case QS_EPI_ADD: return launch_i4_t<NTC, QS_EPI_ADD, GKS, CW>(p, s);
+    case QS_EPI_QKV: return launch_i4_t<NTC, QS_EPI_QKV, GKS, CW>(p, s);
+    case QS_EPI_SILU_MUL: return launch_i4_t<NTC, QS_EPI_SILU_MUL, GKS, CW>(p, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int GKS>
+static cudaError_t launch_i4_n(const LinearParams& p, cudaStream_t s) {
+  if (p.ncols == 1) return launch_i4_e<1, GKS, 1>(p, s);
+  if (p.ncols == 2) return launch_i4_e<1, GKS, 2>(p, s);
+  if (p.ncols <= 4) return launch_i4_e<1, GKS, 4>(p, s);
+  if (p.ncols <= 8) return launch_i4_e<1, GKS, 8>(p, s);
+  if (p.ncols <= 16) return launch_i4_e<2, GKS, 8>(p, s);
+  return cudaErrorInvalidValue;
 }
 
 // ---------------------------------------------------------------------------
@@ -591,6 +897,7 @@ int linear_grid_ctas(int wmode, int N, int K, int nctas) {
 }
 
 int linear_maxc(int wmode, int N, int K, int nctas) {
+  if (wmode == QS_W_INT4) return 1;  // linear_i4_kernel: no cross-CTA partials
   const int KCH = wmode == QS_W_F16 ? LinCfg<QS_W_F16, 1, 1>::KCH : LinCfg<QS_W_INT4, 1, 1>::KCH;
   const long long KS = K / 16, MG = (N + 63) / 64, KC = (KS + KCH - 1) / KCH, U = MG * KC;
   const long long C = linear_grid_ctas(wmode, N, K, nctas);
@@ -626,14 +933,9 @@ static cudaError_t launch_lin_e(const LinearParams& p, cudaStream_t s) {
   }
 }
 
-// column-count dispatch; INT4 packs 8/CW weight groups into the MMA's N columns (int4_unit)
+// column-count dispatch (f16 stream-K; INT4 runs linear_i4_kernel)
 template <int WMODE, int GKS>
 static cudaError_t launch_lin_n(const LinearParams& p, cudaStream_t s) {
-  if (WMODE == QS_W_INT4) {
-    if (p.ncols == 1) return launch_lin_e<WMODE, 1, GKS, 1>(p, s);
-    if (p.ncols == 2) return launch_lin_e<WMODE, 1, GKS, 2>(p, s);
-    if (p.ncols <= 4) return launch_lin_e<WMODE, 1, GKS, 4>(p, s);
-  }
   if (p.ncols <= 8) return launch_lin_e<WMODE, 1, GKS, 8>(p, s);
   if (p.ncols <= 16) return launch_lin_e<WMODE, 2, GKS, 8>(p, s);
   return cudaErrorInvalidValue;
@@ -643,10 +945,10 @@ cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {
   if (p.wmode == QS_W_F16) return launch_lin_n<QS_W_F16, 1>(p, s);
   if (p.wmode == QS_W_INT4) {
     switch (p.wgroup) {
-      case 16: return launch_lin_n<QS_W_INT4, 1>(p, s);
-      case 32: return launch_lin_n<QS_W_INT4, 2>(p, s);
-      case 64: return launch_lin_n<QS_W_INT4, 4>(p, s);
-      case 128: return launch_lin_n<QS_W_INT4, 8>(p, s);
+      case 16: return launch_i4_n<1>(p, s);
+      case 32: return launch_i4_n<2>(p, s);
+      case 64: return launch_i4_n<4>(p, s);
+      case 128: return launch_i4_n<8>(p, s);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -663,23 +965,32 @@ static int occ_of() {
   return n;
 }
 
-template <int WMODE, int GKS>
-static int occ_n(int ncols) {
-  if (WMODE == QS_W_INT4) {
-    if (ncols == 1) return occ_of<WMODE, 1, GKS, 1>();
-    if (ncols == 2) return occ_of<WMODE, 1, GKS, 2>();
-    if (ncols <= 4) return occ_of<WMODE, 1, GKS, 4>();
-  }
-  return ncols <= 8 ? occ_of<WMODE, 1, GKS, 8>() : occ_of<WMODE, 2, GKS, 8>();
+template <int NTC, int GKS, int CW>
+static int occ_i4() {
+  using C = I4Cfg<NTC, GKS, CW>;
+  auto kern = linear_i4_kernel<NTC, QS_EPI_STORE, GKS, CW>;
+  int n = 0;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, C::THREADS, C::SMEM);
+  return n;
 }
 
+template <int GKS>
+static int occ_i4_n(int ncols) {
+  if (ncols == 1) return occ_i4<1, GKS, 1>();
+  if (ncols == 2) return occ_i4<1, GKS, 2>();
+  if (ncols <= 4) return occ_i4<1, GKS, 4>();
+  return ncols <= 8 ? occ_i4<1, GKS, 8>() : occ_i4<2, GKS, 8>();
+}
+
+// resident CTAs per SM (f16: the stream-K grid is SMs x this; INT4: informational, its grid is N/32)
 int linear_occupancy(int wmode, int wgroup, int ncols) {
-  if (wmode == QS_W_F16) return occ_n<QS_W_F16, 1>(ncols);
+  if (wmode == QS_W_F16) return ncols <= 8 ? occ_of<QS_W_F16, 1, 1, 8>() : occ_of<QS_W_F16, 2, 1, 8>();
   switch (wgroup) {
-    case 16: return occ_n<QS_W_INT4, 1>(ncols);
-    case 32: return occ_n<QS_W_INT4, 2>(ncols);
-    case 64: return occ_n<QS_W_INT4, 4>(ncols);
-    case 128: return occ_n<QS_W_INT4, 8>(ncols);
+    case 16: return occ_i4_n<1>(ncols);
+    case 32: return occ_i4_n<2>(ncols);
+    case 64: return occ_i4_n<4>(ncols);
+    case 128: return occ_i4_n<8>(ncols);
     default: return 0;
   }
 }

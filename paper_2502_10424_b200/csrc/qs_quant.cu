@@ -224,23 +224,23 @@ __global__ void wq_refcodes_kernel(const float* __restrict__ w, WGeom geo, const
   out[b] = (uint8_t)(c[0] | (c[1] << 4));
 }
 
-// frag4 words, m-group major: [mg][KSpad/4][4 tiles][32 lanes][4]  (tile mt = 4 mg + w; A = W^T tile,
-// rows = outputs, cols = d_in).  One (4-tile group, k-chunk) unit of the linear kernel is one
-// contiguous range; tiles past d_out/16 (padding to a multiple of 4) are zero.
+// frag4 words, tile-pair major: [pair][KSpad/4][2 tiles][32 lanes][4]  (tile mt = 2 pair + w; A = W^T
+// tile, rows = outputs, cols = d_in).  A 64-k-step stage of one pair (linear_i4_kernel) is one
+// contiguous range; a padding tile (odd d_out/16) is zero.
 __global__ void wq_frag_kernel(const float* __restrict__ w, WGeom geo, const float* __restrict__ s,
                                const float* __restrict__ z, uint32_t* __restrict__ frag, int ks_pad) {
   long long wi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int MT = geo.d_out / 16, MT4 = (MT + 3) / 4 * 4;
-  long long nwords = (long long)MT4 * ks_pad * 32;
+  const int MT = geo.d_out / 16, MT2 = (MT + 1) / 2 * 2;
+  long long nwords = (long long)MT2 * ks_pad * 32;
   if (wi >= nwords) return;
   int v4 = (int)(wi & 3);
   long long rest = wi >> 2;
   int lane = (int)(rest & 31);
   rest >>= 5;
-  int wt = (int)(rest & 3);
-  rest >>= 2;
+  int wt = (int)(rest & 1);
+  rest >>= 1;
   int kq = (int)(rest % (ks_pad / 4));
-  int mt = (int)(rest / (ks_pad / 4)) * 4 + wt;
+  int mt = (int)(rest / (ks_pad / 4)) * 2 + wt;
   int ks = kq * 4 + v4;
   int g = lane >> 2, t = lane & 3;
   uint32_t word = 0;
@@ -257,19 +257,19 @@ __global__ void wq_frag_kernel(const float* __restrict__ w, WGeom geo, const flo
   frag[wi] = word;
 }
 
-// params, m-group major: float4 per [mg][group][4 tiles][g] (zeros for padding tiles)
+// params, tile-pair major: float4 per [pair][group][2 tiles][g] (zeros for a padding tile)
 __global__ void wq_fragparams_kernel(WGeom geo, const float* __restrict__ s, const float* __restrict__ z,
                                      float4* __restrict__ out) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int MT = geo.d_out / 16, MT4 = (MT + 3) / 4 * 4;
-  long long total = (long long)MT4 * geo.gpr * 8;
+  const int MT = geo.d_out / 16, MT2 = (MT + 1) / 2 * 2;
+  long long total = (long long)MT2 * geo.gpr * 8;
   if (i >= total) return;
   int g = (int)(i & 7);
   long long rest = i >> 3;
-  int wt = (int)(rest & 3);
-  rest >>= 2;
+  int wt = (int)(rest & 1);
+  rest >>= 1;
   int grp = (int)(rest % geo.gpr);
-  int mt = (int)(rest / geo.gpr) * 4 + wt;
+  int mt = (int)(rest / geo.gpr) * 2 + wt;
   if (mt >= MT) {
     out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
@@ -538,11 +538,11 @@ cudaError_t launch_quantize_weights(const float* w, int d_in, int d_out, int gro
   if (ref) wq_refcodes_kernel<<<blocks_for(((long long)d_in * d_out + 1) / 2, 256), 256, 0, st>>>(w, geo, s, z, ref);
   if (frag4) {
     int ks = d_in / 16, ks_pad = (ks + 3) / 4 * 4;
-    long long nwords = (long long)((d_out / 16 + 3) / 4 * 4) * ks_pad * 32;
+    long long nwords = (long long)((d_out / 16 + 1) / 2 * 2) * ks_pad * 32;
     wq_frag_kernel<<<blocks_for(nwords, 256), 256, 0, st>>>(w, geo, s, z, frag4, ks_pad);
   }
   if (fparams) {
-    long long tot = (long long)((d_out / 16 + 3) / 4 * 4) * geo.gpr * 8;
+    long long tot = (long long)((d_out / 16 + 1) / 2 * 2) * geo.gpr * 8;
     wq_fragparams_kernel<<<blocks_for(tot, 256), 256, 0, st>>>(geo, s, z, fparams);
   }
   return cudaGetLastError();

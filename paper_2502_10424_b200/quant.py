@@ -323,9 +323,9 @@ def quantize_weights_device(w_dev, group_size: int, want_plane: bool = True, wan
     frag = fparams = None
     if want_frag:
         ks_pad = (d_in // 16 + 3) // 4 * 4
-        mt4 = (d_out // 16 + 3) // 4 * 4  # m-group-major layout pads to whole 4-tile groups
-        frag = torch.empty(mt4 * ks_pad * 32, dtype=torch.int32, device=dev)
-        fparams = torch.empty(mt4 * gpr * 8 * 4, dtype=torch.float32, device=dev)
+        mt2 = (d_out // 16 + 1) // 2 * 2  # tile-pair-major layout pads to whole pairs
+        frag = torch.empty(mt2 * ks_pad * 32, dtype=torch.int32, device=dev)
+        fparams = torch.empty(mt2 * gpr * 8 * 4, dtype=torch.float32, device=dev)
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.call("qs_quantize_weights", _lib.ptr(w_dev), d_in, d_out, group_size, _lib.ptr(ref), _lib.ptr(s),
               _lib.ptr(z), _lib.ptr(frag), _lib.ptr(fparams), _lib.ptr(flags), _lib.stream_ptr())

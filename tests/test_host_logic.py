@@ -96,16 +96,19 @@ def _stream_k_maxc(N, K, nctas, kch):
     return max(len(set(owner[m * KC:(m + 1) * KC].tolist())) for m in range(MG))
 
 
-@pytest.mark.parametrize("wmode,kch", [(0, 8), (1, 16)])
 @pytest.mark.parametrize("N,K,nctas", [(4096, 4096, 296), (22016, 4096, 444), (4096, 11008, 148), (192, 64, 1000),
                                        (64, 176, 7), (32000, 4096, 296)])
-def test_stream_k_plan_matches_partition(wmode, kch, N, K, nctas):
+def test_stream_k_plan_matches_partition(N, K, nctas):
+    """f16 stream-K workspace slots == the partition's widest tile; INT4 (one CTA per
+    tile pair, no cross-CTA partials) needs a single slot."""
     from paper_2502_10424_b200 import _build
 
     lib = ctypes.CDLL(_build.build())
     mx = ctypes.c_int(0)
-    assert lib.qs_linear_plan(wmode, N, K, nctas, ctypes.byref(mx)) == 0
-    assert mx.value == _stream_k_maxc(N, K, nctas, kch)
+    assert lib.qs_linear_plan(0, N, K, nctas, ctypes.byref(mx)) == 0
+    assert mx.value == _stream_k_maxc(N, K, nctas, 8)
+    assert lib.qs_linear_plan(1, N, K, nctas, ctypes.byref(mx)) == 0
+    assert mx.value == 1
 
 
 def test_interleave_cols_gate_up_tiles():
