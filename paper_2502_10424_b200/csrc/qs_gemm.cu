@@ -523,16 +523,18 @@ __global__ void __launch_bounds__(LinCfg<WMODE, NTC, GKS, CW>::THREADS) linear_k
 // limiter of these short INT4 launches.  Weights are stored pair-major
 // ([pair][k-quad][2 tiles][32 lanes][16 B], params [pair][group][2 tiles][8][float4]), so
 // a 64-k-step stage of a pair is one contiguous bulk copy of codes and one of params.
-// Warps 0-3: tile w&1, k-half w>>1 of every stage; the two k-halves of a tile are summed
-// through shared memory at the end (fixed order).  Grid = N/32 CTAs: small CTAs keep the
-// SMs balanced, and PDL overlaps each CTA's first weight stages with the previous kernel.
+// Persistent: one CTA per SM takes pairs b, b + grid, ...; its TMA ring (up to 8 stages of 64
+// k-steps) runs straight across pair boundaries.  Warps 0-7: tile w&1, k-quarter w>>1 of every
+// stage; the four k-quarters of a tile are summed through shared memory in fixed order at the
+// pair's end.  PDL overlaps the first weight stages with the previous kernel.
 // ---------------------------------------------------------------------------
 template <int NTC, int GKS, int CW>
 struct I4Cfg {
-  static constexpr int NCW = 4;
+  static constexpr int KP = 8;                                    // k-parts: warps per tile
+  static constexpr int NCW = 2 * KP;                              // tile w&1, k-part w>>1
   static constexpr int THREADS = (NCW + 1) * 32;
-  static constexpr int KCH = 64;                                  // k-steps per stage
-  static constexpr int HKS = KCH / 2;                             // k-steps per consumer warp per stage
+  static constexpr int KCH = 128;                                 // k-steps per stage
+  static constexpr int HKS = KCH / KP;                            // k-steps per consumer warp per stage
   static constexpr int WBYTES = (KCH / 4) * 2 * 512;              // codes of both tiles
   static constexpr int ROWS = NTC == 1 ? CW : 16;
   static constexpr int BROW = KCH * 32 + 16;
@@ -542,9 +544,10 @@ struct I4Cfg {
   static constexpr int OFF_P = OFF_B + ROWS * BROW;
   static constexpr int OFF_X = OFF_P + PBYTES;
   static constexpr int STAGE = (OFF_X + ROWS * XROW + 127) / 128 * 128;
-  static constexpr int NSTAGE = 3;
   static constexpr int YCOLS = 8 * NTC;
-  static constexpr int SMEM = NSTAGE * STAGE + 2 * 32 * YCOLS * 4 + 2 * NSTAGE * 8 + 16;
+  static constexpr int FIXED = KP * 32 * YCOLS * 4 + 2 * 8 * 8 + 16;
+  static constexpr int NSTAGE = (232448 - FIXED) / STAGE < 8 ? (232448 - FIXED) / STAGE : 8;  // one CTA per SM
+  static constexpr int SMEM = NSTAGE * STAGE + FIXED;
 };
 
 // HKS k-steps of one 16-row tile for one consumer warp (window / group-slot scheme of
@@ -657,17 +660,19 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
   constexpr int KCH = C::KCH;
   extern __shared__ __align__(128) uint8_t sm[];
   float* ysm = reinterpret_cast<float*>(sm + C::NSTAGE * C::STAGE);  // [32][COLS] results
-  float* hsm = ysm + 32 * COLS;                                       // [32][COLS] k-half 1 partials
-  uint64_t* full_b = reinterpret_cast<uint64_t*>(hsm + 32 * COLS);
-  uint64_t* empty_b = full_b + C::NSTAGE;
+  float* hsm = ysm + 32 * COLS;                                       // [KP-1][32][COLS] k-part partials
+  uint64_t* full_b = reinterpret_cast<uint64_t*>(hsm + (C::KP - 1) * 32 * COLS);
+  uint64_t* empty_b = full_b + 8;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int KS = P.K / 16;
   const int ks_pad = (KS + 3) / 4 * 4;
   const int gpr = (P.K + P.wgroup - 1) / P.wgroup;
-  const int tp = blockIdx.x;                     // tile pair
-  const int nst = (KS + KCH - 1) / KCH;          // stages of the full K range
+  const int TP = (P.N / 16 + 1) / 2;              // tile pairs
+  const int nst = (KS + KCH - 1) / KCH;          // stages per pair (full K range)
+  const int npairs = (TP - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // pairs b, b+grid, ...
+  const int total = npairs * nst;                // stages this CTA streams
   const int ncols = P.ncols;
 
   if (tid == 0) {
@@ -681,8 +686,11 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
 
   if (warp == C::NCW) {
     // ======================= producer warp (lane 0 issues) =======================
-    auto issue_static = [&](int u) {
-      const int s = u % C::NSTAGE;
+    // stage q of this CTA = stage q % nst of pair blockIdx.x + (q / nst) * gridDim.x; the ring
+    // runs straight across pair boundaries, so the next pair's weights are already in flight
+    auto issue_static = [&](int q) {
+      const int s = q % C::NSTAGE;
+      const int tp = blockIdx.x + (q / nst) * gridDim.x, u = q % nst;
       const int ks0 = u * KCH, nks = min(KCH, KS - ks0);
       uint8_t* sp = sm + s * C::STAGE;
       const uint32_t wb = (uint32_t)((nks + 3) / 4) * 1024;
@@ -693,8 +701,8 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
       bulk_g2s(sp + C::OFF_P, reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)tp * gpr + ks0 * 16 / P.wgroup) * 256,
                pb, &full_b[s]);
     };
-    auto issue_act = [&](int u) {
-      const int s = u % C::NSTAGE;
+    auto issue_act = [&](int q) {
+      const int s = q % C::NSTAGE, u = q % nst;
       const int ks0 = u * KCH, nks = min(KCH, KS - ks0);
       uint8_t* sp = sm + s * C::STAGE;
       const uint32_t bb = (uint32_t)nks * 32, xb = (uint32_t)((nks + 3) / 4) * 16;
@@ -704,18 +712,18 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
         bulk_g2s(sp + C::OFF_X + c * C::XROW, P.xs + (size_t)c * P.ldxs + ks0, xb, &full_b[s]);
       }
     };
-    const int npre = min(nst, C::NSTAGE);
+    const int npre = min(total, C::NSTAGE);
     if (lane == 0)
-      for (int u = 0; u < npre; ++u) issue_static(u);  // weights stream in before the dependency resolves
+      for (int q = 0; q < npre; ++q) issue_static(q);  // weights stream in before the dependency resolves
     pdl_wait();
     pdl_trigger();
     if (lane == 0) {
-      for (int u = 0; u < nst; ++u) {
-        if (u >= npre) {
-          mbar_wait(&empty_b[u % C::NSTAGE], ((u / C::NSTAGE) - 1) & 1);
-          issue_static(u);
+      for (int q = 0; q < total; ++q) {
+        if (q >= npre) {
+          mbar_wait(&empty_b[q % C::NSTAGE], ((q / C::NSTAGE) - 1) & 1);
+          issue_static(q);
         }
-        issue_act(u);
+        issue_act(q);
       }
     }
     __syncwarp();
@@ -725,54 +733,63 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
   pdl_trigger();
 
   // ======================= consumer warps =======================
-  const int tile = warp & 1, kh = warp >> 1;
-  float acc[NTC][4];
-#pragma unroll
-  for (int nt = 0; nt < NTC; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-  for (int u = 0, s = 0, ph = 0; u < nst; ++u) {
-    mbar_wait(&full_b[s], ph);
-    const int nks = min(KCH, KS - u * KCH) - kh * C::HKS;  // this warp's k-steps of the stage
-    if (nks > 0 && !(P.dbg & 1)) {
-      const uint8_t* sp = sm + s * C::STAGE;
-      const int ko = kh * C::HKS;
-      const uint4* wa = reinterpret_cast<const uint4*>(sp) + (ko / 4) * 64 + tile * 32 + lane;
-      const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + (ko * 16 / P.wgroup) * 16 + tile * 8 + g;
-      const float* xsm = reinterpret_cast<const float*>(sp + C::OFF_X) + ko;
-      const uint8_t* bb = sp + C::OFF_B + ko * 32;
-      if (nks >= C::HKS)
-        i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, C::HKS, g, t4, acc);
-      else
-        i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, nks, g, t4, acc);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_b[s]);
-    if (++s == C::NSTAGE) {
-      s = 0;
-      ph ^= 1;
-    }
-  }
-  // ---- sum the two k-halves of each tile (k-half 0 + k-half 1), then the epilogue ----
+  const int tile = warp & 1, kp = warp >> 1;
   const int rr = tile * 16 + g;
-  if (kh == 1) {
+  int s = 0, ph = 0;
+  for (int pi = 0; pi < npairs; ++pi) {
+    const int tp = blockIdx.x + pi * gridDim.x;
+    float acc[NTC][4];
 #pragma unroll
     for (int nt = 0; nt < NTC; ++nt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) hsm[(rr + (e >> 1) * 8) * COLS + nt * 8 + 2 * t4 + (e & 1)] = acc[nt][e];
-  }
-  asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
-  if (kh == 0) {
-#pragma unroll
-    for (int nt = 0; nt < NTC; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int idx = (rr + (e >> 1) * 8) * COLS + nt * 8 + 2 * t4 + (e & 1);
-        ysm[idx] = __fadd_rn(acc[nt][e], hsm[idx]);
+      for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+    for (int u = 0; u < nst; ++u) {
+      mbar_wait(&full_b[s], ph);
+      const int nks = min(KCH, KS - u * KCH) - kp * C::HKS;  // this warp's k-steps of the stage
+      if (nks > 0 && !(P.dbg & 1)) {
+        const uint8_t* sp = sm + s * C::STAGE;
+        const int ko = kp * C::HKS;
+        const uint4* wa = reinterpret_cast<const uint4*>(sp) + (ko / 4) * 64 + tile * 32 + lane;
+        const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + (ko * 16 / P.wgroup) * 16 + tile * 8 + g;
+        const float* xsm = reinterpret_cast<const float*>(sp + C::OFF_X) + ko;
+        const uint8_t* bb = sp + C::OFF_B + ko * 32;
+        if (nks >= C::HKS)
+          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, C::HKS, g, t4, acc);
+        else
+          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, nks, g, t4, acc);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_b[s]);
+      if (++s == C::NSTAGE) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    // ---- sum the k-parts of each tile in order (0 + 1 + ... ), then the epilogue ----
+    if (kp > 0) {
+#pragma unroll
+      for (int nt = 0; nt < NTC; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          hsm[((kp - 1) * 32 + rr + (e >> 1) * 8) * COLS + nt * 8 + 2 * t4 + (e & 1)] = acc[nt][e];
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
+    if (kp == 0) {
+#pragma unroll
+      for (int nt = 0; nt < NTC; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int idx = (rr + (e >> 1) * 8) * COLS + nt * 8 + 2 * t4 + (e & 1);
+          float a = acc[nt][e];
+#pragma unroll
+          for (int k = 0; k < C::KP - 1; ++k) a = __fadd_rn(a, hsm[k * 32 * COLS + idx]);
+          ysm[idx] = a;
+        }
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
+    linear_epilogue<EPI, COLS, C::NCW * 32>(P, ysm, tp * 32, 32, tid, ncols);
+    asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));  // ysm / hsm reuse by the next pair
   }
-  asm volatile("bar.sync 2, %0;" ::"n"(C::NCW * 32));
-  linear_epilogue<EPI, COLS, C::NCW * 32>(P, ysm, tp * 32, 32, tid, ncols);
 }
 
 template <int NTC, int EPI, int GKS, int CW>
@@ -786,7 +803,13 @@ static cudaError_t launch_i4_t(const LinearParams& p, cudaStream_t s) {
     configured = true;
   }
   const int pairs = (p.N / 16 + 1) / 2;
-  return launch_pdl(kern, dim3(pairs), dim3(C::THREADS), C::SMEM, s, p);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return launch_pdl(kern, dim3(pairs < sms ? pairs : sms), dim3(C::THREADS), C::SMEM, s, p);
 }
 
 template <int NTC, int GKS, int CW>
