@@ -5,6 +5,7 @@
 //   argmax selection /root/reference/pkg/src/quantspec/specdec.py:209-212
 //   greedy verify    /root/reference/pkg/src/quantspec/specdec.py:276-299
 #include <math.h>
+#include <stdint.h>
 #include <stdlib.h>
 
 #include "qs_common.cuh"
@@ -78,7 +79,33 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int* 
   const float* row = logits + (size_t)blockIdx.x * vocab;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+  // 16-byte loads, four in flight per thread per round (a long scan of dependent scalar loads
+  // was L2-latency bound); the (value, first index) order makes the result independent of it
+  const bool vec = (vocab & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0;
+  const int nv = vec ? vocab / 4 : 0;
+  const float4* row4 = reinterpret_cast<const float4*>(row);
+  for (int b = threadIdx.x; b < nv; b += 4 * blockDim.x) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = b + u * blockDim.x;
+      v[u] = j < nv ? row4[j] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = b + u * blockDim.x;
+      if (j < nv) {
+        const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (better(e[q], 4 * j + q, bv, bi)) {
+            bv = e[q];
+            bi = 4 * j + q;
+          }
+      }
+    }
+  }
+  for (int i = 4 * nv + threadIdx.x; i < vocab; i += blockDim.x) {
     float v = row[i];
     if (better(v, i, bv, bi)) {
       bv = v;

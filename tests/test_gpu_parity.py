@@ -562,6 +562,23 @@ def test_decode_step_logits_vs_oracle(toy, view):
                                             ocost.kv_param_bytes, ocost.kv_fp_bytes, ocost.kv_quantized_elements]
 
 
+@pytest.mark.parametrize("V", [32000, 32003, 128256])
+def test_argmax_first_max_wide_rows(V):
+    """qs_argmax == np.argmax (first maximum; first NaN) on vocabulary-sized rows: the
+    16-byte-load path (V % 4 == 0) and its scalar tail (V % 4 != 0), planted exact ties."""
+    rng = np.random.default_rng(V)
+    rows = rng.standard_normal((6, V)).astype(np.float32)
+    rows[1, [7, 9000, V - 1]] = rows[1].max() + 1.0            # tie across the row -> 7
+    rows[2, [V - 2, V - 1]] = rows[2].max() + 1.0              # tie in the tail
+    rows[3, 4 * (V // 8) + 3] = rows[3].max() + 2.0            # max on a float4 lane 3
+    rows[4, [11, 5000]] = np.nan                               # np.argmax returns the first NaN
+    rows[5, :] = 0.0                                           # all equal -> 0
+    lg = torch.from_numpy(rows).cuda()
+    am = torch.zeros(6, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.load().qs_argmax(lg.data_ptr(), 6, V, am.data_ptr(), 1, _lib.stream_ptr()))
+    assert am.cpu().tolist() == np.argmax(rows, axis=1).tolist()
+
+
 def test_greedy_accept_kernel_matches_oracle_rule():
     rng = np.random.default_rng(9)
     dev = torch.device("cuda")
