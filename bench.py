@@ -197,6 +197,8 @@ def time_kernel(fn, iters: int = 21):
         fn()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    # hold the GPU while the host enqueues every launch, so no event pair brackets host launch latency
+    torch.cuda._sleep(int(2e8))
     for s, e in ev:
         s.record()
         fn()

@@ -282,17 +282,18 @@ __global__ void wq_fragparams_kernel(WGeom geo, const float* __restrict__ s, con
   out[i] = make_float4(s0, __fmaf_rn(-1024.f, s0, z0), __fmul_rn(s1, 0.0625f), __fmaf_rn(-64.f, s1, z1));
 }
 
-// fp16 frag layout, m-group major: [mg][ks][4 tiles][32 lanes][8 halves] (tile mt = 4 mg + w; zero padding tiles)
+// fp16 frag layout, tile-pair major: [pair][ks][2 tiles][32 lanes][8 halves] (tile mt = 2 pair + w;
+// a padding tile (odd d_out/16) is zero).  A stage of k-steps of one pair is one contiguous range.
 __global__ void pack_f16_kernel(const float* __restrict__ w, int d_in, int d_out, __half* __restrict__ out) {
-  long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (mg, ks, w, lane)
-  const int KS = d_in / 16, MT = d_out / 16, MT4 = (MT + 3) / 4 * 4;
-  long long total = (long long)MT4 * KS * 32;
+  long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (pair, ks, w, lane)
+  const int KS = d_in / 16, MT = d_out / 16, MT2 = (MT + 1) / 2 * 2;
+  long long total = (long long)MT2 * KS * 32;
   if (li >= total) return;
   int lane = (int)(li & 31);
   long long rest = li >> 5;
-  int wt = (int)(rest & 3);
-  rest >>= 2;
-  int ks = (int)(rest % KS), mt = (int)(rest / KS) * 4 + wt;
+  int wt = (int)(rest & 1);
+  rest >>= 1;
+  int ks = (int)(rest % KS), mt = (int)(rest / KS) * 2 + wt;
   int g = lane >> 2, t = lane & 3;
   __align__(16) __half hv[8];
 #pragma unroll
@@ -549,7 +550,7 @@ cudaError_t launch_quantize_weights(const float* w, int d_in, int d_out, int gro
 }
 
 cudaError_t launch_pack_f16(const float* w, int d_in, int d_out, __half* out, cudaStream_t st) {
-  long long total = (long long)((d_out / 16 + 3) / 4 * 4) * (d_in / 16) * 32;
+  long long total = (long long)((d_out / 16 + 1) / 2 * 2) * (d_in / 16) * 32;
   pack_f16_kernel<<<blocks_for(total, 256), 256, 0, st>>>(w, d_in, d_out, out);
   return cudaGetLastError();
 }

@@ -80,8 +80,8 @@ def pack_f16(w):
     """[d_in, d_out] f32 CUDA tensor -> frag16 halves."""
     torch = _torch()
     d_in, d_out = (int(x) for x in w.shape)
-    mt4 = (d_out // 16 + 3) // 4 * 4
-    out = torch.empty(mt4 * (d_in // 16) * 32 * 8, dtype=torch.float16, device=w.device)
+    mt2 = (d_out // 16 + 1) // 2 * 2  # tile-pair-major frag16 layout pads to whole pairs
+    out = torch.empty(mt2 * (d_in // 16) * 32 * 8, dtype=torch.float16, device=w.device)
     _lib.call("qs_pack_weights_f16", w.data_ptr(), d_in, d_out, out.data_ptr(), _lib.stream_ptr())
     return out
 
