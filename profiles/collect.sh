@@ -9,7 +9,7 @@ TAG=${1:-r01}
 mkdir -p gpurun_out
 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
-    -k 'regex:attn_kernel|linear_kernel|prep_act|embed_kernel|argmax|accept|add_int|kv_quant|fp_rotate' \
+    -k 'regex:attn_kernel|linear_|prep_act|embed_kernel|argmax|accept|add_int|kv_quant|fp_rotate' \
     -s 400 -c 1400 --csv --log-file gpurun_out/${TAG}_launches.csv \
     python bench.py --steps 2 --warmup 3 --modes both > /tmp/${TAG}_ll.log 2>&1
 python profiles/launch_shares.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launch_shares.txt 2>&1

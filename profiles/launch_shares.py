@@ -14,7 +14,7 @@ import sys
 
 
 def family(name: str) -> str:
-    m = re.search(r"(attn_kernel|linear_kernel|prep_act_kernel|embed_kernel|argmax_kernel|accept_kernel|add_int_kernel|"
+    m = re.search(r"(attn_kernel|linear_i4_kernel|linear_f16p_kernel|prep_act_kernel|embed_kernel|argmax_kernel|accept_kernel|add_int_kernel|"
                   r"kv_quant_kernel|fp_rotate_kernel)(<[^>]*>)?", name)
     return (m.group(1) + (m.group(2) or "")) if m else name[:60]
 
