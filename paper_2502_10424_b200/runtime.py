@@ -17,6 +17,8 @@ is the readback of (accepted count, next token).
 
 from __future__ import annotations
 
+import dataclasses
+
 import math
 from dataclasses import dataclass
 
@@ -155,17 +157,26 @@ class DeviceWeights:
 
 
 def build_device_weights(geo: Geometry, layer_mats, embedding, final_norm, lm_head, attn_norms, mlp_norms, *,
-                         int4_group: int | None = None, rope=None, want_fp16: bool = True):
+                         int4_group: int | None = None, rope=None, want_fp16: bool = True,
+                         head_shard: tuple[int, int] | None = None):
     """layer_mats: iterable yielding per-layer dicts of CUDA f32 [d_in, d_out] tensors.
 
     Returns (fp16 DeviceWeights or None, INT4 DeviceWeights or None); tensors
     are consumed one layer at a time so only packed copies stay resident.
+    ``head_shard=(rank, world)`` keeps only this rank's query / key / value head
+    columns of the QKV projection (KV-head sharding); the output
+    projection, MLP and lm_head stay replicated.
     """
     torch = _torch()
     rope = rope if rope is not None else rope_table(geo.head_dim, geo.rope_base, geo.max_positions)
     f_layers, q_layers = [], []
     for mats in layer_mats:
-        qkv = torch.cat([mats["wq"], mats["wk"], mats["wv"]], dim=1)
+        wq, wk, wv = mats["wq"], mats["wk"], mats["wv"]
+        if head_shard is not None:
+            r, n = head_shard
+            qn, kn = geo.nq // n, geo.nk // n
+            wq, wk, wv = wq[:, r * qn:(r + 1) * qn], wk[:, r * kn:(r + 1) * kn], wv[:, r * kn:(r + 1) * kn]
+        qkv = torch.cat([wq, wk, wv], dim=1)
         if want_fp16:
             f_layers.append(dict(qkv=PackedLinear.f16(qkv), o=PackedLinear.f16(mats["wo"]),
                                  gu=PackedLinear.f16_pair(mats["w_gate"], mats["w_up"]),
@@ -236,17 +247,36 @@ def plan_attention_splits(n_heads_total: int, max_chunks: int, ctas_per_sm: int 
 class Runner:
     """Scratch buffers + kernel sequence for forwards against one cache."""
 
-    def __init__(self, geo: Geometry, cache, *, max_cols: int = 16, attn_splits: int | None = None):
+    def __init__(self, geo: Geometry, cache, *, max_cols: int = 16, attn_splits: int | None = None,
+                 shard: tuple | None = None):
+        """``shard=(rank, world, process_group)``: KV-head sharding for a single sequence
+        whose context does not fit one GPU.  This rank's cache and QKV
+        weights hold heads [rank*H/world, (rank+1)*H/world); attention runs on those
+        heads only and its outputs are all-gathered (NCCL over NVLink on a real box)
+        before the replicated output projection / MLP."""
         torch = _torch()
         self.geo = geo
         self.cache = cache
         self.B = cache.batch
         self.max_cols = max_cols
+        self.shard = shard
+        if shard is not None:
+            _, world, _ = shard
+            if geo.num_kv_heads % world:
+                raise ConfigError(f"{geo.num_kv_heads} KV heads do not shard over {world} ranks")
+            lgeo = dataclasses.replace(geo, num_heads=geo.num_heads // world, num_kv_heads=geo.num_kv_heads // world)
+        else:
+            lgeo = geo
+        self.lgeo = lgeo  # this rank's attention heads
         dev = torch.device("cuda")
         d, nq = geo.hidden, geo.nq
         self.x = torch.zeros((max_cols, d), dtype=torch.float32, device=dev)
-        self.q = torch.zeros((max_cols, nq), dtype=torch.float32, device=dev)
+        self.q = torch.zeros((max_cols, lgeo.nq), dtype=torch.float32, device=dev)
         self.attn = torch.zeros_like(self.q)
+        if shard is not None:
+            self.attn_full = torch.zeros((max_cols, nq), dtype=torch.float32, device=dev)
+            self.gather_bufs = [torch.zeros((max_cols, lgeo.nq), dtype=torch.float32, device=dev)
+                                for _ in range(shard[1])]
         # f16 linear-layer inputs (+ 16-element sums for the INT4 zero-point term), padded rows
         kmax = max(d, nq)
         self.xh = torch.zeros((max_cols, (kmax + 64 + 7) // 8 * 8), dtype=torch.float16, device=dev)
@@ -260,7 +290,7 @@ class Runner:
         self.res = torch.zeros(4, dtype=torch.int32, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
         self.is_fp = not hasattr(cache, "d_n_blocks")
-        r = geo.num_heads // geo.num_kv_heads
+        r = lgeo.num_heads // lgeo.num_kv_heads
         self.r = r
         # attention: split-K grid per view, fixed for every T so row results are
         # batch-invariant (a T-row verify == T single-row steps, bit for bit)
@@ -277,9 +307,9 @@ class Runner:
         # queries per CTA: 8 per tile in the quantised views, 4 in the fp16 view (qs_attn_partials_floats)
         nq_cta = max(8 * max(1, -(-per // 8)), 4 * max(1, -(-per // 4)))
         max_splits = attn_splits or max(1, min(self.max_chunks, 4 * SM_COUNT))
-        nparts = self.B * geo.num_kv_heads * self.n_qgroups_max * (max_splits + 2) * nq_cta * (geo.head_dim + 2)
+        nparts = self.B * lgeo.num_kv_heads * self.n_qgroups_max * (max_splits + 2) * nq_cta * (geo.head_dim + 2)
         self.partials = torch.zeros(nparts, dtype=torch.float32, device=dev)
-        self.attn_counters = torch.zeros(self.B * geo.num_kv_heads * self.n_qgroups_max, dtype=torch.int32, device=dev)
+        self.attn_counters = torch.zeros(self.B * lgeo.num_kv_heads * self.n_qgroups_max, dtype=torch.int32, device=dev)
         self.fp_cps = 0
         if self.is_fp:
             self.fp_cps = -(-self.max_chunks // self.splits_for(_lib.VIEW_FP16))
@@ -300,7 +330,7 @@ class Runner:
                 cols = self.r if view == _lib.VIEW_DRAFT else min(12, self.max_T * self.r)
                 occ = _lib.load().qs_attn_occupancy(self.geo.head_dim, cols, view)
                 occ = occ if occ > 0 else 1
-                n = plan_attention_splits(self.B * self.geo.num_kv_heads * self.n_qgroups_max, self.max_chunks, occ)
+                n = plan_attention_splits(self.B * self.lgeo.num_kv_heads * self.n_qgroups_max, self.max_chunks, occ)
             self._splits[view] = n
         return n
 
@@ -337,7 +367,7 @@ class Runner:
             a.counters = self.lin_counters.data_ptr()
             if epi == _lib.EPI_QKV:
                 c = self.cache
-                a.Nq, a.Nk, a.hd, a.T = geo.nq, geo.nk, geo.head_dim, T
+                a.Nq, a.Nk, a.hd, a.T = self.lgeo.nq, self.lgeo.nk, geo.head_dim, T
                 a.q_out = self.q.data_ptr()
                 a.row_offset = row_offset
                 a.rope = self._rope.data_ptr()
@@ -380,17 +410,19 @@ class Runner:
         if a is None:
             geo, c = self.geo, self.cache
             a = _lib.AttnArgs()
-            a.B, a.Hkv, a.hd, a.T, a.r = self.B, geo.num_kv_heads, geo.head_dim, T, self.r
+            a.B, a.Hkv, a.hd, a.T, a.r = self.B, self.lgeo.num_kv_heads, geo.head_dim, T, self.r
             a.n_queries = T * self.r
             a.n_qgroups = max(1, -(-a.n_queries // 12))
             a.n_main = self.splits_for(view if not self.is_fp else _lib.VIEW_FP16)
             a.row_offset = row_offset
             a.sm_scale_log2 = float(1.4426950408889634 / math.sqrt(geo.head_dim))
-            a.q, a.out, a.q_row_stride = self.q.data_ptr(), self.attn.data_ptr(), geo.nq
+            a.q, a.out, a.q_row_stride = self.q.data_ptr(), self.attn.data_ptr(), self.lgeo.nq
             a.partials, a.counters = self.partials.data_ptr(), self.attn_counters.data_ptr()
-            # fused hand-off: the merge writes the O projection's f16 input + 16-sums (no prep launch)
-            a.out_h, a.ld_out_h = self.xh.data_ptr(), self.xh.shape[1]
-            a.out_s, a.ld_out_s = self.xs.data_ptr(), self.xs.shape[1]
+            # fused hand-off: the merge writes the O projection's f16 input + 16-sums (no prep launch);
+            # a head shard gathers first, so its merge writes only the f32 rows
+            if self.shard is None:
+                a.out_h, a.ld_out_h = self.xh.data_ptr(), self.xh.shape[1]
+                a.out_s, a.ld_out_s = self.xs.data_ptr(), self.xs.shape[1]
             if self.is_fp:
                 a.G = 64
                 a.fp_len = c.d_len.data_ptr()
@@ -449,6 +481,9 @@ class Runner:
             self._prep(self.x, w.attn_norms[li], X, ncols, s)
             self._linear(lw["qkv"], X, None, ncols, _lib.EPI_QKV, layer=li, T=T, row_offset=row_offset, stream=s)
             self._attention(li, view, T, row_offset, s)  # also writes X = (f16, 16-sums) of its output
+            if self.shard is not None:
+                self._gather_heads(ncols)
+                self._prep(self.attn_full, None, X, ncols, s)
             self._linear(lw["o"], X, self.x, ncols, _lib.EPI_ADD, stream=s)
             self._prep(self.x, w.mlp_norms[li], X, ncols, s)
             self._linear(lw["gu"], X, None, ncols, _lib.EPI_SILU_MUL, yh=H, stream=s)
@@ -457,6 +492,19 @@ class Runner:
         self._linear(w.lm_head, X, self.logits, ncols, _lib.EPI_STORE, stream=s)
         if argmax_to is not None:
             _lib.check(lib.qs_argmax(self.logits.data_ptr(), ncols, geo.vocab, argmax_to, 1, s), "qs_argmax")
+
+    def _gather_heads(self, ncols: int) -> None:
+        """All-gather every rank's attention rows [ncols, H_local*hd] into [ncols, H*hd]
+        (rank r's heads are the r-th block of the head order)."""
+        import torch.distributed as dist
+
+        _, world, group = self.shard
+        nql = self.lgeo.nq
+        bufs = [b[:ncols] for b in self.gather_bufs]
+        dist.all_gather(bufs, self.attn[:ncols].contiguous(), group=group)
+        full = self.attn_full[:ncols].view(ncols, world, nql)
+        for r in range(world):
+            full[:, r].copy_(bufs[r])
 
     def kernel_launches_per_forward(self, nlayers: int) -> int:
         return 1 + nlayers * 7 + 3
