@@ -256,13 +256,10 @@ __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uin
         }
       }
       if constexpr (CW == 1) {
-        float r0 = __fadd_rn(vg[0], vg[1]), r2 = __fadd_rn(v8[0], v8[1]);
-        r0 = __fadd_rn(r0, __shfl_xor_sync(0xffffffffu, r0, 1));
-        r2 = __fadd_rn(r2, __shfl_xor_sync(0xffffffffu, r2, 1));
-        r0 = __fadd_rn(r0, __shfl_xor_sync(0xffffffffu, r0, 2));
-        r2 = __fadd_rn(r2, __shfl_xor_sync(0xffffffffu, r2, 2));
-        acc[nt][0] = __fadd_rn(acc[nt][0], r0);
-        acc[nt][2] = __fadd_rn(acc[nt][2], r2);
+        // lane-local partials of this lane's group slots; the quad sum happens once per tile
+        // pair (i4_quad_sum) instead of once per window
+        acc[nt][0] = __fadd_rn(acc[nt][0], __fadd_rn(vg[0], vg[1]));
+        acc[nt][2] = __fadd_rn(acc[nt][2], __fadd_rn(v8[0], v8[1]));
       } else {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -279,6 +276,20 @@ __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uin
         }
       }
     }
+  }
+}
+
+// CW == 1: sum the four lanes' slot partials of rows g, g+8 (every lane of the quad ends with the total)
+template <int NTC, int CW>
+__device__ __forceinline__ void i4_quad_sum(float (&acc)[NTC][4]) {
+  if constexpr (CW == 1) {
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; e += 2) {
+        acc[nt][e] = __fadd_rn(acc[nt][e], __shfl_xor_sync(0xffffffffu, acc[nt][e], 1));
+        acc[nt][e] = __fadd_rn(acc[nt][e], __shfl_xor_sync(0xffffffffu, acc[nt][e], 2));
+      }
   }
 }
 
@@ -395,6 +406,7 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
       }
     }
     // ---- sum the k-parts of each tile in order (0 + 1 + ... ), then the epilogue ----
+    i4_quad_sum<NTC, CW>(acc);
     if (kp > 0) {
 #pragma unroll
       for (int nt = 0; nt < NTC; ++nt)
