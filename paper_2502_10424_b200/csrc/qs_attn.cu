@@ -510,9 +510,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   uint64_t* empty_b = bars + 16;
   const int G = P.G;
   const int lgG = 31 - __clz(G);
-  const int bpc = QS_CHUNK_Q >> lgG;
   const int n_blocks = P.n_blocks[seq];
-  const size_t plane_blk = (size_t)G * HD / 2;
   const int nchunk = c_end - c_begin;
   auto stage_ptr = [&](int s) { return region + s * C::QSTAGE; };
 
@@ -953,7 +951,6 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
   int* ticket_s = reinterpret_cast<int*>(bars + 24);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
   const int seq = blockIdx.z;
   const int head = blockIdx.x / P.n_qgroups, qg = blockIdx.x % P.n_qgroups;
   const int split = blockIdx.y;
