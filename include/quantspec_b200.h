@@ -122,6 +122,13 @@ typedef struct {
   const void* rope;   /* float2 [max_pos][hd/2] (cos, sin)           */
   int max_pos;
   int dbg;            /* 0; diagnostic bits (1: consumers skip the MMA work, 2: no tile reduction) */
+  /* INT4 only, optional: build the f16 activations + 16-sums inside the kernel from f32 rows
+   * xf [ncols][ldxf] (RMS-normalised with `gain` when non-NULL, Q/tensor.py:35-42) instead of
+   * reading xh / xs -- replaces a qs_prep_act launch; one row (ncols = 1), K <= 4096 */
+  const float* xf;
+  int64_t ldxf;
+  const float* gain;
+  float eps;
 } qs_linear_args;
 
 /* KV store descriptor (device pointers + geometry), Q/cache.py:42-133 */

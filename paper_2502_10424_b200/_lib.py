@@ -53,6 +53,7 @@ class LinearArgs(C.Structure):
         ("Nq", i32), ("Nk", i32), ("hd", i32), ("T", i32),
         ("q_out", vp), ("k_dst", vp), ("v_dst", vp), ("kv_seq_stride", i64), ("kv_head_stride", i64),
         ("row_base", vp), ("row_offset", i32), ("pos_base", vp), ("rope", vp), ("max_pos", i32), ("dbg", i32),
+        ("xf", vp), ("ldxf", i64), ("gain", vp), ("eps", C.c_float),
     ]
 
 

@@ -174,7 +174,13 @@ struct I4Cfg {
   static constexpr int OFF_X = OFF_P + PBYTES;
   static constexpr int STAGE = (OFF_X + ROWS * XROW + 127) / 128 * 128;
   static constexpr int YCOLS = 8 * NTC;
-  static constexpr int FIXED = KP * 32 * YCOLS * 4 + 2 * 8 * 8 + 16;
+  // in-kernel activation prep (P.xf): the f16 row + 16-sums of up to ACT_K inputs
+  // (one activation row -- the draft's T = 1 -- of up to 4096 inputs: the normed projections)
+  static constexpr int ACT_K = 4096;
+  static constexpr int ACT_ROW = ACT_K * 2 + 16;
+  static constexpr int ACT_SROW = ACT_K / 16 + 4;
+  static constexpr int ACT_BYTES = (NTC == 1 && CW == 1) ? ACT_ROW + ACT_SROW * 4 + 64 : 0;
+  static constexpr int FIXED = KP * 32 * YCOLS * 4 + 2 * 8 * 8 + 16 + ACT_BYTES;
   static constexpr int NSTAGE = (232448 - FIXED) / STAGE < 8 ? (232448 - FIXED) / STAGE : 8;  // one CTA per SM
   static constexpr int SMEM = NSTAGE * STAGE + FIXED;
 };
@@ -185,11 +191,10 @@ struct I4Cfg {
 template <class C, int NTC, int GKS, int CW>
 __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uint8_t* bbase, const float4* pp,
                                          const float* xsm, const int nks, const int g, const int t4,
-                                         float (&acc)[NTC][4]) {
+                                         float (&acc)[NTC][4], const int brs, const int XW) {
   constexpr int G8 = 8 / CW;
   constexpr int WIN = (G8 * GKS < C::HKS) ? G8 * GKS : C::HKS;  // k-steps per window
   constexpr int NSLOT = WIN / GKS;
-  constexpr int XW = C::XROW / 4;
   const int my_slot = g / CW;
 #pragma unroll
   for (int w = 0; w < C::HKS / WIN; ++w) {
@@ -207,7 +212,7 @@ __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uin
       const bool mine = my_slot == sl;
       const uint8_t* brow[NTC];
 #pragma unroll
-      for (int nt = 0; nt < NTC; ++nt) brow[nt] = bbase + (nt * 8 + g % CW) * C::BROW + 4 * t4;
+      for (int nt = 0; nt < NTC; ++nt) brow[nt] = bbase + (nt * 8 + g % CW) * brs + 4 * t4;
 #pragma unroll
       for (int j = 0; j < GKS; ++j) {
         const int ks = k0 + sl * GKS + j;
@@ -303,6 +308,8 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
   float* hsm = ysm + 32 * COLS;                                       // [KP-1][32][COLS] k-part partials
   uint64_t* full_b = reinterpret_cast<uint64_t*>(hsm + (C::KP - 1) * 32 * COLS);
   uint64_t* empty_b = full_b + 8;
+  uint8_t* act_h = reinterpret_cast<uint8_t*>(empty_b + 8) + 16;                // [ACT_ROW] f16 row
+  float* act_s = reinterpret_cast<float*>(act_h + C::ACT_ROW);                   // [ACT_SROW] 16-sums
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
@@ -310,6 +317,7 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
   const int ks_pad = (KS + 3) / 4 * 4;
   const int gpr = (P.K + P.wgroup - 1) / P.wgroup;
   const int TP = (P.N / 16 + 1) / 2;              // tile pairs
+  const bool act_in = C::ACT_BYTES > 0 && P.xf != nullptr;  // activations built here, not streamed
   const int nst = (KS + KCH - 1) / KCH;          // stages per pair (full K range)
   const int npairs = (TP - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // pairs b, b+grid, ...
   const int total = npairs * nst;                // stages this CTA streams
@@ -336,7 +344,7 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
       const uint32_t wb = (uint32_t)((nks + 3) / 4) * 1024;
       const uint32_t pb = (uint32_t)((nks * 16 + P.wgroup - 1) / P.wgroup) * 256;
       const uint32_t bb = (uint32_t)nks * 32, xb = (uint32_t)((nks + 3) / 4) * 16;
-      mbar_arrive_expect_tx(&full_b[s], wb + pb + ncols * (bb + xb));
+      mbar_arrive_expect_tx(&full_b[s], wb + pb + (act_in ? 0u : ncols * (bb + xb)));
       bulk_g2s(sp, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)tp * (ks_pad / 4) + ks0 / 4) * 1024, wb, &full_b[s]);
       bulk_g2s(sp + C::OFF_P, reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)tp * gpr + ks0 * 16 / P.wgroup) * 256,
                pb, &full_b[s]);
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
           mbar_wait(&empty_b[q % C::NSTAGE], ((q / C::NSTAGE) - 1) & 1);
           issue_static(q);
         }
-        issue_act(q);
+        if (!act_in) issue_act(q);
       }
     }
     __syncwarp();
@@ -371,6 +379,56 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
   }
   pdl_wait();
   pdl_trigger();
+  if (act_in) {
+    // f16 activations (+ RMS norm) and their 16-sums for the whole K range, once per CTA,
+    // while the first weight stages are still in flight (numerics of qs_prep_act)
+    float* red = ysm;  // scratch [NCW] (ysm is not used before the first epilogue)
+    constexpr int NT_ = C::NCW * 32;
+    for (int c = 0; c < ncols; ++c) {
+      const float* xr = P.xf + (size_t)c * P.ldxf;
+      float scale = 1.f;
+      if (P.gain) {
+        float a = 0.f;
+        for (int i = tid; i < P.K / 4; i += NT_) {
+          const float4 v = reinterpret_cast<const float4*>(xr)[i];
+          a += __fmul_rn(v.x, v.x);
+          a += __fmul_rn(v.y, v.y);
+          a += __fmul_rn(v.z, v.z);
+          a += __fmul_rn(v.w, v.w);
+        }
+        a = warp_sum(a);
+        if (lane == 0) red[warp] = a;
+        asm volatile("bar.sync 2, %0;" ::"n"(NT_));
+        float tot = 0.f;
+#pragma unroll
+        for (int w = 0; w < C::NCW; ++w) tot += red[w];
+        scale = __fsqrt_rn(__fadd_rn(__fdiv_rn(tot, (float)P.K), P.eps));
+        asm volatile("bar.sync 2, %0;" ::"n"(NT_));  // red reuse by the next column
+      }
+      __half* hr = reinterpret_cast<__half*>(act_h + c * C::ACT_ROW);
+      for (int gi = tid; gi < P.K / 16; gi += NT_) {
+        float s16 = 0.f;
+        __align__(16) __half hv[16];
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 v = reinterpret_cast<const float4*>(xr + gi * 16)[j4];
+          float4 gv = make_float4(1.f, 1.f, 1.f, 1.f);
+          if (P.gain) gv = reinterpret_cast<const float4*>(P.gain + gi * 16)[j4];
+          const float e[4] = {v.x, v.y, v.z, v.w}, gg[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float y = P.gain ? __fmul_rn(__fdiv_rn(e[q], scale), gg[q]) : e[q];
+            hv[j4 * 4 + q] = __float2half_rn(y);
+            s16 += __half2float(hv[j4 * 4 + q]);
+          }
+        }
+        *reinterpret_cast<uint4*>(hr + gi * 16) = *reinterpret_cast<uint4*>(hv);
+        *reinterpret_cast<uint4*>(hr + gi * 16 + 8) = *reinterpret_cast<uint4*>(hv + 8);
+        act_s[c * C::ACT_SROW + gi] = s16;
+      }
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(NT_));
+  }
 
   // ======================= consumer warps =======================
   const int tile = warp & 1, kp = warp >> 1;
@@ -391,12 +449,14 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
         const int ko = kp * C::HKS;
         const uint4* wa = reinterpret_cast<const uint4*>(sp) + (ko / 4) * 64 + tile * 32 + lane;
         const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + (ko * 16 / P.wgroup) * 16 + tile * 8 + g;
-        const float* xsm = reinterpret_cast<const float*>(sp + C::OFF_X) + ko;
-        const uint8_t* bb = sp + C::OFF_B + ko * 32;
+        const int kabs = u * KCH + ko;  // absolute k-step (activations built in-kernel)
+        const float* xsm = act_in ? act_s + kabs : reinterpret_cast<const float*>(sp + C::OFF_X) + ko;
+        const uint8_t* bb = act_in ? act_h + kabs * 32 : sp + C::OFF_B + ko * 32;
+        const int brs = act_in ? C::ACT_ROW : C::BROW, xw = act_in ? C::ACT_SROW : C::XROW / 4;
         if (nks >= C::HKS)
-          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, C::HKS, g, t4, acc);
+          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, C::HKS, g, t4, acc, brs, xw);
         else
-          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, nks, g, t4, acc);
+          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, nks, g, t4, acc, brs, xw);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_b[s]);

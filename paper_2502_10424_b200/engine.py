@@ -107,7 +107,9 @@ class SpecEngine:
             self.graphs.run(("draft", gamma_step), self._draft_fn(gamma_step), gen)
         self.graphs.run(("verify", gamma_step), self._verify_fn(gamma_step), gen)
         nl = len(self.target.layers)
-        self.launches += gamma_step * self.run.kernel_launches_per_forward(nl) + self.run.kernel_launches_per_forward(nl) + 1
+        fused = self.draft.wmode == _lib.W_INT4 and self.run._fuse_prep(self.draft.layers[0]["qkv"], self.cache.batch)
+        self.launches += (gamma_step * self.run.kernel_launches_per_forward(nl, fused)
+                          + self.run.kernel_launches_per_forward(nl) + 1)
         if not sync:
             return None
         torch.cuda.current_stream().synchronize()

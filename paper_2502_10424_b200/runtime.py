@@ -335,8 +335,12 @@ class Runner:
         return n
 
     # -- linear ---------------------------------------------------------------
+    def _fuse_prep(self, pl: PackedLinear, ncols: int) -> bool:
+        """INT4 layers build their f16 input (+ RMS norm) in-kernel (no qs_prep_act launch)."""
+        return pl.wmode == _lib.W_INT4 and ncols == 1 and pl.K <= 4096
+
     def _linear(self, pl: PackedLinear, src, y, ncols: int, epi: int, *, ldy: int | None = None, layer: int = 0,
-                T: int = 1, row_offset: int = 0, yh=None, stream: int) -> None:
+                T: int = 1, row_offset: int = 0, yh=None, stream: int, xf=None, gain=None) -> None:
         """One stream-K linear launch.  ``src`` = (f16 rows, 16-sums) written by
         ``qs_prep_act`` or a SiLU epilogue; ``yh`` = (f16 rows, 16-sums) output
         of the SiLU epilogue."""
@@ -365,6 +369,10 @@ class Runner:
                 a.ys, a.ldys = yh[1].data_ptr(), yh[1].shape[1]
             a.work = self.work.data_ptr()
             a.counters = self.lin_counters.data_ptr()
+            if xf is not None:
+                a.xf, a.ldxf = xf.data_ptr(), xf.shape[1]
+                a.gain = gain.data_ptr() if gain is not None else None
+                a.eps = float(geo.norm_eps)
             if epi == _lib.EPI_QKV:
                 c = self.cache
                 a.Nq, a.Nk, a.hd, a.T = self.lgeo.nq, self.lgeo.nk, geo.head_dim, T
@@ -478,18 +486,29 @@ class Runner:
                                 self.flags.data_ptr(), s), "qs_embed")
         X, H = (self.xh, self.xs), (self.hh, self.hs)
         for li, lw in enumerate(w.layers):
-            self._prep(self.x, w.attn_norms[li], X, ncols, s)
-            self._linear(lw["qkv"], X, None, ncols, _lib.EPI_QKV, layer=li, T=T, row_offset=row_offset, stream=s)
+            if self._fuse_prep(lw["qkv"], ncols):
+                self._linear(lw["qkv"], X, None, ncols, _lib.EPI_QKV, layer=li, T=T, row_offset=row_offset, stream=s,
+                             xf=self.x, gain=w.attn_norms[li])
+            else:
+                self._prep(self.x, w.attn_norms[li], X, ncols, s)
+                self._linear(lw["qkv"], X, None, ncols, _lib.EPI_QKV, layer=li, T=T, row_offset=row_offset, stream=s)
             self._attention(li, view, T, row_offset, s)  # also writes X = (f16, 16-sums) of its output
             if self.shard is not None:
                 self._gather_heads(ncols)
                 self._prep(self.attn_full, None, X, ncols, s)
             self._linear(lw["o"], X, self.x, ncols, _lib.EPI_ADD, stream=s)
-            self._prep(self.x, w.mlp_norms[li], X, ncols, s)
-            self._linear(lw["gu"], X, None, ncols, _lib.EPI_SILU_MUL, yh=H, stream=s)
+            if self._fuse_prep(lw["gu"], ncols):
+                self._linear(lw["gu"], X, None, ncols, _lib.EPI_SILU_MUL, yh=H, stream=s, xf=self.x,
+                             gain=w.mlp_norms[li])
+            else:
+                self._prep(self.x, w.mlp_norms[li], X, ncols, s)
+                self._linear(lw["gu"], X, None, ncols, _lib.EPI_SILU_MUL, yh=H, stream=s)
             self._linear(lw["down"], H, self.x, ncols, _lib.EPI_ADD, stream=s)
-        self._prep(self.x, w.final_norm, X, ncols, s)
-        self._linear(w.lm_head, X, self.logits, ncols, _lib.EPI_STORE, stream=s)
+        if self._fuse_prep(w.lm_head, ncols):
+            self._linear(w.lm_head, X, self.logits, ncols, _lib.EPI_STORE, stream=s, xf=self.x, gain=w.final_norm)
+        else:
+            self._prep(self.x, w.final_norm, X, ncols, s)
+            self._linear(w.lm_head, X, self.logits, ncols, _lib.EPI_STORE, stream=s)
         if argmax_to is not None:
             _lib.check(lib.qs_argmax(self.logits.data_ptr(), ncols, geo.vocab, argmax_to, 1, s), "qs_argmax")
 
@@ -506,5 +525,7 @@ class Runner:
         for r in range(world):
             full[:, r].copy_(bufs[r])
 
-    def kernel_launches_per_forward(self, nlayers: int) -> int:
-        return 1 + nlayers * 7 + 3
+    def kernel_launches_per_forward(self, nlayers: int, fused_prep: bool = False) -> int:
+        """embed + per layer (prep, QKV, attention, O, prep, gate/up, down) + prep, lm_head, argmax;
+        INT4 layers build their inputs in-kernel (``fused_prep``: no prep launches)."""
+        return 1 + nlayers * (5 if fused_prep else 7) + (2 if fused_prep else 3)
