@@ -77,9 +77,11 @@ struct AttnCfg {
   static constexpr int BIAS_FLOATS = 8 * NQ * 2;          // [block][q][x1 tokens | x16 tokens]
   static constexpr int QSTAGE = (BIAS_OFF + BIAS_FLOATS * 4 + 127) / 128 * 128;
   // ---- fp16 chunks: 64 tokens in the fp16 kernel, 32 in the quantised kernel's tails ----
-  static constexpr int CF = QUANT ? 32 : 64;
+  // quantised kernels' fp1/fp2 tails: the whole 128-token buffer in one pass over all 8 warps
+  // (the tail CTAs run in the second wave, after the main splits, so their latency is exposed)
+  static constexpr int CF = QUANT ? 128 : 64;
   static constexpr int FSTAGE = 2 * CF * HD * 2;
-  static constexpr int NSTAGE_F = 2;
+  static constexpr int NSTAGE_F = QUANT ? 1 : 2;
   static constexpr int REGION_F = NSTAGE_F * FSTAGE;
   static constexpr int MS = HD + 4;
   static constexpr int MERGE_BYTES = NCW * NQ * MS * 4;
@@ -243,9 +245,15 @@ __device__ __forceinline__ void fp16_region(uint8_t* region, uint32_t* bqf, cons
   const int mt = warp;
   const bool has_tile = mt * 16 < CF && warp < C::NCW;
   for (int i = 0; i < nchunk; ++i) {
-    cp_async_wait<C::NSTAGE_F - 2>();
+    if constexpr (C::NSTAGE_F == 1) {
+      if (i > 0) __syncthreads();  // every warp is done with the previous chunk
+      issue_f(i);
+      cp_async_wait<0>();
+    } else {
+      cp_async_wait<C::NSTAGE_F - 2>();
+    }
     __syncthreads();
-    issue_f(i + C::NSTAGE_F - 1);
+    if constexpr (C::NSTAGE_F > 1) issue_f(i + C::NSTAGE_F - 1);
     if (!has_tile) continue;
     const int c = c_begin + i;
     const __half* ks_ = fstage(i % C::NSTAGE_F);
@@ -393,9 +401,15 @@ __device__ __forceinline__ void fp16_region_q(uint8_t* region, uint32_t* aqf, co
   const bool has_tile = mt * 16 < CF && warp < C::NCW;
   const int ii = lane >> 3, rr = lane & 7;
   for (int i = 0; i < nchunk; ++i) {
-    cp_async_wait<C::NSTAGE_F - 2>();
+    if constexpr (C::NSTAGE_F == 1) {
+      if (i > 0) __syncthreads();  // every warp is done with the previous chunk
+      issue_f(i);
+      cp_async_wait<0>();
+    } else {
+      cp_async_wait<C::NSTAGE_F - 2>();
+    }
     __syncthreads();
-    issue_f(i + C::NSTAGE_F - 1);
+    if constexpr (C::NSTAGE_F > 1) issue_f(i + C::NSTAGE_F - 1);
     if (!has_tile) continue;
     const int c = c_begin + i;
     const __half* ks_ = fstage(i % C::NSTAGE_F);
