@@ -36,7 +36,7 @@ METRIC = "decode tokens/sec @128K ctx + speedup vs FP16 AR; attn HBM GB/s vs pea
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=24)
+    p.add_argument("--steps", type=int, default=48)
     p.add_argument("--warmup", type=int, default=4)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--context", type=int, default=131072)

@@ -357,7 +357,7 @@ def _act_buffers(x):
     return xh, xs
 
 
-def _run_linear(pl, x, ncols, *, epi=None, nctas=None, y=None, yh=None):
+def _run_linear(pl, x, ncols, *, epi=None, nctas=None, y=None, yh=None, xf=None, gain=None, eps=1e-5):
     import ctypes
 
     from paper_2502_10424_b200.runtime import linear_grid
@@ -383,9 +383,12 @@ def _run_linear(pl, x, ncols, *, epi=None, nctas=None, y=None, yh=None):
     work = torch.full((mg * a.maxc * 16 * 64,), float("nan"), device="cuda")
     cnt = torch.zeros(mg + 1, dtype=torch.int32, device="cuda")
     a.work, a.counters = work.data_ptr(), cnt.data_ptr()
+    if xf is not None:  # INT4 in-kernel activation prep (xh / xs are then not read)
+        a.xf, a.ldxf, a.eps = xf.data_ptr(), xf.shape[1], eps
+        a.gain = gain.data_ptr() if gain is not None else None
     _lib.check(_lib.load().qs_linear(a, _lib.stream_ptr()))
     torch.cuda.synchronize()
-    assert int(cnt.sum().item()) == 0  # stream-K tile counters reset by the last contributor
+    assert int(cnt.sum().item()) == 0  # the kernels need no cross-CTA workspace
     return y
 
 
@@ -413,21 +416,47 @@ def test_linear_vs_torch(K, N, ncols, mode):
 
 
 @pytest.mark.parametrize("mode", ["f16", "int4"])
-@pytest.mark.parametrize("nctas", [1, 7, 148, 296, 1000])
-def test_linear_stream_k_grids(mode, nctas):
-    """Any grid size (units per CTA from <1 to whole tiles) reduces correctly."""
+@pytest.mark.parametrize("K,N", [(1024, 576), (272, 48), (4112, 80), (64, 16), (4096, 4112)])
+@pytest.mark.parametrize("ncols", [1, 3])
+def test_linear_ragged_shapes(mode, K, N, ncols):
+    """Odd tile counts (a zero padding tile in the last pair), K ranges ending inside a
+    stage, a single tile, more pairs than SMs."""
     from paper_2502_10424_b200.runtime import PackedLinear
 
-    K, N, ncols = 1024, 576, 3
-    g = torch.Generator(device="cuda").manual_seed(nctas)
+    g = torch.Generator(device="cuda").manual_seed(K + N + ncols)
     w = torch.randn(K, N, device="cuda", generator=g) / math.sqrt(K)
     x = torch.randn(ncols, K, device="cuda", generator=g)
-    pl = PackedLinear.f16(w) if mode == "f16" else PackedLinear.int4(w, 64)
+    pl = PackedLinear.f16(w) if mode == "f16" else PackedLinear.int4(w, 16)
     wref = w.half().float() if mode == "f16" else torch.from_numpy(
-        qs.dequantize_weights(qs.quantize_weights(w.cpu().numpy(), 64))).cuda()
-    y = _run_linear(pl, x, ncols, nctas=nctas)
+        qs.dequantize_weights(qs.quantize_weights(w.cpu().numpy(), 16))).cuda()
+    y = _run_linear(pl, x, ncols)
     ref = x.half().float() @ wref
     assert (y - ref).abs().max().item() <= 2e-3 * ref.abs().max().item() + 1e-4
+
+
+@pytest.mark.parametrize("K,N,epi", [(4096, 4096, 0), (4096, 22016, 0), (128, 4112, 0), (4096, 4096, 1)])
+@pytest.mark.parametrize("with_gain", [False, True])
+def test_int4_in_kernel_prep_matches_prep_act(K, N, epi, with_gain):
+    """The INT4 kernel building its f16 input (+ RMS norm) from f32 rows equals
+    qs_prep_act + the same kernel reading xh / xs (up to the norm's summation order)."""
+    from paper_2502_10424_b200.runtime import PackedLinear
+
+    g = torch.Generator(device="cuda").manual_seed(K + N)
+    w = torch.randn(K, N, device="cuda", generator=g) / math.sqrt(K)
+    x = torch.randn(1, K, device="cuda", generator=g) * 3.0
+    gain = (torch.rand(K, device="cuda", generator=g) + 0.5) if with_gain else None
+    pl = PackedLinear.int4(w, 32)
+    # reference: qs_prep_act (rmsnorm when gain) -> f16 + 16-sums -> the kernel
+    xh = torch.zeros(1, K + 64, dtype=torch.float16, device="cuda")
+    xs = torch.zeros(1, (K // 16 + 4 + 3) // 4 * 4, device="cuda")
+    _lib.check(_lib.load().qs_prep_act(x.data_ptr(), gain.data_ptr() if gain is not None else None, 1e-5,
+                                       xh.data_ptr(), xh.shape[1], xs.data_ptr(), xs.shape[1], 1, K,
+                                       _lib.stream_ptr()))
+    base = torch.randn(1, N, device="cuda", generator=g)
+    y0, y1 = base.clone(), base.clone()
+    want = _run_linear(pl, xh[:, :K].float(), 1, epi=epi, y=y0)  # the (normed) f16 rows as input
+    got = _run_linear(pl, x, 1, epi=epi, y=y1, xf=x, gain=gain)
+    assert (got - want).abs().max().item() <= 1e-3 * want.abs().max().item() + 1e-5
 
 
 @pytest.mark.parametrize("mode", ["f16", "int4"])
