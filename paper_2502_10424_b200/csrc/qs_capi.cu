@@ -208,8 +208,8 @@ qs_status qs_linear(const qs_linear_args* a, void* stream) {
   if (a->maxc < qs::linear_maxc(a->wmode, a->N, a->K, a->nctas))
     QS_FAIL(QS_ERR_CONFIG, "workspace slots (maxc=%d) too few for this grid", a->maxc);
   if (a->xf) {
-    if (a->wmode != QS_W_INT4 || a->ncols != 1 || a->K > 4096 || a->ldxf % 4 || a->ldxf < a->K)
-      QS_FAIL(QS_ERR_CONFIG, "in-kernel activation prep needs INT4 weights, one row, K <= 4096, 16-byte rows");
+    if (a->ncols != 1 || a->K > 4096 || a->ldxf % 4 || a->ldxf < a->K)
+      QS_FAIL(QS_ERR_CONFIG, "in-kernel activation prep needs one row, K <= 4096, 16-byte rows");
   } else if (a->ldxh % 8 || a->ldxh < a->K + 64 ||
              (a->wmode == QS_W_INT4 && (a->ldxs % 4 || a->ldxs < a->K / 16 + 4))) {
     QS_FAIL(QS_ERR_CONFIG, "activation buffers need padded, 16-byte aligned rows");

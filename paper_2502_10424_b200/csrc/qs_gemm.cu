@@ -143,6 +143,83 @@ __device__ __forceinline__ void linear_epilogue(const LinearParams& P, float* ys
 }
 
 
+// One activation row -> f16 copy (RMS-normalised when gain != NULL, Q/tensor.py:35-42) + the sums
+// of every 16 f16-rounded values.  Work is done by threads [0, 256) in a fixed mapping (one 16-element
+// group per thread per round, fixed reduction tree), so every caller produces identical bits --
+// qs_prep_act and the linear kernels' in-kernel prep must agree for a T-row verify to equal T
+// single-row steps.  BAR: 0 = __syncthreads, else a named barrier over BAR threads (all of which call).
+template <int BAR>
+__device__ __forceinline__ void act_prep_row(const float* __restrict__ xr, const float* __restrict__ gain, float eps,
+                                             int d, __half* __restrict__ hr, float* __restrict__ sr, float* red,
+                                             int tid) {
+  constexpr int NW = 256;
+  auto sync = [] {
+    if constexpr (BAR == 0) __syncthreads();
+    else asm volatile("bar.sync 3, %0;" ::"n"(BAR));
+  };
+  const int ng = d / 16;
+  float scale = 1.f;
+  if (gain) {
+    if (tid < NW) {
+      float a = 0.f;
+      for (int gi = tid; gi < ng; gi += NW) {
+        const float4* p = reinterpret_cast<const float4*>(xr + gi * 16);
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = p[j];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          a += __fmul_rn(v[j].x, v[j].x);
+          a += __fmul_rn(v[j].y, v[j].y);
+          a += __fmul_rn(v[j].z, v[j].z);
+          a += __fmul_rn(v[j].w, v[j].w);
+        }
+      }
+      a = warp_sum(a);
+      if ((tid & 31) == 0) red[tid >> 5] = a;
+    }
+    sync();
+    if (tid < 32) {
+      float v = tid < NW / 32 ? red[tid] : 0.f;
+      v = warp_sum(v);
+      if (tid == 0) red[32] = __fsqrt_rn(__fadd_rn(__fdiv_rn(v, (float)d), eps));
+    }
+    sync();
+    scale = red[32];
+  }
+  if (tid < NW) {
+    for (int gi = tid; gi < ng; gi += NW) {
+      float xv[16], gv[16];
+      const float4* p = reinterpret_cast<const float4*>(xr + gi * 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 v = p[j];
+        xv[4 * j] = v.x; xv[4 * j + 1] = v.y; xv[4 * j + 2] = v.z; xv[4 * j + 3] = v.w;
+      }
+      if (gain) {
+        const float4* gp = reinterpret_cast<const float4*>(gain + gi * 16);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 v = gp[j];
+          gv[4 * j] = v.x; gv[4 * j + 1] = v.y; gv[4 * j + 2] = v.z; gv[4 * j + 3] = v.w;
+        }
+      }
+      float s = 0.f;
+      __align__(16) __half hv[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float v = gain ? __fmul_rn(__fdiv_rn(xv[j], scale), gv[j]) : xv[j];
+        hv[j] = __float2half_rn(v);
+        s += __half2float(hv[j]);
+      }
+      *reinterpret_cast<uint4*>(hr + gi * 16) = *reinterpret_cast<uint4*>(hv);
+      *reinterpret_cast<uint4*>(hr + gi * 16 + 8) = *reinterpret_cast<uint4*>(hv + 8);
+      sr[gi] = s;
+    }
+  }
+  sync();
+}
+
 // ---------------------------------------------------------------------------
 // INT4 W4A16 GEMV/GEMM without cross-CTA reduction (the draft's weights).
 //
@@ -380,54 +457,9 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
   pdl_wait();
   pdl_trigger();
   if (act_in) {
-    // f16 activations (+ RMS norm) and their 16-sums for the whole K range, once per CTA,
-    // while the first weight stages are still in flight (numerics of qs_prep_act)
-    float* red = ysm;  // scratch [NCW] (ysm is not used before the first epilogue)
-    constexpr int NT_ = C::NCW * 32;
-    for (int c = 0; c < ncols; ++c) {
-      const float* xr = P.xf + (size_t)c * P.ldxf;
-      float scale = 1.f;
-      if (P.gain) {
-        float a = 0.f;
-        for (int i = tid; i < P.K / 4; i += NT_) {
-          const float4 v = reinterpret_cast<const float4*>(xr)[i];
-          a += __fmul_rn(v.x, v.x);
-          a += __fmul_rn(v.y, v.y);
-          a += __fmul_rn(v.z, v.z);
-          a += __fmul_rn(v.w, v.w);
-        }
-        a = warp_sum(a);
-        if (lane == 0) red[warp] = a;
-        asm volatile("bar.sync 2, %0;" ::"n"(NT_));
-        float tot = 0.f;
-#pragma unroll
-        for (int w = 0; w < C::NCW; ++w) tot += red[w];
-        scale = __fsqrt_rn(__fadd_rn(__fdiv_rn(tot, (float)P.K), P.eps));
-        asm volatile("bar.sync 2, %0;" ::"n"(NT_));  // red reuse by the next column
-      }
-      __half* hr = reinterpret_cast<__half*>(act_h + c * C::ACT_ROW);
-      for (int gi = tid; gi < P.K / 16; gi += NT_) {
-        float s16 = 0.f;
-        __align__(16) __half hv[16];
-#pragma unroll
-        for (int j4 = 0; j4 < 4; ++j4) {
-          const float4 v = reinterpret_cast<const float4*>(xr + gi * 16)[j4];
-          float4 gv = make_float4(1.f, 1.f, 1.f, 1.f);
-          if (P.gain) gv = reinterpret_cast<const float4*>(P.gain + gi * 16)[j4];
-          const float e[4] = {v.x, v.y, v.z, v.w}, gg[4] = {gv.x, gv.y, gv.z, gv.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float y = P.gain ? __fmul_rn(__fdiv_rn(e[q], scale), gg[q]) : e[q];
-            hv[j4 * 4 + q] = __float2half_rn(y);
-            s16 += __half2float(hv[j4 * 4 + q]);
-          }
-        }
-        *reinterpret_cast<uint4*>(hr + gi * 16) = *reinterpret_cast<uint4*>(hv);
-        *reinterpret_cast<uint4*>(hr + gi * 16 + 8) = *reinterpret_cast<uint4*>(hv + 8);
-        act_s[c * C::ACT_SROW + gi] = s16;
-      }
-    }
-    asm volatile("bar.sync 2, %0;" ::"n"(NT_));
+    // f16 activation (+ RMS norm) and its 16-sums for the whole K range, once per CTA, while the
+    // first weight stages are still in flight (the same bits qs_prep_act would write)
+    act_prep_row<C::NCW * 32>(P.xf, P.gain, P.eps, P.K, reinterpret_cast<__half*>(act_h), act_s, ysm, tid);
   }
 
   // ======================= consumer warps =======================
@@ -512,7 +544,11 @@ struct F16Cfg {
   static constexpr int OFF_B = WBYTES;
   static constexpr int STAGE = (OFF_B + ROWS * BROW + 127) / 128 * 128;
   static constexpr int YCOLS = 8 * NTC;
-  static constexpr int FIXED = KP * 32 * YCOLS * 4 + 2 * 8 * 8 + 16;
+  // single-column steps may build their f16 activation row in-kernel (ACT_K <= 4096)
+  static constexpr int ACT_K = 4096;
+  static constexpr int ACT_ROW = NTC == 1 ? ACT_K * 2 : 0;
+  static constexpr int ACT_SROW = NTC == 1 ? ACT_K / 16 * 4 : 0;
+  static constexpr int FIXED = KP * 32 * YCOLS * 4 + 2 * 8 * 8 + 16 + ACT_ROW + ACT_SROW;
   static constexpr int NSTAGE = (232448 - FIXED) / STAGE < 8 ? (232448 - FIXED) / STAGE : 8;
   static constexpr int SMEM = NSTAGE * STAGE + FIXED;
 };
@@ -527,11 +563,14 @@ __global__ void __launch_bounds__(F16Cfg<NTC>::THREADS) linear_f16p_kernel(const
   float* hsm = ysm + 32 * COLS;
   uint64_t* full_b = reinterpret_cast<uint64_t*>(hsm + (C::KP - 1) * 32 * COLS);
   uint64_t* empty_b = full_b + 8;
+  uint8_t* act_h = reinterpret_cast<uint8_t*>(empty_b + 8) + 16;  // [ACT_ROW] f16 row
+  float* act_s = reinterpret_cast<float*>(act_h + C::ACT_ROW);     // 16-sums (unused by the f16 math)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int KS = P.K / 16;
   const int TP = (P.N / 16 + 1) / 2;
+  const bool act_in = C::ACT_ROW > 0 && P.xf != nullptr;
   const int nst = (KS + KCH - 1) / KCH;
   const int npairs = (TP - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   const int total = npairs * nst;
@@ -552,7 +591,7 @@ __global__ void __launch_bounds__(F16Cfg<NTC>::THREADS) linear_f16p_kernel(const
       const int tp = blockIdx.x + (q / nst) * gridDim.x, u = q % nst;
       const int ks0 = u * KCH, nks = min(KCH, KS - ks0);
       const uint32_t wb = (uint32_t)nks * 1024, bb = (uint32_t)nks * 32;
-      mbar_arrive_expect_tx(&full_b[s], wb + ncols * bb);
+      mbar_arrive_expect_tx(&full_b[s], wb + (act_in ? 0u : ncols * bb));
       bulk_g2s(sm + s * C::STAGE, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)tp * KS + ks0) * 1024, wb, &full_b[s]);
     };
     auto issue_act = [&](int q) {
@@ -574,7 +613,7 @@ __global__ void __launch_bounds__(F16Cfg<NTC>::THREADS) linear_f16p_kernel(const
           mbar_wait(&empty_b[q % C::NSTAGE], ((q / C::NSTAGE) - 1) & 1);
           issue_static(q);
         }
-        issue_act(q);
+        if (!act_in) issue_act(q);
       }
     }
     __syncwarp();
@@ -582,6 +621,7 @@ __global__ void __launch_bounds__(F16Cfg<NTC>::THREADS) linear_f16p_kernel(const
   }
   pdl_wait();
   pdl_trigger();
+  if (act_in) act_prep_row<C::NCW * 32>(P.xf, P.gain, P.eps, P.K, reinterpret_cast<__half*>(act_h), act_s, ysm, tid);
 
   const int tile = warp & 1, kp = warp >> 1;
   const int rr = tile * 16 + g;
@@ -600,7 +640,9 @@ __global__ void __launch_bounds__(F16Cfg<NTC>::THREADS) linear_f16p_kernel(const
       if (nks > 0 && !(P.dbg & 1)) {
         const uint8_t* sp = sm + s * C::STAGE;
         const uint4* wa = reinterpret_cast<const uint4*>(sp) + ko * 64 + tile * 32 + lane;
-        const uint8_t* bst = sp + C::OFF_B + g * C::BROW + 4 * t4 + ko * 32;
+        // B rows: the streamed activation rows, or every lane on the in-kernel row (ncols == 1)
+        const uint8_t* bst = act_in ? act_h + 4 * t4 + (u * KCH + ko) * 32
+                                    : sp + C::OFF_B + g * C::BROW + 4 * t4 + ko * 32;
 #pragma unroll
         for (int ks = 0; ks < C::HKS; ++ks) {
           if (ks < nks) {
@@ -727,74 +769,14 @@ static cudaError_t launch_i4_n(const LinearParams& p, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 // activation prep: f16 copy (optionally RMS-normalised) + 16-sums
 // ---------------------------------------------------------------------------
-__global__ void prep_act_kernel(const float* __restrict__ x, const float* __restrict__ gain, float eps,
-                                __half* __restrict__ xh, long long ldxh, float* __restrict__ xs, long long ldxs,
-                                int d) {
+__global__ void __launch_bounds__(256) prep_act_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                                                       float eps, __half* __restrict__ xh, long long ldxh,
+                                                       float* __restrict__ xs, long long ldxs, int d) {
   pdl_wait();
   pdl_trigger();
-  const float* xr = x + (size_t)blockIdx.x * d;
-  __half* hr = xh + (size_t)blockIdx.x * ldxh;
-  float* sr = xs + (size_t)blockIdx.x * ldxs;
-  __shared__ float red[32];
-  __shared__ float s_inv;
-  const int ng = d / 16;
-  float scale = 1.f;
-  if (gain) {
-    // one thread per 16-element group, four 16-byte loads in flight per group
-    float a = 0.f;
-    for (int gi = threadIdx.x; gi < ng; gi += blockDim.x) {
-      const float4* p = reinterpret_cast<const float4*>(xr + gi * 16);
-      float4 v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = p[j];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        a += __fmul_rn(v[j].x, v[j].x);
-        a += __fmul_rn(v[j].y, v[j].y);
-        a += __fmul_rn(v[j].z, v[j].z);
-        a += __fmul_rn(v[j].w, v[j].w);
-      }
-    }
-    a = warp_sum(a);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-      v = warp_sum(v);
-      if (threadIdx.x == 0) s_inv = __fsqrt_rn(__fadd_rn(__fdiv_rn(v, (float)d), eps));
-    }
-    __syncthreads();
-    scale = s_inv;
-  }
-  // one thread per 16-element group: convert, store, sum the rounded values
-  for (int gi = threadIdx.x; gi < ng; gi += blockDim.x) {
-    float xv[16], gv[16];
-    const float4* p = reinterpret_cast<const float4*>(xr + gi * 16);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 v = p[j];
-      xv[4 * j] = v.x; xv[4 * j + 1] = v.y; xv[4 * j + 2] = v.z; xv[4 * j + 3] = v.w;
-    }
-    if (gain) {
-      const float4* gp = reinterpret_cast<const float4*>(gain + gi * 16);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float4 v = gp[j];
-        gv[4 * j] = v.x; gv[4 * j + 1] = v.y; gv[4 * j + 2] = v.z; gv[4 * j + 3] = v.w;
-      }
-    }
-    float s = 0.f;
-    __align__(16) __half hv[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float v = gain ? __fmul_rn(__fdiv_rn(xv[j], scale), gv[j]) : xv[j];
-      hv[j] = __float2half_rn(v);
-      s += __half2float(hv[j]);
-    }
-    *reinterpret_cast<uint4*>(hr + gi * 16) = *reinterpret_cast<uint4*>(hv);
-    *reinterpret_cast<uint4*>(hr + gi * 16 + 8) = *reinterpret_cast<uint4*>(hv + 8);
-    sr[gi] = s;
-  }
+  __shared__ float red[33];
+  act_prep_row<0>(x + (size_t)blockIdx.x * d, gain, eps, d, xh + (size_t)blockIdx.x * ldxh,
+                  xs + (size_t)blockIdx.x * ldxs, red, threadIdx.x);
 }
 
 cudaError_t launch_prep_act(const float* x, const float* gain, float eps, void* xh, long long ldxh, float* xs,

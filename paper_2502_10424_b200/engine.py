@@ -107,7 +107,7 @@ class SpecEngine:
             self.graphs.run(("draft", gamma_step), self._draft_fn(gamma_step), gen)
         self.graphs.run(("verify", gamma_step), self._verify_fn(gamma_step), gen)
         nl = len(self.target.layers)
-        fused = self.draft.wmode == _lib.W_INT4 and self.run._fuse_prep(self.draft.layers[0]["qkv"], self.cache.batch)
+        fused = self.run._fuse_prep(self.draft.layers[0]["qkv"], self.cache.batch)
         self.launches += (gamma_step * self.run.kernel_launches_per_forward(nl, fused)
                           + self.run.kernel_launches_per_forward(nl) + 1)
         if not sync:
@@ -164,7 +164,8 @@ class ARAutoEngine:
         """Decode one token (appends it to the cache); returns it when sync."""
         torch = _torch()
         self.graphs.run(("ar",), self._step_fn(), self.cache.generation)
-        self.launches += self.run.kernel_launches_per_forward(len(self.target.layers)) + 2
+        fused = self.run._fuse_prep(self.target.layers[0]["qkv"], self.cache.batch)
+        self.launches += self.run.kernel_launches_per_forward(len(self.target.layers), fused) + 2
         if self.is_fp:
             self.cache._len += 1
         else:

@@ -336,8 +336,9 @@ class Runner:
 
     # -- linear ---------------------------------------------------------------
     def _fuse_prep(self, pl: PackedLinear, ncols: int) -> bool:
-        """INT4 layers build their f16 input (+ RMS norm) in-kernel (no qs_prep_act launch)."""
-        return pl.wmode == _lib.W_INT4 and ncols == 1 and pl.K <= 4096
+        """Single-row steps build their f16 input (+ RMS norm) in the linear kernel (no
+        qs_prep_act launch); both run act_prep_row, so the bits are the same either way."""
+        return ncols == 1 and pl.K <= 4096
 
     def _linear(self, pl: PackedLinear, src, y, ncols: int, epi: int, *, ldy: int | None = None, layer: int = 0,
                 T: int = 1, row_offset: int = 0, yh=None, stream: int, xf=None, gain=None) -> None:
@@ -527,5 +528,5 @@ class Runner:
 
     def kernel_launches_per_forward(self, nlayers: int, fused_prep: bool = False) -> int:
         """embed + per layer (prep, QKV, attention, O, prep, gate/up, down) + prep, lm_head, argmax;
-        INT4 layers build their inputs in-kernel (``fused_prep``: no prep launches)."""
+        single-row steps build their inputs in-kernel (``fused_prep``: no prep launches)."""
         return 1 + nlayers * (5 if fused_prep else 7) + (2 if fused_prep else 3)
