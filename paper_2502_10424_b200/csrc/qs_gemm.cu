@@ -234,18 +234,25 @@ __device__ __forceinline__ void act_prep_row(const float* __restrict__ xr, const
 // stage; the four k-quarters of a tile are summed through shared memory in fixed order at the
 // pair's end.  PDL overlaps the first weight stages with the previous kernel.
 // ---------------------------------------------------------------------------
+#ifndef QS_I4_KCH1
+#define QS_I4_KCH1 128  // A/B builds: k-steps per stage of the single-row INT4 config
+#endif
 template <int NTC, int GKS, int CW>
 struct I4Cfg {
   static constexpr int KP = 8;                                    // k-parts: warps per tile
   static constexpr int NCW = 2 * KP;                              // tile w&1, k-part w>>1
   static constexpr int THREADS = (NCW + 1) * 32;
-  static constexpr int KCH = 128;                                 // k-steps per stage
+  static constexpr bool SINGLE = NTC == 1 && CW == 1;             // one activation row
+  static constexpr int KCH = SINGLE ? QS_I4_KCH1 : 128;           // k-steps per stage
+  static constexpr int MINB = (SINGLE && KCH <= 64) ? 2 : 1;      // resident CTAs per SM
+  static constexpr int SMEM_CAP = MINB == 2 ? 233472 / 2 - 1024 : 232448;
   static constexpr int HKS = KCH / KP;                            // k-steps per consumer warp per stage
   static constexpr int WBYTES = (KCH / 4) * 2 * 512;              // codes of both tiles
   static constexpr int ROWS = NTC == 1 ? CW : 16;
-  static constexpr int BROW = KCH * 32 + 16;
+  static constexpr int RPAD = ROWS > 1 ? 16 : 0;                  // bank skew between activation rows
+  static constexpr int BROW = KCH * 32 + RPAD;
   static constexpr int PBYTES = (KCH / GKS) * 2 * 128;            // {S,Z} x 16 rows x 2 tiles per group
-  static constexpr int XROW = KCH * 4 + 16;
+  static constexpr int XROW = KCH * 4 + RPAD;
   static constexpr int OFF_B = WBYTES;
   static constexpr int OFF_P = OFF_B + ROWS * BROW;
   static constexpr int OFF_X = OFF_P + PBYTES;
@@ -254,18 +261,20 @@ struct I4Cfg {
   // in-kernel activation prep (P.xf): the f16 row + 16-sums of up to ACT_K inputs
   // (one activation row -- the draft's T = 1 -- of up to 4096 inputs: the normed projections)
   static constexpr int ACT_K = 4096;
-  static constexpr int ACT_ROW = ACT_K * 2 + 16;
-  static constexpr int ACT_SROW = ACT_K / 16 + 4;
-  static constexpr int ACT_BYTES = (NTC == 1 && CW == 1) ? ACT_ROW + ACT_SROW * 4 + 64 : 0;
-  static constexpr int FIXED = KP * 32 * YCOLS * 4 + 2 * 8 * 8 + 16 + ACT_BYTES;
-  static constexpr int NSTAGE = (232448 - FIXED) / STAGE < 8 ? (232448 - FIXED) / STAGE : 8;  // one CTA per SM
+  static constexpr int ACT_ROW = ACT_K * 2;
+  static constexpr int ACT_SROW = ACT_K / 16;
+  static constexpr int ACT_BYTES = (NTC == 1 && CW == 1) ? ACT_ROW + ACT_SROW * 4 : 0;
+  // k-part partials (the results ysm alias slot 0) + barriers + act row; trimmed so that the
+  // single-row config holds four 52.5 KB stages (210 KB of weights in flight per SM)
+  static constexpr int FIXED = (KP - 1) * 32 * YCOLS * 4 + 2 * 8 * 8 + 16 + ACT_BYTES;
+  static constexpr int NSTAGE = (SMEM_CAP - FIXED) / STAGE < 8 ? (SMEM_CAP - FIXED) / STAGE : 8;
   static constexpr int SMEM = NSTAGE * STAGE + FIXED;
 };
 
 // HKS k-steps of one 16-row tile for one consumer warp (window / group-slot scheme of
 // int4_unit; pair-major strides).  wa: this lane's first uint4 of the k-range; bbase: B rows
 // at the k-range; pp: float4 params of the first group (this tile, row g); xsm: 16-sums.
-template <class C, int NTC, int GKS, int CW>
+template <class C, int NTC, int GKS, int CW, bool NOMMA = false>
 __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uint8_t* bbase, const float4* pp,
                                          const float* xsm, const int nks, const int g, const int t4,
                                          float (&acc)[NTC][4], const int brs, const int XW) {
@@ -305,7 +314,10 @@ __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uin
               b0 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32);
               b1 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32 + 16);
             }
-            mma_acc(D2[(sl * GKS + j) & 1][nt], a, b0, b1);
+            if constexpr (NOMMA)  // diagnostic (dbg bit 2): same operand traffic, no tensor-core op
+              D2[(sl * GKS + j) & 1][nt][0] += __uint_as_float((a[0] ^ a[1] ^ a[2] ^ a[3] ^ b0 ^ b1) & 0x3fffffffu);
+            else
+              mma_acc(D2[(sl * GKS + j) & 1][nt], a, b0, b1);
           }
         }
       }
@@ -376,13 +388,13 @@ __device__ __forceinline__ void i4_quad_sum(float (&acc)[NTC][4]) {
 }
 
 template <int NTC, int EPI, int GKS, int CW>
-__global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel(const __grid_constant__ LinearParams P) {
+__global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS, I4Cfg<NTC, GKS, CW>::MINB) linear_i4_kernel(const __grid_constant__ LinearParams P) {
   using C = I4Cfg<NTC, GKS, CW>;
   constexpr int COLS = 8 * NTC;
   constexpr int KCH = C::KCH;
   extern __shared__ __align__(128) uint8_t sm[];
-  float* ysm = reinterpret_cast<float*>(sm + C::NSTAGE * C::STAGE);  // [32][COLS] results
-  float* hsm = ysm + 32 * COLS;                                       // [KP-1][32][COLS] k-part partials
+  float* hsm = reinterpret_cast<float*>(sm + C::NSTAGE * C::STAGE);  // [KP-1][32][COLS] k-part partials
+  float* ysm = hsm;  // [32][COLS] results: slot 0, overwritten by the thread that read it
   uint64_t* full_b = reinterpret_cast<uint64_t*>(hsm + (C::KP - 1) * 32 * COLS);
   uint64_t* empty_b = full_b + 8;
   uint8_t* act_h = reinterpret_cast<uint8_t*>(empty_b + 8) + 16;                // [ACT_ROW] f16 row
@@ -485,7 +497,9 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS) linear_i4_kernel
         const float* xsm = act_in ? act_s + kabs : reinterpret_cast<const float*>(sp + C::OFF_X) + ko;
         const uint8_t* bb = act_in ? act_h + kabs * 32 : sp + C::OFF_B + ko * 32;
         const int brs = act_in ? C::ACT_ROW : C::BROW, xw = act_in ? C::ACT_SROW : C::XROW / 4;
-        if (nks >= C::HKS)
+        if (P.dbg & 2)
+          i4_steps<C, NTC, GKS, CW, true>(wa, bb, pp, xsm, min(nks, C::HKS), g, t4, acc, brs, xw);
+        else if (nks >= C::HKS)
           i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, C::HKS, g, t4, acc, brs, xw);
         else
           i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, nks, g, t4, acc, brs, xw);
@@ -742,7 +756,8 @@ static cudaError_t launch_i4_t(const LinearParams& p, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  return launch_pdl(kern, dim3(pairs < sms ? pairs : sms), dim3(C::THREADS), C::SMEM, s, p);
+  const int slots = sms * C::MINB;
+  return launch_pdl(kern, dim3(pairs < slots ? pairs : slots), dim3(C::THREADS), C::SMEM, s, p);
 }
 
 template <int NTC, int GKS, int CW>
