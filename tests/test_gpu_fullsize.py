@@ -27,9 +27,10 @@ def store():
     kv = H * HD
     k = torch.randn(S_P, kv, device="cuda", generator=g) * (torch.rand(kv, device="cuda", generator=g) * 1.8 + 0.2)
     v = torch.randn(S_P, kv, device="cuda", generator=g)
-    cache = qs.HierarchicalKVCache.from_prefill(qs.CacheLayout(1, H, HD, G), [k.half()], [v.half()],
-                                                max_tokens=S_P + 2 * G)
+    k16, v16 = k.half(), v.half()
     del k, v
+    cache = qs.HierarchicalKVCache.from_prefill(qs.CacheLayout(1, H, HD, G), [k16], [v16], max_tokens=S_P + 2 * G)
+    cache.prompt = (k16, v16)  # kept for the block checks below
     return cache
 
 
@@ -74,7 +75,7 @@ def test_attention_full_size_vs_fp32_reference(store, view, T):
         cache.fp_k[0, 0, 1, :, base + t] = new_k[t]
         cache.fp_v[0, 0, 1, :, base + t] = new_v[t]
     geo = Geometry(1, H * HD, H, H, HD, 16, 16, 1 << 20)
-    run = Runner(geo, cache, max_cols=8)
+    run = Runner(geo, cache, max_cols=16)
     q = torch.randn(T, H * HD, device="cuda", generator=g) * 2.0
     run.q[:T] = q
     run._attention(0, _lib.VIEW_DRAFT if view == "draft" else _lib.VIEW_TARGET, T, 0, _lib.stream_ptr())
@@ -90,3 +91,37 @@ def test_attention_full_size_vs_fp32_reference(store, view, T):
         want = _reference(q[t].view(H, HD), [qk, f1k, f2k[:n2]], [qv, f1v, f2v[:n2]])
         err = (got[t] - want).abs().max().item()
         assert err <= 2e-3 * vmax, (view, t, err, vmax)
+
+
+def _check_block(cache, block, k_rows, v_rows):
+    import numpy as np
+
+    from oracle import qs_oracle as O
+
+    want = O.quantize_kv_block(O.Layout(1, H, HD, G), k_rows, v_rows)
+    got = cache.export_block_planes(0, block)
+    for gp, wp in zip(got, (want.ku, want.kl, want.vu, want.vl)):
+        assert np.array_equal(gp.codes, wp.codes), block
+        assert np.array_equal(gp.scales.view(np.uint32), wp.scales.view(np.uint32)), block
+        assert np.array_equal(gp.zeros.view(np.uint32), wp.zeros.view(np.uint32)), block
+
+
+def test_full_size_blocks_and_flush_bit_exact(store):
+    """Prefill blocks at the start, middle and end of the 1023-block arena, then a decode-time
+    flush into block 1023 (fp1 -> planes, fp2 -> fp1), bit-exact against the oracle's
+    quantize_kv_block (Q/cache.py:249-303) on the same fp16 rows.  Runs last: it mutates the store."""
+    cache = store
+    k16, v16 = cache.prompt
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    for b in (0, 511, 1022):
+        _check_block(cache, b, f(k16[b * G : (b + 1) * G]), f(v16[b * G : (b + 1) * G]))
+    fp1_k, fp1_v = (f(x) for x in _fp(cache, 0, G))
+    g = torch.Generator(device="cuda").manual_seed(99)
+    base = cache.fp2_len
+    rows_k = torch.randn(G - base, H * HD, device="cuda", generator=g).half()
+    rows_v = torch.randn(G - base, H * HD, device="cuda", generator=g).half()
+    for t in range(G - base):
+        cache.append_decode_token(0, rows_k[t], rows_v[t])
+    assert cache.fp2_len == G and cache.flush_if_full()
+    assert cache.quantized_token_count == 1024 * G and cache.fp2_len == 0 and cache.fp1_len == G
+    _check_block(cache, 1023, fp1_k, fp1_v)
