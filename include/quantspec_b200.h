@@ -122,9 +122,10 @@ typedef struct {
   const void* rope;   /* float2 [max_pos][hd/2] (cos, sin)           */
   int max_pos;
   int dbg;            /* 0; diagnostic bits (1: consumers skip the MMA work, 2: no tile reduction) */
-  /* INT4 only, optional: build the f16 activations + 16-sums inside the kernel from f32 rows
-   * xf [ncols][ldxf] (RMS-normalised with `gain` when non-NULL, Q/tensor.py:35-42) instead of
-   * reading xh / xs -- replaces a qs_prep_act launch; one row (ncols = 1), K <= 4096 */
+  /* optional (both weight modes): build the f16 activations (+ 16-sums) inside the kernel from
+   * f32 rows xf [ncols][ldxf] (RMS-normalised with `gain` when non-NULL, Q/tensor.py:35-42)
+   * instead of reading xh / xs -- replaces a qs_prep_act launch with bit-identical inputs (the
+   * same device routine); one row (ncols = 1), K <= 4096 */
   const float* xf;
   int64_t ldxf;
   const float* gain;
