@@ -121,7 +121,7 @@ typedef struct {
   const int* pos_base;/* [B] position of row_base (seq_len)         */
   const void* rope;   /* float2 [max_pos][hd/2] (cos, sin)           */
   int max_pos;
-  int dbg;            /* 0; diagnostic bits (1: consumers skip the MMA work, 2: no tile reduction) */
+  int dbg;            /* 0; diagnostic bits (1: consumers skip the MMA work; 2, INT4 only: ALU ops replace the MMAs) */
   /* optional (both weight modes): build the f16 activations (+ 16-sums) inside the kernel from
    * f32 rows xf [ncols][ldxf] (RMS-normalised with `gain` when non-NULL, Q/tensor.py:35-42)
    * instead of reading xh / xs -- replaces a qs_prep_act launch with bit-identical inputs (the
