@@ -404,7 +404,8 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS, I4Cfg<NTC, GKS, 
   const int g = lane >> 2, t4 = lane & 3;
   const int KS = P.K / 16;
   const int ks_pad = (KS + 3) / 4 * 4;
-  const int gpr = (P.K + P.wgroup - 1) / P.wgroup;
+  constexpr int WG = GKS * 16;  // weight group (the dispatch picks GKS = wgroup / 16)
+  const int gpr = (P.K + WG - 1) / WG;
   const int TP = (P.N / 16 + 1) / 2;              // tile pairs
   const bool act_in = C::ACT_BYTES > 0 && P.xf != nullptr;  // activations built here, not streamed
   const int nst = (KS + KCH - 1) / KCH;          // stages per pair (full K range)
@@ -431,11 +432,11 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS, I4Cfg<NTC, GKS, 
       const int ks0 = u * KCH, nks = min(KCH, KS - ks0);
       uint8_t* sp = sm + s * C::STAGE;
       const uint32_t wb = (uint32_t)((nks + 3) / 4) * 1024;
-      const uint32_t pb = (uint32_t)((nks * 16 + P.wgroup - 1) / P.wgroup) * 256;
+      const uint32_t pb = (uint32_t)((nks * 16 + WG - 1) / WG) * 256;
       const uint32_t bb = (uint32_t)nks * 32, xb = (uint32_t)((nks + 3) / 4) * 16;
       mbar_arrive_expect_tx(&full_b[s], wb + pb + (act_in ? 0u : ncols * (bb + xb)));
       bulk_g2s(sp, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)tp * (ks_pad / 4) + ks0 / 4) * 1024, wb, &full_b[s]);
-      bulk_g2s(sp + C::OFF_P, reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)tp * gpr + ks0 * 16 / P.wgroup) * 256,
+      bulk_g2s(sp + C::OFF_P, reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)tp * gpr + ks0 * 16 / WG) * 256,
                pb, &full_b[s]);
     };
     auto issue_act = [&](int q) {
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS, I4Cfg<NTC, GKS, 
         const uint8_t* sp = sm + s * C::STAGE;
         const int ko = kp * C::HKS;
         const uint4* wa = reinterpret_cast<const uint4*>(sp) + (ko / 4) * 64 + tile * 32 + lane;
-        const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + (ko * 16 / P.wgroup) * 16 + tile * 8 + g;
+        const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + (ko * 16 / WG) * 16 + tile * 8 + g;
         const int kabs = u * KCH + ko;  // absolute k-step (activations built in-kernel)
         const float* xsm = act_in ? act_s + kabs : reinterpret_cast<const float*>(sp + C::OFF_X) + ko;
         const uint8_t* bb = act_in ? act_h + kabs * 32 : sp + C::OFF_B + ko * 32;
