@@ -127,7 +127,7 @@ def build_workload(args, dev_index: int):
     cfg = dict(LLAMA2_7B)
     cfg["num_layers"] = args.layers
     S = args.context
-    margin = 2048
+    margin = 4096
     geo = Geometry(cfg["num_layers"], cfg["hidden"], cfg["num_heads"], cfg["num_kv_heads"], cfg["head_dim"],
                    cfg["mlp_hidden"], cfg["vocab"], S + margin)
     d, m, V = geo.hidden, geo.mlp_hidden, geo.vocab
@@ -247,54 +247,72 @@ def kernel_roofline(geo, fw, qw, hcache, fcache, peak):
     return out
 
 
-def measure_spec(fw, dw, cache, first, gamma, steps, warmup, use_graphs, clocks=None):
+def _binom_ci(acc: int, n: int) -> list:
+    """95% Wilson interval of an acceptance rate."""
+    if n == 0:
+        return [None, None]
+    z, p = 1.96, acc / n
+    den = 1 + z * z / n
+    c = (p + z * z / (2 * n)) / den
+    h = z * math.sqrt(p * (1 - p) / n + z * z / (4 * n * n)) / den
+    return [c - h, c + h]
+
+
+def measure_spec(geo, fw, dw, cache, first, gamma, steps, warmup, use_graphs, *, weight_mode, int4_bytes=0.0,
+                 long_drafted=1000):
+    """Device time (CUDA events) and wall time of the SAME ``steps`` cycles of the public decode loop
+    (SpeculativeDecoder.decode over a SpecEngine): per cycle the loop uploads the gamma_steps
+    (pinned H2D), replays the captured cycle, and reads back (v, next, drafts, status); so the
+    event-timed value and the wall-clock e2e cover identical work."""
     import torch
 
     from paper_2502_10424_b200.engine import SpecEngine
+    from paper_2502_10424_b200.model import ModelConfig
+    from paper_2502_10424_b200.specdec import SpecConfig, SpeculativeDecoder
 
+    cfg = ModelConfig(geo.num_layers, geo.num_heads, geo.head_dim, geo.hidden, geo.mlp_hidden, geo.vocab,
+                      geo.max_positions, num_kv_heads=geo.num_kv_heads)
+    dec = SpeculativeDecoder.for_device(cfg, SpecConfig(gamma=gamma, decode_len=1 << 30, weight_mode=weight_mode),
+                                        fw, dw, int4_weight_bytes=int4_bytes, use_graphs=use_graphs)
     eng = SpecEngine(fw, dw, cache, gamma, use_graphs=use_graphs)
-    eng.set_pending(first)
-    nxt = first
-
-    def one():
-        nonlocal nxt
-        gs = max(0, min(gamma, cache.fp2_space() - 1))
-        drafts, v, nxt = eng.cycle(gs)
-        cache.flush_if_full()
-        return gs, v
-
-    for _ in range(warmup):
-        one()
+    B = cache.batch
+    pending = list(first) if isinstance(first, (list, tuple)) else [first] * B
+    res = dec.decode(eng, pending, max_cycles=warmup, costs=False)
+    pending = [r.tokens[-1] for r in res]
     torch.cuda.synchronize()
     l0 = eng.launches
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    emitted = drafted = accepted = 0
+    t0 = time.perf_counter()
     s.record()
-    for _ in range(steps):
-        gs, v = one()
-        drafted += gs
-        accepted += v
-        emitted += v + 1
+    res = dec.decode(eng, pending, max_cycles=steps, costs=False)
     e.record()
     torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
     dt = s.elapsed_time(e) / 1e3
     launches = eng.launches - l0
-    # e2e: the public engine API with the step input (pending token) staged from pinned
-    # host memory and the step result (accepted count, tokens) read back every cycle
-    host_tok = torch.zeros(1, dtype=torch.int32).pin_memory()
-    host_tok[0] = nxt
-    e_emit = 0
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        eng.run.tok[0:1].copy_(host_tok, non_blocking=True)
-        gs, v = one()
-        host_tok[0] = nxt
-        e_emit += v + 1
-    torch.cuda.synchronize()
-    e2e_dt = time.perf_counter() - t0
-    return {"tok_s": emitted / dt, "ms_per_step": dt * 1e3 / steps, "acceptance": accepted / max(1, drafted),
-            "tokens_per_cycle": emitted / steps, "e2e_tok_s": e_emit / e2e_dt, "launches": launches,
-            "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4 * (2 + gamma + 1), "context_after": cache.seq_len}
+    emitted = sum(len(r.tokens) - 1 for r in res)
+    drafted = sum(r.metrics.drafted_tokens for r in res)
+    accepted = sum(r.metrics.accepted_tokens for r in res)
+    out = {"tok_s": emitted / dt, "ms_per_step": dt * 1e3 / steps, "acceptance": accepted / max(1, drafted),
+           "drafted": drafted, "tokens_per_cycle": emitted / steps / B, "e2e_tok_s": emitted / wall,
+           "launches": launches, "h2d_bytes_per_step": eng.h2d_bytes, "d2h_bytes_per_step": eng.d2h_bytes,
+           "context_after": int(cache.seq_lens().max()), "batch": B}
+    # acceptance over >= long_drafted drafted tokens (untimed continuation of the same trajectory)
+    if long_drafted:
+        pending = [r.tokens[-1] for r in res]
+        d_all, a_all, cyc = drafted, accepted, 0
+        while d_all < long_drafted and cyc < 4000:
+            r2 = dec.decode(eng, pending, max_cycles=16, costs=False)
+            pending = [r.tokens[-1] for r in r2]
+            d_all += sum(r.metrics.drafted_tokens for r in r2)
+            a_all += sum(r.metrics.accepted_tokens for r in r2)
+            cyc += 16
+        out["acceptance_long"] = {"rate": a_all / max(1, d_all), "drafted": d_all, "ci95": _binom_ci(a_all, d_all)}
+        a = a_all / max(1, d_all)
+        tpc = (1 - a ** (gamma + 1)) / (1 - a) if a < 1 else gamma + 1.0
+        # the same cycle time at the long-run acceptance (expected tokens per cycle E = (1 - a^(g+1)) / (1 - a))
+        out["tok_s_at_long_acceptance"] = B * tpc / (dt / steps)
+    return out
 
 
 def measure_ar(fw, cache, first, steps, warmup, use_graphs):
@@ -303,27 +321,23 @@ def measure_ar(fw, cache, first, steps, warmup, use_graphs):
     from paper_2502_10424_b200.engine import ARAutoEngine
 
     eng = ARAutoEngine(fw, cache, use_graphs=use_graphs)
-    eng.set_pending(first)
+    B = cache.batch
+    eng.set_pending(list(first) if isinstance(first, (list, tuple)) else [first] * B)
     for _ in range(warmup):
         eng.step(sync=False)
-        cache.flush_if_full()
     torch.cuda.synchronize()
     l0 = eng.launches
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
     s.record()
     for _ in range(steps):
-        eng.step(sync=False)
-        cache.flush_if_full()
+        eng.step(sync=True)  # the public step: one token per sequence read back every step
     e.record()
     torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
     dt = s.elapsed_time(e) / 1e3
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        eng.step(sync=True)
-        cache.flush_if_full()
-    e2e_dt = time.perf_counter() - t0
-    return {"tok_s": steps / dt, "ms_per_step": dt * 1e3 / steps, "e2e_tok_s": steps / e2e_dt,
-            "launches": eng.launches - l0}
+    return {"tok_s": B * steps / dt, "ms_per_step": dt * 1e3 / steps, "e2e_tok_s": B * steps / wall,
+            "launches": eng.launches - l0, "batch": B}
 
 
 # ---------------------------------------------------------------------------
@@ -442,9 +456,11 @@ def main():
         barrier()
         t_all = time.time()
         if "both" in modes:
-            res["both"] = measure_spec(fw, qw, hcache, first, args.gamma, args.steps, args.warmup, use_graphs)
+            res["both"] = measure_spec(geo, fw, qw, hcache, first, args.gamma, args.steps, args.warmup, use_graphs,
+                                       weight_mode="int4", int4_bytes=qw.algorithmic_bytes())
         if "kv_only" in modes:
-            res["kv_only"] = measure_spec(fw, fw, hcache, first, args.gamma, args.steps, args.warmup, use_graphs)
+            res["kv_only"] = measure_spec(geo, fw, fw, hcache, first, args.gamma, args.steps, args.warmup, use_graphs,
+                                          weight_mode="fp")
         if "fp16_ar" in modes:
             res["fp16_ar"] = measure_ar(fw, fcache, first, args.steps, args.warmup, use_graphs)
         barrier()

@@ -72,9 +72,10 @@ typedef struct {
   /* fp16 main region (sensitive-layer archive or fp16 cache) */
   const void *main_k, *main_v; /* half */
   int64_t main_seq_stride, main_head_stride; /* halves */
-  /* fp1 / fp2 recent-token buffers (half) */
+  /* fp1 / fp2 recent-token buffers (half) [seq][layer][2][kv_head][fp_rows][hd] */
   const void *fp1_k, *fp1_v, *fp2_k, *fp2_v;
   int64_t fp_seq_stride; /* halves */
+  int fp_rows;           /* rows per (buffer, head): G + slack for the ragged batch's junk rows */
   float* partials;       /* scratch */
   int* counters;         /* [B*Hkv*n_qgroups] zero-initialised */
   int dbg;               /* 0; diagnostic bits (1: skip consumer math, 2: skip producer fold) */
@@ -88,14 +89,14 @@ typedef struct {
 
 /* x @ W with fused epilogue.  Replaces the fp32 `h @ W` products of
  * decode_step (Q/model.py:379-397) and, for QS_W_INT4, the dequantised f32
- * copies of quantize_model_weights (Q/model.py:141-168). */
+ * copies of quantize_model_weights (Q/model.py:141-168).  Persistent kernels:
+ * one CTA per SM owns whole 32-row tile pairs over the full K range, so the
+ * result of one activation row never depends on how many rows share the launch. */
 typedef struct {
   int wmode;          /* QS_W_F16 | QS_W_INT4                       */
   int epi;            /* QS_EPI_*                                    */
   int N, K;           /* output rows (d_out), reduction (d_in)       */
-  int ncols;          /* activation rows (B*T), 1..16                */
-  int nctas;          /* stream-K grid (fixed per layer: results do not depend on ncols) */
-  int maxc;           /* max contributing CTAs per 64-row tile (workspace slots) */
+  int ncols;          /* activation rows (B*T), 1..48                */
   int wgroup;         /* INT4 group size along d_in                  */
   const void* w;      /* frag16 halves or frag4 u32                  */
   const void* wparams;/* INT4: float4 {S_g,Z_g,S_g8,Z_g8} per (mtile,group,g) */
@@ -109,8 +110,6 @@ typedef struct {
   int64_t ldyh;
   float* ys;          /* SILU: [ncols][ldys] 16-sums of yh           */
   int64_t ldys;
-  float* work;        /* [N/64][maxc][16][64] partial tiles           */
-  int* counters;      /* [N/64] zero-initialised                     */
   /* QKV epilogue */
   int Nq, Nk, hd, T;  /* q rows, k rows (= v rows), head dim, rows per sequence */
   float* q_out;       /* [ncols][Nq]                                 */
@@ -118,9 +117,11 @@ typedef struct {
   int64_t kv_seq_stride, kv_head_stride; /* halves */
   const int* row_base;/* [B] first free row (fp2_len or fp16-cache len) */
   int row_offset;
+  int row_cap;        /* rows per head of k_dst / v_dst: a row >= row_cap is not written (flag 4) */
   const int* pos_base;/* [B] position of row_base (seq_len)         */
   const void* rope;   /* float2 [max_pos][hd/2] (cos, sin)           */
-  int max_pos;
+  int max_pos;        /* a position >= max_pos sets flag 8 (ConfigError) and is not rotated */
+  int* flags;         /* optional device status word (bit 4 overflow, bit 8 position) */
   int dbg;            /* 0; diagnostic bits (1: consumers skip the MMA work; 2, INT4 only: ALU ops replace the MMAs) */
   /* optional (both weight modes): build the f16 activations (+ 16-sums) inside the kernel from
    * f32 rows xf [ncols][ldxf] (RMS-normalised with `gain` when non-NULL, Q/tensor.py:35-42)
@@ -135,9 +136,10 @@ typedef struct {
 /* KV store descriptor (device pointers + geometry), Q/cache.py:42-133 */
 typedef struct {
   int B, L, Hkv, hd, G, max_blocks;
+  int fp_rows;                /* rows per (buffer, head) of fp_k / fp_v (>= G) */
   uint8_t *ku, *kl, *vu, *vl; /* [B][L][Hkv][max_blocks][G*hd/2]          */
   void *kp, *vp;              /* float2 [B][L][Hkv][max_blocks][hd or G]   */
-  void *fp_k, *fp_v;          /* half [B][L][2][Hkv][G][hd]                */
+  void *fp_k, *fp_v;          /* half [B][L][2][Hkv][fp_rows][hd]          */
   void *arch_k, *arch_v;      /* half [B][n_sens][Hkv][max_blocks*G][hd]   */
   uint64_t sens_mask[2];      /* bit l set: layer l is sensitive (archives fp16) */
 } qs_kv_store;
@@ -170,9 +172,13 @@ qs_status qs_pack_weights_f16(const float* w, int d_in, int d_out, void* frag16,
  * from head-major fp16 rows src[Hkv][src_rows][hd]; writes blocks dst_block.. */
 qs_status qs_kv_quantize_blocks(const qs_kv_store* st, int seq, int layer, const void* src_k, const void* src_v,
                                 int64_t src_head_stride, int nblk, int dst_block, int* flags, void* stream);
-/* flush_if_full Q/cache.py:249-281, full-fp1 branch: quantise fp1 of every layer
- * into block dst_block, then fp1 <- fp2 */
-qs_status qs_kv_flush(const qs_kv_store* st, int seq, int dst_block, int* flags, void* stream);
+/* flush_if_full Q/cache.py:249-281, full-fp1 branch, for every sequence of the batch whose
+ * device lengths say so (fp2_len[s] == G and fp1_len[s] == G): quantise fp1 of every layer into
+ * block n_blocks[s], fp1 <- fp2, n_blocks[s] += 1, fp2_len[s] -= G.  Decided on the device, so a
+ * captured decode cycle flushes without a host round trip; the host mirrors the same rule from the
+ * per-cycle readback.  flags: bit 1 non-finite K/V (DataError, Q/quant.py:60-64), bit 4 arena full. */
+qs_status qs_kv_flush(const qs_kv_store* st, int* n_blocks, const int* fp1_len, int* fp2_len, int* flags,
+                      void* stream);
 /* _decode_block / _quantized_region Q/cache.py:317-343: f32 view of blocks [0, nblk) */
 qs_status qs_kv_dequant_view(const qs_kv_store* st, int seq, int layer, int nblk, int target, float* out_k,
                              float* out_v, void* stream);
@@ -190,21 +196,20 @@ qs_status qs_rmsnorm(const float* x, const float* gain, float* out, int n, int d
  * xs = f32 sums of every 16 consecutive f16 values (INT4 zero-point term) */
 qs_status qs_prep_act(const float* x, const float* gain, float eps, void* xh, int64_t ldxh, float* xs,
                       int64_t ldxs, int n, int d, void* stream);
-/* workspace slots (per 64-row tile) a stream-K grid of nctas CTAs needs for one linear layer */
-qs_status qs_linear_plan(int wmode, int N, int K, int nctas, int* maxc);
-/* resident linear-kernel CTAs per SM (the host fixes nctas = SMs * this, independent of ncols) */
-int qs_linear_occupancy(int wmode, int wgroup, int ncols);
-/* embedding lookup (Q/model.py:375) for n tokens */
-qs_status qs_embed(const float* table, const int* tokens, float* out, int n, int d, int vocab, int* flags,
-                   void* stream);
+/* embedding lookup (Q/model.py:375) for n = B*T rows; row c takes
+ * tokens[(c / T) * tok_stride + c % T]; an id outside [0, vocab) sets flags bit 2 (DataError) */
+qs_status qs_embed(const float* table, const int* tokens, int tok_stride, int T, float* out, int n, int d,
+                   int vocab, int* flags, void* stream);
 /* greedy selection np.argmax (first max), Q/specdec.py:209-212 */
 qs_status qs_argmax(const float* logits, int n, int vocab, int* out_idx, int out_stride, void* stream);
-/* greedy verification Q/specdec.py:276-299: drafts[0..gamma-1] (the verify
- * forward's tokens 1..gamma), tgt[0..gamma] = target argmax per row.  Writes
- * res = {v, next_token}, *next_token = next (the next cycle's pending token),
- * and adds v+1 (rows kept after rollback(gamma - v)) to *bump0 / *bump1. */
-qs_status qs_greedy_accept(const int* drafts, const int* target, int gamma, int* res, int* next_token,
-                           int* bump0, int* bump1, void* stream);
+/* greedy verification Q/specdec.py:276-299 for a ragged batch of B sequences.  Sequence b's
+ * verify tokens are tok[b*tok_stride + 0..T-1] = (pending, d_0..d_{T-2}); tgt[b*T + i] is the
+ * target argmax of its row i; gamma_step[b] <= T-1 of its drafts count (NULL: all T-1).
+ * Per sequence: v = accepted prefix, next = tgt[v] (corrected or bonus); writes res[2b] = v,
+ * res[2b+1] = next, tok[b*tok_stride] = next (the next cycle's pending token) and adds v+1
+ * (the rows kept after rollback(gamma_step - v)) to fp2_len[b] and pos[b] (either may be NULL). */
+qs_status qs_greedy_accept(int* tok, int tok_stride, const int* target, int T, const int* gamma_step, int B,
+                           int* res, int* fp2_len, int* pos, void* stream);
 /* device-side length bump (append bookkeeping of Q/cache.py:234) */
 qs_status qs_add_int(int* p, int n, int delta, void* stream);
 

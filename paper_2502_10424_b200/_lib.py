@@ -17,6 +17,9 @@ LIB_PATH = os.environ.get("QS_LIB") or os.path.join(_PKG, "libqsb200.so")  # QS_
 
 VIEW_DRAFT, VIEW_TARGET, VIEW_FP16 = 0, 1, 2
 EPI_STORE, EPI_ADD, EPI_QKV, EPI_SILU_MUL = 0, 1, 2, 3
+MAX_COLS = 48  # QS_MAX_COLS: activation rows (B * T) of one linear launch
+# device status word bits (d_flags / Runner.flags)
+FLAG_NONFINITE, FLAG_VOCAB, FLAG_OVERFLOW, FLAG_POSITION = 1, 2, 4, 8
 W_F16, W_INT4 = 0, 1
 
 vp = C.c_void_p
@@ -37,7 +40,7 @@ class AttnArgs(C.Structure):
         ("kp", vp), ("vp", vp),
         ("kp_seq_stride", i64), ("kp_head_stride", i64), ("vp_seq_stride", i64), ("vp_head_stride", i64),
         ("main_k", vp), ("main_v", vp), ("main_seq_stride", i64), ("main_head_stride", i64),
-        ("fp1_k", vp), ("fp1_v", vp), ("fp2_k", vp), ("fp2_v", vp), ("fp_seq_stride", i64),
+        ("fp1_k", vp), ("fp1_v", vp), ("fp2_k", vp), ("fp2_v", vp), ("fp_seq_stride", i64), ("fp_rows", i32),
         ("partials", vp), ("counters", vp), ("dbg", i32),
         ("out_h", vp), ("ld_out_h", i64), ("out_s", vp), ("ld_out_s", i64),
     ]
@@ -45,21 +48,20 @@ class AttnArgs(C.Structure):
 
 class LinearArgs(C.Structure):
     _fields_ = [
-        ("wmode", i32), ("epi", i32), ("N", i32), ("K", i32), ("ncols", i32), ("nctas", i32),
-        ("maxc", i32), ("wgroup", i32),
+        ("wmode", i32), ("epi", i32), ("N", i32), ("K", i32), ("ncols", i32), ("wgroup", i32),
         ("w", vp), ("wparams", vp), ("xh", vp), ("ldxh", i64), ("xs", vp), ("ldxs", i64),
         ("y", vp), ("ldy", i64), ("yh", vp), ("ldyh", i64), ("ys", vp), ("ldys", i64),
-        ("work", vp), ("counters", vp),
         ("Nq", i32), ("Nk", i32), ("hd", i32), ("T", i32),
         ("q_out", vp), ("k_dst", vp), ("v_dst", vp), ("kv_seq_stride", i64), ("kv_head_stride", i64),
-        ("row_base", vp), ("row_offset", i32), ("pos_base", vp), ("rope", vp), ("max_pos", i32), ("dbg", i32),
+        ("row_base", vp), ("row_offset", i32), ("row_cap", i32), ("pos_base", vp), ("rope", vp), ("max_pos", i32),
+        ("flags", vp), ("dbg", i32),
         ("xf", vp), ("ldxf", i64), ("gain", vp), ("eps", C.c_float),
     ]
 
 
 class KVStore(C.Structure):
     _fields_ = [
-        ("B", i32), ("L", i32), ("Hkv", i32), ("hd", i32), ("G", i32), ("max_blocks", i32),
+        ("B", i32), ("L", i32), ("Hkv", i32), ("hd", i32), ("G", i32), ("max_blocks", i32), ("fp_rows", i32),
         ("ku", vp), ("kl", vp), ("vu", vp), ("vl", vp), ("kp", vp), ("vp", vp),
         ("fp_k", vp), ("fp_v", vp), ("arch_k", vp), ("arch_v", vp),
         ("sens_mask", C.c_uint64 * 2),
@@ -76,19 +78,17 @@ _SIGS = {
     "qs_quantize_weights": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
     "qs_pack_weights_f16": (i32, [vp, i32, i32, vp, vp]),
     "qs_kv_quantize_blocks": (i32, [C.POINTER(KVStore), i32, i32, vp, vp, i64, i32, i32, vp, vp]),
-    "qs_kv_flush": (i32, [C.POINTER(KVStore), i32, i32, vp, vp]),
+    "qs_kv_flush": (i32, [C.POINTER(KVStore), vp, vp, vp, vp, vp]),
     "qs_kv_dequant_view": (i32, [C.POINTER(KVStore), i32, i32, i32, i32, vp, vp, vp]),
     "qs_attn_decode": (i32, [C.POINTER(AttnArgs), i32, vp]),
     "qs_attn_partials_floats": (i32, [C.POINTER(AttnArgs)]),
     "qs_attn_occupancy": (i32, [i32, i32, i32]),
     "qs_linear": (i32, [C.POINTER(LinearArgs), vp]),
-    "qs_linear_plan": (i32, [i32, i32, i32, i32, C.POINTER(i32)]),
-    "qs_linear_occupancy": (i32, [i32, i32, i32]),
     "qs_rmsnorm": (i32, [vp, vp, vp, i32, i32, f32, vp]),
     "qs_prep_act": (i32, [vp, vp, f32, vp, i64, vp, i64, i32, i32, vp]),
-    "qs_embed": (i32, [vp, vp, vp, i32, i32, i32, vp, vp]),
+    "qs_embed": (i32, [vp, vp, i32, i32, vp, i32, i32, i32, vp, vp]),
     "qs_argmax": (i32, [vp, i32, i32, vp, i32, vp]),
-    "qs_greedy_accept": (i32, [vp, vp, i32, vp, vp, vp, vp, vp]),
+    "qs_greedy_accept": (i32, [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp]),
     "qs_add_int": (i32, [vp, i32, i32, vp]),
 }
 

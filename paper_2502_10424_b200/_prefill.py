@@ -51,7 +51,7 @@ def run_prefill(geo, ids_dev, embedding, layer_iter, final_norm, lm_head, rope, 
 
     S = int(ids_dev.numel())
     if dtype is None:
-        dtype = torch.float32 if S * geo.hidden <= (1 << 22) else torch.float16
+        dtype = torch.float32 if S * geo.hidden <= (1 << 23) else torch.float16
     H, Hk, hd = geo.num_heads, geo.num_kv_heads, geo.head_dim
     x = embedding[ids_dev.long()].float()  # residual stream stays f32
     cs = rope[:S]
@@ -115,3 +115,34 @@ def prefill_device(weights, ids: np.ndarray, cache_mode: str, *, group_size=None
                          lambda l, k, v: cache.load_prefill_layer(l, k, v))
     cache.finish_prefill(S)
     return logits.cpu().numpy().astype(np.float32), cache
+
+
+def prefill_batch_device(weights, prompts, *, group_size=None, sensitive_layers=frozenset(), max_tokens=None):
+    """Prefill several independent prompts (ragged lengths) into ONE batched HierarchicalKVCache
+    (sequence b <- prompts[b]); returns (per-sequence last-row logits, cache)."""
+    torch = _torch()
+    cfg = weights.config
+    fw, _ = weights.device()
+    g = group_size if group_size is not None else 128
+    lens = [int(np.asarray(p).size) for p in prompts]
+    cap = max_tokens or (max(lens) + 2 * g + 256)
+    lay = CacheLayout(cfg.num_layers, cfg.num_heads, cfg.head_dim, g, frozenset(sensitive_layers), cfg.num_kv_heads)
+    cache = HierarchicalKVCache(lay, max_tokens=max(cap, max(lens) + 2 * g), batch=len(prompts))
+
+    def layers():
+        for lw in weights.layers:
+            d = {n: torch.from_numpy(np.ascontiguousarray(getattr(lw, n), dtype=np.float32)).cuda()
+                 for n in ("wq", "wk", "wv", "wo", "w_gate", "w_up", "w_down")}
+            d["attn_norm"] = torch.from_numpy(np.asarray(lw.attn_norm, np.float32)).cuda()
+            d["mlp_norm"] = torch.from_numpy(np.asarray(lw.mlp_norm, np.float32)).cuda()
+            yield d
+
+    head = torch.from_numpy(np.ascontiguousarray(weights.lm_head, dtype=np.float32)).cuda()
+    out = []
+    for b, p in enumerate(prompts):
+        ids = torch.from_numpy(np.asarray(p, dtype=np.int32).ravel()).cuda()
+        lg = run_prefill(fw.geo, ids, fw.embedding, layers(), fw.final_norm, head, fw.rope,
+                         lambda l, k, v, b=b: cache.load_prefill_layer(l, k, v, seq=b))
+        cache.finish_prefill(lens[b], seq=b)
+        out.append(lg.cpu().numpy().astype(np.float32))
+    return out, cache

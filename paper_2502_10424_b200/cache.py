@@ -24,14 +24,12 @@ that input).
 
 from __future__ import annotations
 
-import io
 import math
-import struct
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib, layout, quant
+from . import _lib, layout, qskv, quant
 from .errors import (
     BufferOverflowError,
     CacheIntegrityError,
@@ -46,8 +44,9 @@ FP_ELEM_BYTES = 4.0
 DRAFT_CODE_BYTES = 0.5
 TARGET_CODE_BYTES = 1.0
 
-SNAPSHOT_MAGIC = b"QSKV"
-SNAPSHOT_VERSION = 1
+# fp2 rows past G: a ragged batch pads every sequence's draft / verify rows to the longest
+# gamma_step of the cycle; the padding rows' K/V land here and are never committed
+FP_SLACK = 16
 
 
 def _torch():
@@ -133,19 +132,28 @@ def _check_device_geometry(layout: CacheLayout) -> None:
 
 
 class HierarchicalKVCache:
-    """Mutable per-session device cache; one logical owner mutates it at a time."""
+    """Mutable device cache of ``batch`` independent sequences; one logical owner mutates it at a time.
+
+    The reference protocol (append_decode_token / rollback / flush_if_full / views / snapshots)
+    acts on sequence 0; the batched decode engine (engine.SpecEngine) drives every sequence
+    through the device length arrays and keeps the per-sequence host mirror in step with
+    ``commit_cycle``.
+    """
 
     def __init__(self, layout: CacheLayout, *, max_tokens: int | None = None, batch: int = 1):
         _check_device_geometry(layout)
         torch = _torch()
+        if batch < 1:
+            raise ConfigError(f"batch must be >= 1, got {batch}")
         self.layout = layout
         self.batch = batch
         L, H, hd, G = layout.num_layers, layout.kv_heads, layout.head_dim, layout.group_size
         self.max_blocks = max(1, math.ceil((max_tokens or 8 * G) / G))
+        self.fp_rows = G + FP_SLACK
         dev = torch.device("cuda")
         self._dev = dev
         self._alloc_arena(self.max_blocks)
-        self.fp_k = torch.zeros((batch, L, 2, H, G, hd), dtype=torch.float16, device=dev)
+        self.fp_k = torch.zeros((batch, L, 2, H, self.fp_rows, hd), dtype=torch.float16, device=dev)
         self.fp_v = torch.zeros_like(self.fp_k)
         self._sens = sorted(layout.sensitive_layers)
         self._alloc_archive(self.max_blocks)
@@ -155,10 +163,10 @@ class HierarchicalKVCache:
         self.d_fp2_len = torch.zeros(batch, dtype=torch.int32, device=dev)
         self.d_pos = torch.zeros(batch, dtype=torch.int32, device=dev)
         self.d_flags = torch.zeros(1, dtype=torch.int32, device=dev)
-        # host mirror (sequence 0 for the reference protocol)
-        self._fp1_len = 0
-        self._fp2_len = np.zeros(L, dtype=np.int64)
-        self.quantized_token_count = 0
+        # host mirror: per sequence quantised tokens and fp1 rows, per (sequence, layer) fp2 rows
+        self._nq = np.zeros(batch, dtype=np.int64)
+        self._fp1 = np.zeros(batch, dtype=np.int64)
+        self._fp2 = np.zeros((batch, L), dtype=np.int64)
         self.generation = 0  # bumps when arenas are reallocated (CUDA graphs re-capture)
 
     # ------------------------------------------------------------------ storage
@@ -166,8 +174,7 @@ class HierarchicalKVCache:
         torch = _torch()
         B, lay = self.batch, self.layout
         L, H, hd, G = lay.num_layers, lay.kv_heads, lay.head_dim, lay.group_size
-        pb = G * hd // 2
-        shp = (B, L, H, max_blocks, pb)
+        shp = (B, L, H, max_blocks, G * hd // 2)
         self.ku = torch.zeros(shp, dtype=torch.uint8, device=self._dev)
         self.kl = torch.zeros(shp, dtype=torch.uint8, device=self._dev)
         self.vu = torch.zeros(shp, dtype=torch.uint8, device=self._dev)
@@ -185,10 +192,10 @@ class HierarchicalKVCache:
         else:
             self.arch_k = self.arch_v = None
 
-    def _grow(self, need_blocks: int) -> None:
+    def ensure_blocks(self, need_blocks: int) -> None:
+        """Grow the quantised arenas to hold ``need_blocks`` blocks per (sequence, layer, head)."""
         if need_blocks <= self.max_blocks:
             return
-        torch = _torch()
         new = max(need_blocks, 2 * self.max_blocks)
         old = (self.ku, self.kl, self.vu, self.vl, self.kp, self.vp, self.arch_k, self.arch_v)
         nb = self.max_blocks
@@ -203,11 +210,14 @@ class HierarchicalKVCache:
         self.max_blocks = new
         self.generation += 1
 
+    _grow = ensure_blocks
+
     def store_struct(self) -> _lib.KVStore:
         lay = self.layout
         s = _lib.KVStore()
         s.B, s.L, s.Hkv, s.hd, s.G, s.max_blocks = (self.batch, lay.num_layers, lay.kv_heads, lay.head_dim,
                                                    lay.group_size, self.max_blocks)
+        s.fp_rows = self.fp_rows
         s.ku, s.kl, s.vu, s.vl = (self.ku.data_ptr(), self.kl.data_ptr(), self.vu.data_ptr(), self.vl.data_ptr())
         s.kp, s.vp = self.kp.data_ptr(), self.vp.data_ptr()
         s.fp_k, s.fp_v = self.fp_k.data_ptr(), self.fp_v.data_ptr()
@@ -222,11 +232,19 @@ class HierarchicalKVCache:
         s.sens_mask[0], s.sens_mask[1] = m0, m1
         return s
 
-    def _check_flags(self, what: str) -> None:
-        f = int(self.d_flags.item())
-        if f:
-            self.d_flags.zero_()
-            raise DataError(f"{what}: non-finite K/V values")
+    def raise_device_flags(self, what: str, flags: int | None = None) -> None:
+        """Map the device status word to the reference exceptions (read it when ``flags`` is None)."""
+        f = int(self.d_flags.item()) if flags is None else int(flags)
+        if not f:
+            return
+        self.d_flags.zero_()
+        if f & _lib.FLAG_NONFINITE:
+            raise DataError(f"{what}: cannot quantize non-finite K/V values")
+        if f & _lib.FLAG_OVERFLOW:
+            raise BufferOverflowError(f"{what}: quantised arena full ({self.max_blocks} blocks)")
+        raise DataError(f"{what}: device status {f:#x}")
+
+    _check_flags = raise_device_flags
 
     # ------------------------------------------------------------ construction
     @classmethod
@@ -250,16 +268,21 @@ class HierarchicalKVCache:
         cache.finish_prefill(s_p)
         return cache
 
+    @staticmethod
+    def _fill_rule(s_p: int, g: int) -> tuple[int, int, int]:
+        """(quantised, fp1, fp2) token counts of a prompt (Q/cache.py:165-171)."""
+        n_quant = ((s_p - g) // g) * g if s_p >= g else 0
+        fp1_n = min(g, s_p - n_quant)
+        return n_quant, fp1_n, s_p - n_quant - fp1_n
+
     def load_prefill_layer(self, layer: int, k, v, seq: int = 0) -> None:
-        """Quantise / buffer one layer's prompt K/V (rows [S_P, kv_dim])."""
+        """Quantise / buffer one layer's prompt K/V (rows [S_P, kv_dim]) of sequence ``seq``."""
         torch = _torch()
         lay = self.layout
         g, H, hd = lay.group_size, lay.kv_heads, lay.head_dim
         s_p = int(k.shape[0])
-        n_quant = ((s_p - g) // g) * g if s_p >= g else 0
-        fp1_n = min(g, s_p - n_quant)
-        fp2_n = s_p - n_quant - fp1_n
-        self._grow(n_quant // g + 1)
+        n_quant, fp1_n, fp2_n = self._fill_rule(s_p, g)
+        self.ensure_blocks(n_quant // g + 1)
 
         def head_major(x):
             t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
@@ -278,47 +301,55 @@ class HierarchicalKVCache:
             self.fp_v[seq, layer, 1, :, :fp2_n] = hv[:, n_quant + fp1_n :]
 
     def finish_prefill(self, s_p: int, seq: int = 0) -> None:
-        g = self.layout.group_size
-        n_quant = ((s_p - g) // g) * g if s_p >= g else 0
-        fp1_n = min(g, s_p - n_quant)
-        fp2_n = s_p - n_quant - fp1_n
-        self._check_flags("prefill")
-        if seq == 0:
-            self._fp1_len = fp1_n
-            self._fp2_len[:] = fp2_n
-            self.quantized_token_count = n_quant
-        self.d_n_blocks[seq] = n_quant // g
+        n_quant, fp1_n, fp2_n = self._fill_rule(s_p, self.layout.group_size)
+        self.raise_device_flags("prefill")
+        self._nq[seq], self._fp1[seq] = n_quant, fp1_n
+        self._fp2[seq, :] = fp2_n
+        self.d_n_blocks[seq] = n_quant // self.layout.group_size
         self.d_fp1_len[seq] = fp1_n
         self.d_fp2_len[seq] = fp2_n
         self.d_pos[seq] = s_p
 
     # ----------------------------------------------------------------- counters
     @property
+    def quantized_token_count(self) -> int:
+        return int(self._nq[0])
+
+    @property
     def fp1_len(self) -> int:
-        return self._fp1_len
+        return int(self._fp1[0])
 
     @property
     def fp2_len(self) -> int:
-        return int(self._fp2_len[0])
+        return int(self._fp2[0, 0])
 
     @property
     def fp_token_count(self) -> int:
-        return self._fp1_len + self.fp2_len
+        return self.fp1_len + self.fp2_len
 
     @property
     def seq_len(self) -> int:
         return self.quantized_token_count + self.fp_token_count
 
-    def fp2_space(self) -> int:
-        return self.layout.group_size - self.fp2_len
+    def seq_lens(self) -> np.ndarray:
+        """Tokens held per sequence."""
+        return self._nq + self._fp1 + self._fp2[:, 0]
+
+    def fp2_space(self, seq: int = 0) -> int:
+        return self.layout.group_size - int(self._fp2[seq, 0])
 
     def check_layer_consistency(self) -> None:
-        if not np.all(self._fp2_len == self._fp2_len[0]):
-            raise CacheIntegrityError(f"per-layer append counts diverged: {self._fp2_len.tolist()}")
+        if not np.all(self._fp2 == self._fp2[:, :1]):
+            raise CacheIntegrityError(f"per-layer append counts diverged: {self._fp2.tolist()}")
+
+    def _single(self, what: str) -> None:
+        if self.batch != 1:
+            raise ConfigError(f"{what} is the single-sequence protocol; a batch of {self.batch} runs through SpecEngine")
 
     # ----------------------------------------------------------------- mutation
     def append_decode_token(self, layer: int, k, v) -> None:
         """Store one token's K/V row in fp2 for ``layer`` (Q/cache.py:216-234)."""
+        self._single("append_decode_token")
         torch = _torch()
         lay = self.layout
         kv = lay.kv_dim
@@ -326,26 +357,27 @@ class HierarchicalKVCache:
         vt = v if isinstance(v, torch.Tensor) else torch.from_numpy(np.asarray(v, dtype=np.float32).ravel())
         if kt.numel() != kv or vt.numel() != kv:
             raise DimensionError(f"expected kv rows of width {kv}, got {kt.numel()}/{vt.numel()}")
-        pos = int(self._fp2_len[layer])
+        pos = int(self._fp2[0, layer])
         if pos >= lay.group_size:
             raise BufferOverflowError(f"fp2 is full (layer {layer}); the engine must flush before appending")
         self.fp_k[0, layer, 1, :, pos] = kt.to(self._dev, torch.float16).reshape(lay.kv_heads, lay.head_dim)
         self.fp_v[0, layer, 1, :, pos] = vt.to(self._dev, torch.float16).reshape(lay.kv_heads, lay.head_dim)
-        self._fp2_len[layer] = pos + 1
-        if np.all(self._fp2_len == self._fp2_len[0]):
-            self.d_fp2_len[0] = int(self._fp2_len[0])
+        self._fp2[0, layer] = pos + 1
+        if np.all(self._fp2[0] == self._fp2[0, 0]):
+            self.d_fp2_len[0] = int(self._fp2[0, 0])
             self.d_pos[0] = self.seq_len
 
     def _advance(self, n: int) -> None:
-        """Account for n rows the device forward appended to every layer."""
+        """Account for n rows the device forward appended to every layer (single sequence)."""
         if self.fp2_len + n > self.layout.group_size:
             raise BufferOverflowError("fp2 overflow")
-        self._fp2_len += n
+        self._fp2 += n
         _lib.call("qs_add_int", self.d_fp2_len.data_ptr(), self.batch, n, _lib.stream_ptr())
         _lib.call("qs_add_int", self.d_pos.data_ptr(), self.batch, n, _lib.stream_ptr())
 
     def rollback(self, n_reject: int) -> None:
         """Drop the last ``n_reject`` fp2 tokens in every layer (Q/cache.py:236-247)."""
+        self._single("rollback")
         if n_reject < 0:
             raise ConfigError(f"rollback count must be nonnegative, got {n_reject}")
         if n_reject == 0:
@@ -353,43 +385,62 @@ class HierarchicalKVCache:
         self.check_layer_consistency()
         if n_reject > self.fp2_len:
             raise CacheIntegrityError(f"cannot roll back {n_reject} tokens; fp2 holds only {self.fp2_len}")
-        self._fp2_len -= n_reject
+        self._fp2 -= n_reject
         _lib.call("qs_add_int", self.d_fp2_len.data_ptr(), self.batch, -n_reject, _lib.stream_ptr())
         _lib.call("qs_add_int", self.d_pos.data_ptr(), self.batch, -n_reject, _lib.stream_ptr())
 
-    def flush_if_full(self) -> bool:
-        """Quantise fp1 and rotate fp2 into it once fp2 is full (Q/cache.py:249-281)."""
-        self.check_layer_consistency()
+    # -- flush (Q/cache.py:249-281) ------------------------------------------------
+    def flush_due(self) -> np.ndarray:
+        """Per sequence: 0 = no flush, 1 = quantise fp1 (device kernel), 2 = short-fp1 top-up."""
         g = self.layout.group_size
-        if self.fp2_len != g:
-            return False
-        if self._fp1_len == g:
-            nb = self.quantized_token_count // g
-            self._grow(nb + 1)
-            st = self.store_struct()
-            _lib.call("qs_kv_flush", st, 0, nb, self.d_flags.data_ptr(), _lib.stream_ptr())
-            _lib.call("qs_add_int", self.d_n_blocks.data_ptr(), self.batch, 1, _lib.stream_ptr())
-            _lib.call("qs_add_int", self.d_fp2_len.data_ptr(), self.batch, -g, _lib.stream_ptr())
-            self.quantized_token_count += g
-            self._fp1_len = g
-            self._fp2_len[:] = 0
-            return True
-        short = self._fp1_len
-        take = g - short
-        self.fp_k[:, :, 0, :, short:] = self.fp_k[:, :, 1, :, :take]
-        self.fp_v[:, :, 0, :, short:] = self.fp_v[:, :, 1, :, :take]
-        keep_k = self.fp_k[:, :, 1, :, take:].clone()
-        keep_v = self.fp_v[:, :, 1, :, take:].clone()
-        self.fp_k[:, :, 1, :, :short] = keep_k
-        self.fp_v[:, :, 1, :, :short] = keep_v
-        self._fp2_len[:] = short
-        self._fp1_len = g
-        self.d_fp1_len.fill_(g)
-        self.d_fp2_len.fill_(short)
-        return True
+        full = self._fp2[:, 0] == g
+        return np.where(full, np.where(self._fp1 == g, 1, 2), 0)
 
-    def _quantize_block_for_test(self, layer: int, k_block, v_block) -> None:  # pragma: no cover - debug aid
-        raise NotImplementedError
+    def launch_device_flush(self, stream=None) -> None:
+        """Enqueue the device-conditioned flush of every sequence whose lengths say so (K1 + rotate);
+        stream ordered, no host sync -- the engine captures it into the decode cycle graph."""
+        _lib.call("qs_kv_flush", self.store_struct(), self.d_n_blocks.data_ptr(), self.d_fp1_len.data_ptr(),
+                  self.d_fp2_len.data_ptr(), self.d_flags.data_ptr(), _lib.stream_ptr(stream))
+
+    def commit_flush(self, due: np.ndarray) -> None:
+        """Host-mirror side of a flush: the full-fp1 sequences were flushed on the device; the
+        short-fp1 ones are topped up here (rare: only after a prompt shorter than 2G)."""
+        g = self.layout.group_size
+        for b in np.nonzero(due == 1)[0]:
+            self._nq[b] += g
+            self._fp2[b, :] = 0
+        for b in np.nonzero(due == 2)[0]:
+            self._short_topup(int(b))
+
+    def _short_topup(self, b: int) -> None:
+        g = self.layout.group_size
+        short = int(self._fp1[b])
+        take = g - short
+        self.fp_k[b, :, 0, :, short:g] = self.fp_k[b, :, 1, :, :take]
+        self.fp_v[b, :, 0, :, short:g] = self.fp_v[b, :, 1, :, :take]
+        keep_k = self.fp_k[b, :, 1, :, take:g].clone()
+        keep_v = self.fp_v[b, :, 1, :, take:g].clone()
+        self.fp_k[b, :, 1, :, :short] = keep_k
+        self.fp_v[b, :, 1, :, :short] = keep_v
+        self._fp2[b, :] = short
+        self._fp1[b] = g
+        self.d_fp1_len[b] = g
+        self.d_fp2_len[b] = short
+
+    def flush_if_full(self) -> bool:
+        """Quantise fp1 and rotate fp2 into it once fp2 is full (Q/cache.py:249-281); sequence 0's
+        answer is returned (every due sequence of a batch is flushed).  Non-finite K/V raise
+        DataError here, as the reference's quantiser does (Q/quant.py:60-64)."""
+        self.check_layer_consistency()
+        due = self.flush_due()
+        if not due.any():
+            return False
+        if (due == 1).any():
+            self.ensure_blocks(int(self._nq.max()) // self.layout.group_size + 1)
+            self.launch_device_flush()
+            self.raise_device_flags("flush_if_full")
+        self.commit_flush(due)
+        return bool(due[0])
 
     # ------------------------------------------------------------------- views
     def draft_view(self, layer: int) -> CacheView:
@@ -404,36 +455,41 @@ class HierarchicalKVCache:
         v = self.fp_v[seq, layer, which, :, :n].permute(1, 0, 2).reshape(n, lay.kv_dim)
         return k.float().cpu().numpy(), v.float().cpu().numpy()
 
+    def _arch_rows(self, layer: int, r0: int, r1: int, seq: int = 0) -> tuple[np.ndarray, np.ndarray]:
+        lay = self.layout
+        slot = self._sens.index(layer)
+        n = r1 - r0
+        k = self.arch_k[seq, slot, :, r0:r1].permute(1, 0, 2).reshape(n, lay.kv_dim)
+        v = self.arch_v[seq, slot, :, r0:r1].permute(1, 0, 2).reshape(n, lay.kv_dim)
+        return k.float().cpu().numpy(), v.float().cpu().numpy()
+
     def quantized_region(self, layer: int, kind: str, seq: int = 0):
         """f32 dequantised quantised history [n_q, kv_dim] (device kernel, f64 math)."""
         torch = _torch()
         lay = self.layout
-        nb = self.quantized_token_count // lay.group_size
+        nb = int(self._nq[seq]) // lay.group_size
         if nb == 0:
             return None
         ok = torch.empty((nb * lay.group_size, lay.kv_dim), dtype=torch.float32, device=self._dev)
         ov = torch.empty_like(ok)
-        st = self.store_struct()
-        _lib.call("qs_kv_dequant_view", st, seq, layer, nb, 1 if kind == "target" else 0, ok.data_ptr(), ov.data_ptr(),
-                  _lib.stream_ptr())
+        _lib.call("qs_kv_dequant_view", self.store_struct(), seq, layer, nb, 1 if kind == "target" else 0,
+                  ok.data_ptr(), ov.data_ptr(), _lib.stream_ptr())
         return ok.cpu().numpy(), ov.cpu().numpy()
 
-    def _view(self, layer: int, kind: str) -> CacheView:
+    def _view(self, layer: int, kind: str, seq: int = 0) -> CacheView:
         lay = self.layout
         if not 0 <= layer < lay.num_layers:
             raise ConfigError(f"layer index {layer} out of range")
         view = CacheView(segments=[])
         code_bytes = DRAFT_CODE_BYTES if kind == "draft" else TARGET_CODE_BYTES
-        nq = self.quantized_token_count
+        nq = int(self._nq[seq])
         if layer in lay.sensitive_layers:
             if nq:
-                slot = self._sens.index(layer)
-                k = self.arch_k[0, slot, :, :nq].permute(1, 0, 2).reshape(nq, lay.kv_dim).float().cpu().numpy()
-                v = self.arch_v[0, slot, :, :nq].permute(1, 0, 2).reshape(nq, lay.kv_dim).float().cpu().numpy()
+                k, v = self._arch_rows(layer, 0, nq, seq)
                 view.segments.append((k, v))
                 view.fp_bytes += FP_ELEM_BYTES * (k.size + v.size)
         elif nq:
-            k, v = self.quantized_region(layer, kind)
+            k, v = self.quantized_region(layer, kind, seq)
             view.segments.append((k, v))
             elems = k.size + v.size
             view.quantized_elements += elems
@@ -442,9 +498,9 @@ class HierarchicalKVCache:
             if kind == "target":
                 groups *= 2
             view.param_bytes += quant.PARAM_PAIR_BYTES * groups
-        for which, n in ((0, self._fp1_len), (1, int(self._fp2_len[layer]))):
+        for which, n in ((0, int(self._fp1[seq])), (1, int(self._fp2[seq, layer]))):
             if n:
-                view.segments.append(self._fp_rows(which, layer, n))
+                view.segments.append(self._fp_rows(which, layer, n, seq))
                 view.fp_bytes += FP_ELEM_BYTES * 2 * n * lay.kv_dim
         return view
 
@@ -455,7 +511,7 @@ class HierarchicalKVCache:
 
     # ------------------------------------------------------- accounting / export
     def memory_report(self) -> MemoryReport:
-        """Exact modeled byte totals (Q/cache.py:384-403)."""
+        """Exact modeled byte totals (Q/cache.py:384-403) of sequence 0."""
         lay = self.layout
         nb = self.quantized_token_count // lay.group_size
         nq_layers = lay.num_layers - len(self._sens)
@@ -479,29 +535,28 @@ class HierarchicalKVCache:
         G, hd, H, kv = lay.group_size, lay.head_dim, lay.kv_heads, lay.kv_dim
         kw, kn, vw, vn = layout.block_maps(G, hd)
 
-        def words(t):
-            return t[seq, layer, :, block].contiguous().cpu().numpy().view(np.uint32)  # [H][nwords]
+        def codes(t, word_idx, nib):  # [G][kv] nibble values of every head
+            words = t[seq, layer, :, block].contiguous().cpu().numpy().view(np.uint32)
+            return np.concatenate([layout.unpack_block(words[h], word_idx, nib) for h in range(H)], axis=1)
 
-        wku, wkl, wvu, wvl = words(self.ku), words(self.kl), words(self.vu), words(self.vl)
-        kp = self.kp[seq, layer, :, block].cpu().numpy()  # [H][hd][2]
-        vpp = self.vp[seq, layer, :, block].cpu().numpy()  # [H][G][2]
-        cku = np.concatenate([layout.unpack_block(wku[h], kw, kn) for h in range(H)], axis=1)  # [G][kv]
-        ckl = np.concatenate([layout.unpack_block(wkl[h], kw, kn) for h in range(H)], axis=1) - 8
-        cvu = np.concatenate([layout.unpack_block(wvu[h], vw, vn) for h in range(H)], axis=1)
-        cvl = np.concatenate([layout.unpack_block(wvl[h], vw, vn) for h in range(H)], axis=1) - 8
-        ks = kp[:, :, 0].reshape(kv).astype(np.float32)
-        kz = kp[:, :, 1].reshape(kv).astype(np.float32)
+        cku, ckl = codes(self.ku, kw, kn), codes(self.kl, kw, kn) - 8
+        cvu, cvl = codes(self.vu, vw, vn), codes(self.vl, vw, vn) - 8
+        kp = self.kp[seq, layer, :, block].cpu().numpy().reshape(kv, 2)          # channel-major (S, Z)
+        vpp = self.vp[seq, layer, :, block].cpu().numpy()                         # [H][G][2]
         ngv = -(-kv // G)
-        first_head = [(j * G) // hd for j in range(ngv)]
-        vs = np.stack([vpp[h, :, 0] for h in first_head], axis=1).reshape(-1).astype(np.float32)  # [G*ngv]
-        vz = np.stack([vpp[h, :, 1] for h in first_head], axis=1).reshape(-1).astype(np.float32)
+        heads = [(j * G) // hd for j in range(ngv)]                               # first head of value group j
+        vsz = np.stack([vpp[h] for h in heads], axis=1).reshape(G * ngv, 2)       # token-major groups
         count = G * kv
-        mk = lambda codes, s, z, mode, axis, rl: quant.QuantPlane(quant.pack_nibbles(codes), count, G, s, z, mode, axis, rl)
-        ku = mk(cku.T.reshape(-1), ks, kz, quant.MODE_ASYM_U4, quant.AXIS_CHANNEL, None)
-        kl = mk(ckl.T.reshape(-1), (ks / np.float32(16)).astype(np.float32), np.zeros_like(ks), quant.MODE_SYM_S4, quant.AXIS_CHANNEL, None)
-        vu = mk(cvu.reshape(-1), vs, vz, quant.MODE_ASYM_U4, quant.AXIS_TOKEN, kv)
-        vl = mk(cvl.reshape(-1), (vs / np.float32(16)).astype(np.float32), np.zeros_like(vs), quant.MODE_SYM_S4, quant.AXIS_TOKEN, kv)
-        return ku, kl, vu, vl
+
+        def plane(c, s, z, mode, axis, rl):
+            return quant.QuantPlane(quant.pack_nibbles(c), count, G, np.ascontiguousarray(s, np.float32),
+                                    np.ascontiguousarray(z, np.float32), mode, axis, rl)
+
+        sixteenth = np.float32(1.0 / 16.0)
+        return (plane(cku.T.reshape(-1), kp[:, 0], kp[:, 1], quant.MODE_ASYM_U4, quant.AXIS_CHANNEL, None),
+                plane(ckl.T.reshape(-1), kp[:, 0] * sixteenth, np.zeros(kv), quant.MODE_SYM_S4, quant.AXIS_CHANNEL, None),
+                plane(cvu.reshape(-1), vsz[:, 0], vsz[:, 1], quant.MODE_ASYM_U4, quant.AXIS_TOKEN, kv),
+                plane(cvl.reshape(-1), vsz[:, 0] * sixteenth, np.zeros(G * ngv), quant.MODE_SYM_S4, quant.AXIS_TOKEN, kv))
 
     def import_block_planes(self, layer: int, block: int, planes, seq: int = 0) -> None:
         """Inverse of export_block_planes (snapshot load)."""
@@ -511,151 +566,82 @@ class HierarchicalKVCache:
         kw, kn, vw, vn = layout.block_maps(G, hd)
         ku, kl, vu, vl = planes
         nwords = G * hd // 8
-        cku = ku.unpacked().astype(np.int64).reshape(kv, G).T
-        ckl = kl.unpacked().astype(np.int64).reshape(kv, G).T + 8
-        cvu = vu.unpacked().astype(np.int64).reshape(G, kv)
-        cvl = vl.unpacked().astype(np.int64).reshape(G, kv) + 8
-        for h in range(H):
-            sl = slice(h * hd, (h + 1) * hd)
-            for dst, codes, wi, ni in ((self.ku, cku, kw, kn), (self.kl, ckl, kw, kn), (self.vu, cvu, vw, vn), (self.vl, cvl, vw, vn)):
-                w = layout.pack_block(codes[:, sl], wi, ni, nwords)
-                dst[seq, layer, h, block] = torch.from_numpy(w.view(np.uint8)).to(self._dev)
-        kp = np.stack([ku.scales, ku.zeros], axis=-1).reshape(H, hd, 2)
-        self.kp[seq, layer, :, block] = torch.from_numpy(np.ascontiguousarray(kp, dtype=np.float32)).to(self._dev)
+        per_plane = ((self.ku, ku.unpacked().astype(np.int64).reshape(kv, G).T, kw, kn),
+                     (self.kl, kl.unpacked().astype(np.int64).reshape(kv, G).T + 8, kw, kn),
+                     (self.vu, vu.unpacked().astype(np.int64).reshape(G, kv), vw, vn),
+                     (self.vl, vl.unpacked().astype(np.int64).reshape(G, kv) + 8, vw, vn))
+        for dst, c, wi, ni in per_plane:
+            words = np.stack([layout.pack_block(c[:, h * hd:(h + 1) * hd], wi, ni, nwords) for h in range(H)])
+            dst[seq, layer, :, block] = torch.from_numpy(words.view(np.uint8).reshape(H, -1)).to(self._dev)
+        kpar = np.stack([ku.scales, ku.zeros], axis=-1).reshape(H, hd, 2)
+        self.kp[seq, layer, :, block] = torch.from_numpy(np.ascontiguousarray(kpar, np.float32)).to(self._dev)
         ngv = -(-kv // G)
-        s = vu.scales.reshape(G, ngv)
-        z = vu.zeros.reshape(G, ngv)
-        for h in range(H):
-            j = (h * hd) // G
-            self.vp[seq, layer, h, block] = torch.from_numpy(np.stack([s[:, j], z[:, j]], axis=-1).astype(np.float32)).to(self._dev)
+        vs, vz = vu.scales.reshape(G, ngv), vu.zeros.reshape(G, ngv)
+        vpar = np.stack([np.stack([vs[:, (h * hd) // G], vz[:, (h * hd) // G]], axis=-1) for h in range(H)])
+        self.vp[seq, layer, :, block] = torch.from_numpy(np.ascontiguousarray(vpar, np.float32)).to(self._dev)
 
     # --------------------------------------------------------------- snapshots
-    def save_snapshot(self, path) -> None:
-        with open(path, "wb") as f:
-            self._write_snapshot(f)
-
-    def _write_snapshot(self, f) -> None:
-        """QSKV format of Q/cache.py:405-447 (fp rows written as f32)."""
+    def to_snapshot(self) -> qskv.Snapshot:
+        """Sequence 0 as a QSKV snapshot value (fp rows as their exact fp16 values in f32)."""
         self.check_layer_consistency()
         lay = self.layout
-        f.write(SNAPSHOT_MAGIC)
-        f.write(struct.pack("<B", SNAPSHOT_VERSION))
-        sens = sorted(lay.sensitive_layers)
-        f.write(struct.pack("<IIIII", lay.num_layers, lay.num_heads, lay.head_dim, lay.group_size, len(sens)))
-        for s in sens:
-            f.write(struct.pack("<I", s))
-        f.write(struct.pack("<QII", self.quantized_token_count, self._fp1_len, self.fp2_len))
-        nb = self.quantized_token_count // lay.group_size
+        G, nb = lay.group_size, self.quantized_token_count // lay.group_size
+        layers = []
         for layer in range(lay.num_layers):
+            lc = qskv.LayerContent()
             if layer in lay.sensitive_layers:
-                f.write(struct.pack("<I", nb))
-                slot = self._sens.index(layer)
-                for b in range(nb):
-                    rows = slice(b * lay.group_size, (b + 1) * lay.group_size)
-                    ak = self.arch_k[0, slot, :, rows].permute(1, 0, 2).reshape(lay.group_size, lay.kv_dim)
-                    av = self.arch_v[0, slot, :, rows].permute(1, 0, 2).reshape(lay.group_size, lay.kv_dim)
-                    f.write(struct.pack("<I", lay.group_size))
-                    f.write(ak.float().cpu().numpy().astype("<f4").tobytes())
-                    f.write(av.float().cpu().numpy().astype("<f4").tobytes())
+                lc.archived = [self._arch_rows(layer, b * G, (b + 1) * G) for b in range(nb)]
             else:
-                f.write(struct.pack("<I", nb))
-                for b in range(nb):
-                    for plane in self.export_block_planes(layer, b):
-                        _write_plane(f, plane)
-            k1, v1 = self._fp_rows(0, layer, self._fp1_len) if self._fp1_len else (np.zeros((0, lay.kv_dim), np.float32),) * 2
-            k2, v2 = self._fp_rows(1, layer, self.fp2_len) if self.fp2_len else (np.zeros((0, lay.kv_dim), np.float32),) * 2
-            for arr in (k1, v1, k2, v2):
-                f.write(np.asarray(arr, dtype="<f4").tobytes())
+                lc.blocks = [self.export_block_planes(layer, b) for b in range(nb)]
+            lc.fp1 = self._fp_rows(0, layer, self.fp1_len)
+            lc.fp2 = self._fp_rows(1, layer, self.fp2_len)
+            layers.append(lc)
+        return qskv.Snapshot(lay.num_layers, lay.kv_heads, lay.head_dim, G, tuple(sorted(lay.sensitive_layers)),
+                             self.quantized_token_count, self.fp1_len, self.fp2_len, layers)
+
+    @classmethod
+    def from_snapshot(cls, snap: qskv.Snapshot) -> "HierarchicalKVCache":
+        torch = _torch()
+        lay = CacheLayout(snap.num_layers, snap.num_heads, snap.head_dim, snap.group_size, frozenset(snap.sensitive))
+        G, H, hd = snap.group_size, snap.num_heads, snap.head_dim
+        cache = cls(lay, max_tokens=snap.quantized + 2 * G)
+
+        def put(dst, rows):  # f32 [n, kv] -> fp16 head-major rows
+            n = rows.shape[0]
+            if n:
+                dst[:, :n] = torch.from_numpy(rows).reshape(n, H, hd).permute(1, 0, 2).to(cache._dev, torch.float16)
+
+        for layer, lc in enumerate(snap.layers):
+            if layer in lay.sensitive_layers:
+                slot = cache._sens.index(layer)
+                r0 = 0
+                for k, v in lc.archived:
+                    put(cache.arch_k[0, slot, :, r0:], k)
+                    put(cache.arch_v[0, slot, :, r0:], v)
+                    r0 += k.shape[0]
+            else:
+                for b, quartet in enumerate(lc.blocks):
+                    cache.import_block_planes(layer, b, quartet)
+            for which, (k, v) in ((0, lc.fp1), (1, lc.fp2)):
+                put(cache.fp_k[0, layer, which], k)
+                put(cache.fp_v[0, layer, which], v)
+        cache._nq[0], cache._fp1[0] = snap.quantized, snap.fp1_len
+        cache._fp2[0, :] = snap.fp2_len
+        cache.d_n_blocks.fill_(snap.quantized // G)
+        cache.d_fp1_len.fill_(snap.fp1_len)
+        cache.d_fp2_len.fill_(snap.fp2_len)
+        cache.d_pos.fill_(snap.quantized + snap.fp1_len + snap.fp2_len)
+        return cache
+
+    def save_snapshot(self, path) -> None:
+        """QSKV file of Q/cache.py:405-447 (readable by the reference)."""
+        with open(path, "wb") as f:
+            f.write(qskv.encode(self.to_snapshot()))
 
     @classmethod
     def load_snapshot(cls, path) -> "HierarchicalKVCache":
         with open(path, "rb") as f:
-            data = f.read()
-        return cls._read_snapshot(io.BytesIO(data))
-
-    @classmethod
-    def _read_snapshot(cls, f) -> "HierarchicalKVCache":
-        torch = _torch()
-        if f.read(4) != SNAPSHOT_MAGIC:
-            raise FormatError("bad snapshot magic")
-        (version,) = _unpack(f, "<B")
-        if version != SNAPSHOT_VERSION:
-            raise FormatError(f"unsupported snapshot version {version}")
-        L, H, hd, G, n_sens = _unpack(f, "<IIIII")
-        sens = frozenset(_unpack(f, "<I")[0] for _ in range(n_sens))
-        lay = CacheLayout(L, H, hd, G, sens)
-        quantized, fp1_len, fp2_len = _unpack(f, "<QII")
-        cache = cls(lay, max_tokens=quantized + 2 * G)
-        kv = lay.kv_dim
-        for layer in range(L):
-            (nblk,) = _unpack(f, "<I")
-            if layer in sens:
-                slot = cache._sens.index(layer)
-                for b in range(nblk):
-                    (rows,) = _unpack(f, "<I")
-                    ak = _read_f32(f, (rows, kv))
-                    av = _read_f32(f, (rows, kv))
-                    r0 = b * G
-                    cache.arch_k[0, slot, :, r0 : r0 + rows] = torch.from_numpy(ak).reshape(rows, H, hd).permute(1, 0, 2).to(cache._dev, torch.float16)
-                    cache.arch_v[0, slot, :, r0 : r0 + rows] = torch.from_numpy(av).reshape(rows, H, hd).permute(1, 0, 2).to(cache._dev, torch.float16)
-            else:
-                for b in range(nblk):
-                    planes = tuple(_read_plane(f) for _ in range(4))
-                    cache.import_block_planes(layer, b, planes)
-            for which, n in ((0, fp1_len), (1, fp2_len)):
-                k = _read_f32(f, (n, kv))
-                v = _read_f32(f, (n, kv))
-                if n:
-                    cache.fp_k[0, layer, which, :, :n] = torch.from_numpy(k).reshape(n, H, hd).permute(1, 0, 2).to(cache._dev, torch.float16)
-                    cache.fp_v[0, layer, which, :, :n] = torch.from_numpy(v).reshape(n, H, hd).permute(1, 0, 2).to(cache._dev, torch.float16)
-        cache._fp1_len = fp1_len
-        cache._fp2_len[:] = fp2_len
-        cache.quantized_token_count = quantized
-        cache.d_n_blocks.fill_(quantized // G)
-        cache.d_fp1_len.fill_(fp1_len)
-        cache.d_fp2_len.fill_(fp2_len)
-        cache.d_pos.fill_(quantized + fp1_len + fp2_len)
-        return cache
-
-
-_AXIS_CODES = {quant.AXIS_CHANNEL: 0, quant.AXIS_TOKEN: 1}
-_MODE_CODES = {quant.MODE_ASYM_U4: 0, quant.MODE_SYM_S4: 1}
-_AXIS_NAMES = {v: k for k, v in _AXIS_CODES.items()}
-_MODE_NAMES = {v: k for k, v in _MODE_CODES.items()}
-
-
-def _unpack(f, fmt: str):
-    size = struct.calcsize(fmt)
-    raw = f.read(size)
-    if len(raw) != size:
-        raise FormatError("snapshot truncated")
-    return struct.unpack(fmt, raw)
-
-
-def _read_f32(f, shape) -> np.ndarray:
-    count = int(np.prod(shape)) if shape else 0
-    raw = f.read(count * 4)
-    if len(raw) != count * 4:
-        raise FormatError("snapshot truncated")
-    return np.frombuffer(raw, dtype="<f4").reshape(shape).astype(np.float32)
-
-
-def _write_plane(f, plane: quant.QuantPlane) -> None:
-    f.write(struct.pack("<QIIBBI", plane.count, plane.group_size, plane.row_len or 0, _AXIS_CODES[plane.axis],
-                        _MODE_CODES[plane.mode], plane.num_groups))
-    f.write(plane.codes.tobytes())
-    f.write(plane.scales.astype("<f4").tobytes())
-    f.write(plane.zeros.astype("<f4").tobytes())
-
-
-def _read_plane(f) -> quant.QuantPlane:
-    count, group_size, row_len, axis_code, mode_code, ngroups = _unpack(f, "<QIIBBI")
-    n = (count + 1) // 2
-    raw = f.read(n)
-    if len(raw) != n:
-        raise FormatError("snapshot truncated")
-    return quant.QuantPlane(np.frombuffer(raw, dtype=np.uint8).copy(), count, group_size, _read_f32(f, (ngroups,)),
-                            _read_f32(f, (ngroups,)), _MODE_NAMES[mode_code], _AXIS_NAMES[axis_code], row_len or None)
+            return cls.from_snapshot(qskv.decode(f.read()))
 
 
 # -----------------------------------------------------------------------------
@@ -666,8 +652,9 @@ def _read_plane(f) -> quant.QuantPlane:
 class FpKVCache:
     """Device fp16 cache with the same append/rollback/view surface (Q/cache.py:561-656).
 
-    Rows live head-major ``[B][L][Hkv][cap][hd]`` so the attention kernel
-    streams one head's history contiguously.
+    Rows live head-major ``[B][L][Hkv][cap][hd]`` so the attention kernel streams one head's
+    history contiguously.  Capacity doubles when it runs out, as the reference's does
+    (Q/cache.py:606-612); ``generation`` bumps so runners and graphs rebuild.
     """
 
     def __init__(self, num_layers: int, kv_dim: int, capacity: int = 64, *, head_dim: int | None = None,
@@ -684,8 +671,9 @@ class FpKVCache:
         self._dev = torch.device("cuda")
         self.k = torch.zeros((batch, num_layers, self.kv_heads, self._cap, self.head_dim), dtype=torch.float16, device=self._dev)
         self.v = torch.zeros_like(self.k)
-        self._len = np.zeros(num_layers, dtype=np.int64)
+        self._lens = np.zeros((batch, num_layers), dtype=np.int64)
         self.d_len = torch.zeros(batch, dtype=torch.int32, device=self._dev)
+        self.d_flags = torch.zeros(1, dtype=torch.int32, device=self._dev)
         self.generation = 0
 
     @classmethod
@@ -709,13 +697,19 @@ class FpKVCache:
             dst[seq, layer, :, :s_p] = t
 
     def finish_prefill(self, s_p: int, seq: int = 0) -> None:
-        if seq == 0:
-            self._len[:] = s_p
+        self._lens[seq, :] = s_p
         self.d_len[seq] = s_p
 
     @property
+    def _len(self) -> np.ndarray:  # per-layer lengths of sequence 0 (reference protocol)
+        return self._lens[0]
+
+    @property
     def seq_len(self) -> int:
-        return int(self._len[0])
+        return int(self._lens[0, 0])
+
+    def seq_lens(self) -> np.ndarray:
+        return self._lens[:, 0].copy()
 
     @property
     def quantized_token_count(self) -> int:
@@ -725,12 +719,12 @@ class FpKVCache:
     def capacity(self) -> int:
         return self._cap
 
-    def fp2_space(self) -> int:
+    def fp2_space(self, seq: int = 0) -> int:
         return 1 << 30
 
     def check_layer_consistency(self) -> None:
-        if not np.all(self._len == self._len[0]):
-            raise CacheIntegrityError(f"per-layer append counts diverged: {self._len.tolist()}")
+        if not np.all(self._lens == self._lens[:, :1]):
+            raise CacheIntegrityError(f"per-layer append counts diverged: {self._lens.tolist()}")
 
     def _ensure(self, need: int) -> None:
         if need <= self._cap:
@@ -744,22 +738,25 @@ class FpKVCache:
         self.k, self.v, self._cap = k, v, new
         self.generation += 1
 
+    ensure_tokens = _ensure
+
     def append_decode_token(self, layer: int, k, v) -> None:
         torch = _torch()
         kt = k if isinstance(k, torch.Tensor) else torch.from_numpy(np.asarray(k, dtype=np.float32).ravel())
         vt = v if isinstance(v, torch.Tensor) else torch.from_numpy(np.asarray(v, dtype=np.float32).ravel())
         if kt.numel() != self.kv_dim or vt.numel() != self.kv_dim:
             raise DimensionError(f"expected kv rows of width {self.kv_dim}")
-        pos = int(self._len[layer])
+        pos = int(self._lens[0, layer])
         self._ensure(pos + 1)
         self.k[0, layer, :, pos] = kt.to(self._dev, torch.float16).reshape(self.kv_heads, self.head_dim)
         self.v[0, layer, :, pos] = vt.to(self._dev, torch.float16).reshape(self.kv_heads, self.head_dim)
-        self._len[layer] = pos + 1
-        if np.all(self._len == self._len[0]):
-            self.d_len[0] = int(self._len[0])
+        self._lens[0, layer] = pos + 1
+        if np.all(self._lens[0] == self._lens[0, 0]):
+            self.d_len[0] = int(self._lens[0, 0])
 
     def _advance(self, n: int) -> None:
-        self._len += n
+        self._ensure(int(self._lens.max()) + n)
+        self._lens += n
         _lib.call("qs_add_int", self.d_len.data_ptr(), self.batch, n, _lib.stream_ptr())
 
     def rollback(self, n_reject: int) -> None:
@@ -768,18 +765,26 @@ class FpKVCache:
         if n_reject == 0:
             return
         self.check_layer_consistency()
-        if n_reject > self.seq_len:
+        if n_reject > int(self._lens[:, 0].min()):
             raise CacheIntegrityError("rollback past the sequence start")
-        self._len -= n_reject
+        self._lens -= n_reject
         _lib.call("qs_add_int", self.d_len.data_ptr(), self.batch, -n_reject, _lib.stream_ptr())
 
     def flush_if_full(self) -> bool:
         return False
 
-    def _view(self, layer: int) -> CacheView:
-        n = int(self._len[layer])
-        k = self.k[0, layer, :, :n].permute(1, 0, 2).reshape(n, self.kv_dim).float().cpu().numpy()
-        v = self.v[0, layer, :, :n].permute(1, 0, 2).reshape(n, self.kv_dim).float().cpu().numpy()
+    def raise_device_flags(self, what: str, flags: int | None = None) -> None:
+        f = int(self.d_flags.item()) if flags is None else int(flags)
+        if f:
+            self.d_flags.zero_()
+            if f & _lib.FLAG_OVERFLOW:
+                raise BufferOverflowError(f"{what}: fp16 cache capacity {self._cap} exceeded")
+            raise DataError(f"{what}: device status {f:#x}")
+
+    def _view(self, layer: int, seq: int = 0) -> CacheView:
+        n = int(self._lens[seq, layer])
+        k = self.k[seq, layer, :, :n].permute(1, 0, 2).reshape(n, self.kv_dim).float().cpu().numpy()
+        v = self.v[seq, layer, :, :n].permute(1, 0, 2).reshape(n, self.kv_dim).float().cpu().numpy()
         view = CacheView(segments=[(k, v)])
         view.fp_bytes = FP_ELEM_BYTES * 2 * n * self.kv_dim
         return view

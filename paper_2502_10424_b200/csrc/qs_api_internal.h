@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include "../../include/quantspec_b200.h"
 
+#define QS_MAX_COLS 48  // activation rows of one linear launch (B * T)
+
 namespace qs {
 using AttnParams = qs_attn_args;
 using LinearParams = qs_linear_args;
@@ -20,8 +22,6 @@ inline int attention_queries_per_cta(int per, int mode) {
 }
 int attention_occupancy(int hd, int per, int mode);
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s);
-int linear_maxc(int wmode, int N, int K, int nctas);
-int linear_occupancy(int wmode, int wgroup, int ncols);
 cudaError_t launch_prep_act(const float* x, const float* gain, float eps, void* xh, long long ldxh, float* xs,
                             long long ldxs, int n, int d, cudaStream_t s);
 

@@ -1028,7 +1028,7 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
     region_kind = is1 ? 2 : 3;
     n_tok = is1 ? fp1_len : fp2_base + P.T;
     causal = is1 ? 0 : 1;
-    const size_t hoff = (size_t)seq * P.fp_seq_stride + (size_t)head * P.G * HD;
+    const size_t hoff = (size_t)seq * P.fp_seq_stride + (size_t)head * P.fp_rows * HD;
     const void* bk = is1 ? P.fp1_k : P.fp2_k;
     const void* bv = is1 ? P.fp1_v : P.fp2_v;
     fk = bk ? reinterpret_cast<const __half*>(bk) + hoff : nullptr;

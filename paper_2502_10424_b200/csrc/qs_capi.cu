@@ -22,13 +22,14 @@ cudaError_t launch_kv_quantize(const qs_kv_store& stt, int seq, int layer0, int 
                                int dst_block, int* flags, cudaStream_t s);
 cudaError_t launch_kv_dequant(const qs_kv_store& st, int seq, int layer, int nblk, int target, float* ok,
                               float* ov, cudaStream_t s);
-cudaError_t launch_fp_rotate(const qs_kv_store& st, int seq, cudaStream_t s);
+cudaError_t launch_kv_flush(const qs_kv_store& st, int* n_blocks, int* fp1_len, int* fp2_len, int* flags,
+                            cudaStream_t s);
 cudaError_t launch_rmsnorm(const float* x, const float* gain, float* out, int n, int d, float eps, cudaStream_t s);
-cudaError_t launch_embed(const float* table, const int* tok, float* out, int n, int d, int vocab, int* flags,
-                         cudaStream_t s);
+cudaError_t launch_embed(const float* table, const int* tok, int tok_stride, int T, float* out, int n, int d,
+                         int vocab, int* flags, cudaStream_t s);
 cudaError_t launch_argmax(const float* logits, int n, int vocab, int* out, int out_stride, cudaStream_t s);
-cudaError_t launch_greedy_accept(const int* drafts, const int* tgt, int gamma, int* res, int* next_tok, int* b0,
-                                 int* b1, cudaStream_t s);
+cudaError_t launch_greedy_accept(int* tok, int tok_stride, const int* tgt, int T, const int* gs, int B, int* res,
+                                 int* fp2_len, int* pos, cudaStream_t s);
 cudaError_t launch_add_int(int* p, int n, int delta, cudaStream_t s);
 
 static thread_local char g_err[512] = "";
@@ -152,17 +153,14 @@ qs_status qs_kv_quantize_blocks(const qs_kv_store* st, int seq, int layer, const
                      "kv_quantize");
 }
 
-qs_status qs_kv_flush(const qs_kv_store* st, int seq, int dst_block, int* flags, void* stream) {
+qs_status qs_kv_flush(const qs_kv_store* st, int* n_blocks, const int* fp1_len, int* fp2_len, int* flags,
+                      void* stream) {
   qs_status r = check_store(st);
   if (r) return r;
-  if (dst_block >= st->max_blocks) QS_FAIL(QS_ERR_OVERFLOW, "quantised arena full (%d blocks)", st->max_blocks);
-  size_t buf = (size_t)st->Hkv * st->G * st->hd;
-  const __half* fk = reinterpret_cast<const __half*>(st->fp_k) + (size_t)seq * st->L * 2 * buf;
-  const __half* fv = reinterpret_cast<const __half*>(st->fp_v) + (size_t)seq * st->L * 2 * buf;
-  cudaError_t e = launch_kv_quantize(*st, seq, 0, st->L, fk, fv, (long long)(2 * buf), (long long)st->G * st->hd, 1,
-                                     dst_block, flags, S(stream));
-  if (e != cudaSuccess) return cuda_status(e, "kv_flush");
-  return cuda_status(launch_fp_rotate(*st, seq, S(stream)), "fp_rotate");
+  if (!n_blocks || !fp1_len || !fp2_len) QS_FAIL(QS_ERR_CONFIG, "flush needs the device length arrays");
+  if (st->fp_rows < st->G) QS_FAIL(QS_ERR_CONFIG, "fp buffers of %d rows cannot hold a group of %d", st->fp_rows, st->G);
+  return cuda_status(launch_kv_flush(*st, n_blocks, const_cast<int*>(fp1_len), fp2_len, flags, S(stream)),
+                     "kv_flush");
 }
 
 qs_status qs_kv_dequant_view(const qs_kv_store* st, int seq, int layer, int nblk, int target, float* out_k,
@@ -192,6 +190,8 @@ qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream) {
   if (per > 12) QS_FAIL(QS_ERR_CONFIG, "at most 12 query columns per CTA (got %d); raise n_qgroups", per);
   if (a->n_main < 1) QS_FAIL(QS_ERR_CONFIG, "need at least one main split");
   if (mode != QS_VIEW_FP16 && (a->G % 16 || a->G > 128 || 128 % a->G)) QS_FAIL(QS_ERR_CONFIG, "group size %d unsupported", a->G);
+  if ((a->fp1_k || a->fp2_k) && a->fp_rows < a->G)
+    QS_FAIL(QS_ERR_CONFIG, "fp buffers of %d rows cannot hold a group of %d", a->fp_rows, a->G);
   if (mode != QS_VIEW_FP16 && !(a->G % a->hd == 0 || a->Hkv * a->hd <= a->G))
     QS_FAIL(QS_ERR_CONFIG, "value groups of %d channels would split a %d-channel head", a->G, a->hd);
   return cuda_status(launch_attention(*a, mode, S(stream)), "attn_decode");
@@ -200,13 +200,12 @@ qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream) {
 qs_status qs_linear(const qs_linear_args* a, void* stream) {
   if (!a) QS_FAIL(QS_ERR_CONFIG, "null args");
   if (a->K % 16 || a->N % 16) QS_FAIL(QS_ERR_DIMENSION, "linear dims must be multiples of 16 (N=%d K=%d)", a->N, a->K);
-  if (a->ncols < 1 || a->ncols > 16) QS_FAIL(QS_ERR_DIMENSION, "1..16 activation rows supported (got %d)", a->ncols);
+  if (a->ncols < 1 || a->ncols > QS_MAX_COLS)
+    QS_FAIL(QS_ERR_DIMENSION, "1..%d activation rows supported (got %d)", QS_MAX_COLS, a->ncols);
+  if (a->wmode == QS_W_INT4 && a->ncols > 16) QS_FAIL(QS_ERR_DIMENSION, "INT4 (draft) linear: at most 16 rows");
   if (a->epi == QS_EPI_SILU_MUL && a->N % 32) QS_FAIL(QS_ERR_DIMENSION, "gate/up interleave needs N multiple of 32");
   if (a->wmode == QS_W_INT4 && a->wgroup != 16 && a->wgroup != 32 && a->wgroup != 64 && a->wgroup != 128)
     QS_FAIL(QS_ERR_CONFIG, "INT4 group %d unsupported on the device path (16/32/64/128)", a->wgroup);
-  if (a->nctas < 1) QS_FAIL(QS_ERR_CONFIG, "nctas must be >= 1");
-  if (a->maxc < qs::linear_maxc(a->wmode, a->N, a->K, a->nctas))
-    QS_FAIL(QS_ERR_CONFIG, "workspace slots (maxc=%d) too few for this grid", a->maxc);
   if (a->xf) {
     if (a->ncols != 1 || a->K > 4096 || a->ldxf % 4 || a->ldxf < a->K)
       QS_FAIL(QS_ERR_CONFIG, "in-kernel activation prep needs one row, K <= 4096, 16-byte rows");
@@ -216,14 +215,6 @@ qs_status qs_linear(const qs_linear_args* a, void* stream) {
   }
   return cuda_status(launch_linear(*a, S(stream)), "linear");
 }
-
-qs_status qs_linear_plan(int wmode, int N, int K, int nctas, int* maxc) {
-  if (!maxc || nctas < 1 || N < 16 || K < 16) QS_FAIL(QS_ERR_CONFIG, "bad linear plan request");
-  *maxc = qs::linear_maxc(wmode, N, K, nctas);
-  return QS_OK;
-}
-
-int qs_linear_occupancy(int wmode, int wgroup, int ncols) { return qs::linear_occupancy(wmode, wgroup, ncols); }
 
 qs_status qs_prep_act(const float* x, const float* gain, float eps, void* xh, int64_t ldxh, float* xs, int64_t ldxs,
                       int n, int d, void* stream) {
@@ -236,9 +227,10 @@ qs_status qs_rmsnorm(const float* x, const float* gain, float* out, int n, int d
   return cuda_status(launch_rmsnorm(x, gain, out, n, d, eps, S(stream)), "rmsnorm");
 }
 
-qs_status qs_embed(const float* table, const int* tokens, float* out, int n, int d, int vocab, int* flags,
-                   void* stream) {
-  return cuda_status(launch_embed(table, tokens, out, n, d, vocab, flags, S(stream)), "embed");
+qs_status qs_embed(const float* table, const int* tokens, int tok_stride, int T, float* out, int n, int d,
+                   int vocab, int* flags, void* stream) {
+  if (T < 1 || tok_stride < T || n < 1 || n % T) QS_FAIL(QS_ERR_DIMENSION, "embed: bad row geometry");
+  return cuda_status(launch_embed(table, tokens, tok_stride, T, out, n, d, vocab, flags, S(stream)), "embed");
 }
 
 qs_status qs_argmax(const float* logits, int n, int vocab, int* out_idx, int out_stride, void* stream) {
@@ -246,10 +238,10 @@ qs_status qs_argmax(const float* logits, int n, int vocab, int* out_idx, int out
   return cuda_status(launch_argmax(logits, n, vocab, out_idx, out_stride, S(stream)), "argmax");
 }
 
-qs_status qs_greedy_accept(const int* drafts, const int* target, int gamma, int* res, int* next_token, int* bump0,
-                           int* bump1, void* stream) {
-  if (gamma < 0) QS_FAIL(QS_ERR_CONFIG, "gamma must be >= 0");
-  return cuda_status(launch_greedy_accept(drafts, target, gamma, res, next_token, bump0, bump1, S(stream)),
+qs_status qs_greedy_accept(int* tok, int tok_stride, const int* target, int T, const int* gamma_step, int B,
+                           int* res, int* fp2_len, int* pos, void* stream) {
+  if (T < 1 || B < 1 || tok_stride < T) QS_FAIL(QS_ERR_CONFIG, "greedy_accept: bad geometry");
+  return cuda_status(launch_greedy_accept(tok, tok_stride, target, T, gamma_step, B, res, fp2_len, pos, S(stream)),
                      "greedy_accept");
 }
 

@@ -252,4 +252,10 @@ __device__ __forceinline__ T warp_max(T v) {
   return v;
 }
 
+__device__ __forceinline__ float warp_min_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 }  // namespace qs

@@ -119,7 +119,11 @@ __device__ __forceinline__ void linear_epilogue(const LinearParams& P, float* ys
       if (n < P.Nq + P.Nk) {
         const int nn = n < P.Nq ? n : n - P.Nq;
         const int d = nn % hd;
-        const int pos = P.pos_base[sq] + P.row_offset + t;
+        int pos = P.pos_base[sq] + P.row_offset + t;
+        if (pos >= P.max_pos) {  // beyond the rope table: ConfigError on the host (Q/model.py:334-336)
+          if (P.flags) atomicOr(P.flags, 8);
+          pos = P.max_pos - 1;
+        }
         const float2 cs = rope[(size_t)pos * (hd / 2) + d / 2];
         const float e2 = __fsub_rn(__fmul_rn(ev, cs.x), __fmul_rn(ov, cs.y));
         const float o2 = __fadd_rn(__fmul_rn(ev, cs.y), __fmul_rn(ov, cs.x));
@@ -134,6 +138,10 @@ __device__ __forceinline__ void linear_epilogue(const LinearParams& P, float* ys
         const int nn = isk ? n - P.Nq : n - P.Nq - P.Nk;
         const int head = nn / hd, d = nn % hd;
         const int row = P.row_base[sq] + P.row_offset + t;
+        if (row >= P.row_cap) {  // past the buffer: BufferOverflowError on the host
+          if (P.flags) atomicOr(P.flags, 4);
+          continue;
+        }
         __half* dst = reinterpret_cast<__half*>(isk ? P.k_dst : P.v_dst) + (size_t)sq * P.kv_seq_stride +
                       (size_t)head * P.kv_head_stride + (size_t)row * hd + d;
         *reinterpret_cast<__half2*>(dst) = __floats2half2_rn(ev, ov);
@@ -551,10 +559,12 @@ struct F16Cfg {
   static constexpr int KP = 8;
   static constexpr int NCW = 2 * KP;
   static constexpr int THREADS = (NCW + 1) * 32;
-  static constexpr int KCH = 32;                       // k-steps per stage (32 KB of weights)
+  // k-steps per stage (32 KB of weights); fixed for every NTC: the k-step -> (k-part, chain)
+  // mapping, hence each column's summation order, must not depend on the number of columns
+  static constexpr int KCH = 32;
   static constexpr int HKS = KCH / KP;
   static constexpr int WBYTES = KCH * 1024;
-  static constexpr int ROWS = NTC == 1 ? 8 : 16;
+  static constexpr int ROWS = 8 * NTC;
   static constexpr int BROW = KCH * 32 + 16;
   static constexpr int OFF_B = WBYTES;
   static constexpr int STAGE = (OFF_B + ROWS * BROW + 127) / 128 * 128;
@@ -566,6 +576,7 @@ struct F16Cfg {
   static constexpr int FIXED = KP * 32 * YCOLS * 4 + 2 * 8 * 8 + 16 + ACT_ROW + ACT_SROW;
   static constexpr int NSTAGE = (232448 - FIXED) / STAGE < 8 ? (232448 - FIXED) / STAGE : 8;
   static constexpr int SMEM = NSTAGE * STAGE + FIXED;
+  static_assert(NSTAGE >= 2, "f16 linear ring needs two stages");
 };
 
 template <int NTC, int EPI>
@@ -800,21 +811,17 @@ cudaError_t launch_prep_act(const float* x, const float* gain, float eps, void* 
   return launch_pdl(prep_act_kernel, dim3(n), dim3(256), 0, s, x, gain, eps, reinterpret_cast<__half*>(xh), ldxh, xs, ldxs, d);
 }
 
-// workspace slots per 64-row tile: none is needed any more (both linear kernels own whole
-// tile pairs over the full K range); kept for the qs_linear_plan ABI
-int linear_maxc(int wmode, int N, int K, int nctas) {
-  (void)wmode;
-  (void)N;
-  (void)K;
-  (void)nctas;
-  return 1;
-}
-
 cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {
   if (p.wmode == QS_W_F16) {
-    if (p.ncols <= 8) return launch_f16p_e<1>(p, s);
-    if (p.ncols <= 16) return launch_f16p_e<2>(p, s);
-    return cudaErrorInvalidValue;
+    switch ((p.ncols + 7) / 8) {
+      case 1: return launch_f16p_e<1>(p, s);
+      case 2: return launch_f16p_e<2>(p, s);
+      case 3: return launch_f16p_e<3>(p, s);
+      case 4: return launch_f16p_e<4>(p, s);
+      case 5: return launch_f16p_e<5>(p, s);
+      case 6: return launch_f16p_e<6>(p, s);
+      default: return cudaErrorInvalidValue;
+    }
   }
   if (p.wmode == QS_W_INT4) {
     switch (p.wgroup) {
@@ -828,45 +835,5 @@ cudaError_t launch_linear(const LinearParams& p, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-
-template <int NTC>
-static int occ_f16() {
-  using C = F16Cfg<NTC>;
-  auto kern = linear_f16p_kernel<NTC, QS_EPI_STORE>;
-  int n = 0;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, C::THREADS, C::SMEM);
-  return n;
-}
-
-template <int NTC, int GKS, int CW>
-static int occ_i4() {
-  using C = I4Cfg<NTC, GKS, CW>;
-  auto kern = linear_i4_kernel<NTC, QS_EPI_STORE, GKS, CW>;
-  int n = 0;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, C::THREADS, C::SMEM);
-  return n;
-}
-
-template <int GKS>
-static int occ_i4_n(int ncols) {
-  if (ncols == 1) return occ_i4<1, GKS, 1>();
-  if (ncols == 2) return occ_i4<1, GKS, 2>();
-  if (ncols <= 4) return occ_i4<1, GKS, 4>();
-  return ncols <= 8 ? occ_i4<1, GKS, 8>() : occ_i4<2, GKS, 8>();
-}
-
-// resident CTAs per SM of the linear kernels (informational: both run min(pairs, SMs) persistent CTAs)
-int linear_occupancy(int wmode, int wgroup, int ncols) {
-  if (wmode == QS_W_F16) return ncols <= 8 ? occ_f16<1>() : occ_f16<2>();
-  switch (wgroup) {
-    case 16: return occ_i4_n<1>(ncols);
-    case 32: return occ_i4_n<2>(ncols);
-    case 64: return occ_i4_n<4>(ncols);
-    case 128: return occ_i4_n<8>(ncols);
-    default: return 0;
-  }
-}
 
 }  // namespace qs

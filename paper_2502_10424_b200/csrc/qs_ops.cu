@@ -46,19 +46,20 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restr
   for (int i = threadIdx.x; i < d; i += blockDim.x) orow[i] = __fmul_rn(__fdiv_rn(xr[i], r), gain[i]);
 }
 
-__global__ void embed_kernel(const float* __restrict__ table, const int* __restrict__ tok, float* __restrict__ out,
-                             int d, int vocab, int* flags) {
+__global__ void embed_kernel(const float* __restrict__ table, const int* __restrict__ tok, int tok_stride, int T,
+                             float* __restrict__ out, int d, int vocab, int* flags) {
   pdl_wait();
   pdl_trigger();
-  int t = tok[blockIdx.x];
+  const int c = blockIdx.x;
+  int t = tok[(c / T) * tok_stride + c % T];
   if (t < 0 || t >= vocab) {
     if (threadIdx.x == 0 && flags) atomicOr(flags, 2);
     t = 0;
   }
   const float4* src = reinterpret_cast<const float4*>(table + (size_t)t * d);
-  float4* dst = reinterpret_cast<float4*>(out + (size_t)blockIdx.x * d);
+  float4* dst = reinterpret_cast<float4*>(out + (size_t)c * d);
   for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
-  for (int i = (d / 4) * 4 + threadIdx.x; i < d; i += blockDim.x) out[(size_t)blockIdx.x * d + i] = table[(size_t)t * d + i];
+  for (int i = (d / 4) * 4 + threadIdx.x; i < d; i += blockDim.x) out[(size_t)c * d + i] = table[(size_t)t * d + i];
 }
 
 // larger value wins; NaN counts as the maximum (np.argmax returns the first NaN);
@@ -138,21 +139,27 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int* 
   }
 }
 
-// tokens[0..gamma] of the verify forward = (pending, d_0..d_{gamma-1});
-// tgt[i] = argmax of target row i.  Greedy rule of Q/specdec.py:279-298.
-__global__ void greedy_accept_kernel(const int* __restrict__ drafts, const int* __restrict__ tgt, int gamma,
-                                     int* __restrict__ res, int* __restrict__ next_tok, int* bump0, int* bump1) {
+// Greedy rule of Q/specdec.py:279-298 for a ragged batch: sequence b's verify tokens are
+// tok[b*stride + 0..T-1] = (pending, d_0, ...), tgt[b*T + i] = argmax of its target row i, and only
+// its first gamma_step[b] drafts count (rows past them are the batch's padding).
+__global__ void greedy_accept_kernel(int* __restrict__ tok, int stride, const int* __restrict__ tgt, int T,
+                                     const int* __restrict__ gs, int B, int* __restrict__ res, int* fp2_len,
+                                     int* pos) {
   pdl_wait();
   pdl_trigger();
-  if (threadIdx.x != 0) return;
-  int v = 0;
-  while (v < gamma && drafts[v] == tgt[v]) ++v;
-  int nxt = tgt[v];
-  res[0] = v;
-  res[1] = nxt;
-  if (next_tok) *next_tok = nxt;
-  if (bump0) *bump0 += v + 1;  // rows kept after rollback(gamma - v)
-  if (bump1) *bump1 += v + 1;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const int gamma = gs ? min(gs[b], T - 1) : T - 1;
+    const int* drafts = tok + (size_t)b * stride + 1;
+    const int* t = tgt + (size_t)b * T;
+    int v = 0;
+    while (v < gamma && drafts[v] == t[v]) ++v;
+    const int nxt = t[v];
+    res[2 * b] = v;
+    res[2 * b + 1] = nxt;
+    tok[(size_t)b * stride] = nxt;
+    if (fp2_len) fp2_len[b] += v + 1;  // rows kept after rollback(gamma - v)
+    if (pos) pos[b] += v + 1;
+  }
 }
 
 __global__ void add_int_kernel(int* p, int n, int delta) {
@@ -165,16 +172,16 @@ __global__ void add_int_kernel(int* p, int n, int delta) {
 cudaError_t launch_rmsnorm(const float* x, const float* gain, float* out, int n, int d, float eps, cudaStream_t s) {
   return launch_pdl(rmsnorm_kernel, dim3(n), dim3(256), 0, s, x, gain, out, d, eps);
 }
-cudaError_t launch_embed(const float* table, const int* tok, float* out, int n, int d, int vocab, int* flags,
-                         cudaStream_t s) {
-  return launch_pdl(embed_kernel, dim3(n), dim3(256), 0, s, table, tok, out, d, vocab, flags);
+cudaError_t launch_embed(const float* table, const int* tok, int tok_stride, int T, float* out, int n, int d,
+                         int vocab, int* flags, cudaStream_t s) {
+  return launch_pdl(embed_kernel, dim3(n), dim3(256), 0, s, table, tok, tok_stride, T, out, d, vocab, flags);
 }
 cudaError_t launch_argmax(const float* logits, int n, int vocab, int* out, int out_stride, cudaStream_t s) {
   return launch_pdl(argmax_kernel, dim3(n), dim3(512), 0, s, logits, vocab, out, out_stride);
 }
-cudaError_t launch_greedy_accept(const int* drafts, const int* tgt, int gamma, int* res, int* next_tok, int* b0,
-                                 int* b1, cudaStream_t s) {
-  return launch_pdl(greedy_accept_kernel, dim3(1), dim3(32), 0, s, drafts, tgt, gamma, res, next_tok, b0, b1);
+cudaError_t launch_greedy_accept(int* tok, int tok_stride, const int* tgt, int T, const int* gs, int B, int* res,
+                                 int* fp2_len, int* pos, cudaStream_t s) {
+  return launch_pdl(greedy_accept_kernel, dim3(1), dim3(32), 0, s, tok, tok_stride, tgt, T, gs, B, res, fp2_len, pos);
 }
 cudaError_t launch_add_int(int* p, int n, int delta, cudaStream_t s) {
   return launch_pdl(add_int_kernel, dim3((n + 127) / 128), dim3(128), 0, s, p, n, delta);

@@ -306,9 +306,22 @@ __global__ void pack_f16_kernel(const float* __restrict__ w, int d_in, int d_out
 }
 
 // ---------------------------------------------------------------------------
-// KV block quantisation into the store (Q/cache.py:283-303)
-// grid: x = block, y = kv head, z = layer offset.  128 threads.
+// K1: KV block quantisation into the store (Q/cache.py:283-303).
+// One CTA (256 threads) per (seq, layer, kv head, block):
+//   1. the block's K rows of this head [G][hd] (one contiguous range of the head-major source)
+//      and the V rows of its value group's channels [G][cg1 - cg0] are staged in shared memory
+//      with 16-byte coalesced loads;
+//   2. key (S, Z): one group per channel over the G tokens (lanes = channels, token parts
+//      combined through shared memory); value (S, Z): one group per token over the group's
+//      channels (a warp per token, shuffle min/max);
+//   3. every thread builds four consecutive frag4 words per plane straight from the staged
+//      values -- one 16-byte store per plane, consecutive threads -> consecutive addresses.
+// Codes use a two-level division: q = (v - Z) * (1/S) in f64 decides the rounding whenever q is
+// farther than 2^-30 from a half-integer; only near a tie does the exact __ddiv_rn path of the
+// reference recipe run, so codes stay bit-identical to Q/quant.py:220-276 in every case.
 // ---------------------------------------------------------------------------
+constexpr int KQ_THREADS = 256;
+
 struct KVQArgs {
   qs_kv_store st;
   int seq, layer0, dst_block0;
@@ -326,92 +339,112 @@ __device__ __forceinline__ int sens_slot(const qs_kv_store& st, int l) {
   for (int i = 0; i < l; ++i) c += layer_sensitive(st, i) ? 1 : 0;
   return c;
 }
+__device__ __forceinline__ int sens_count(const qs_kv_store& st) {
+  return __popcll(st.sens_mask[0]) + __popcll(st.sens_mask[1]);
+}
 
-__global__ void __launch_bounds__(128) kv_quant_kernel(const __grid_constant__ KVQArgs A) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  const qs_kv_store& st = A.st;
-  const int G = st.G, HD = st.hd, H = st.Hkv;
-  const int kv = H * HD;
-  const int b = blockIdx.x, h = blockIdx.y, layer = A.layer0 + blockIdx.z;
+// round-half-away of fl(d / s) (the reference's rha((v - Z) / S)), decided by a reciprocal
+// multiply unless the quotient sits within 2^-30 of a tie
+__device__ __forceinline__ double rha_div(double d, double s, double inv_s) {
+  const double q = d * inv_s;
+  const double a = fabs(q);
+  const double f = a - floor(a);
+  if (fabs(f - 0.5) > 9.313225746154785e-10) return copysign(floor(a + 0.5), q);
+  return rha(__ddiv_rn(d, s));
+}
+
+__device__ __forceinline__ void codes_pair(double v, double s, double z, double inv_s, int& cu, int& cl) {
+  double x = rha_div(__dsub_rn(v, z), s, inv_s);
+  x = fmin(fmax(x, 0.0), 15.0);
+  cu = (int)x;
+  const double recon = __dadd_rn(__dmul_rn((double)cu, s), z);
+  const double r = __dsub_rn(v, recon);
+  const double sl = (double)((float)s * 0.0625f);
+  double y = rha_div(r, sl, inv_s * 16.0);
+  y = fmin(fmax(y, -8.0), 7.0);
+  cl = (int)y;
+}
+
+// One (layer, head, block) job: sk / sv point at row 0 of this head's block in a head-major
+// source (head stride hs halves, row stride hd); writes planes + params of block dblk.
+__device__ void kv_block_job(const qs_kv_store& st, int seq, int layer, int h, int dblk, const __half* sk,
+                             const __half* sv_head0, long long hs, int* flags, uint8_t* smem) {
+  const int G = st.G, HD = st.hd, H = st.Hkv, kv = H * HD;
   const int tid = threadIdx.x;
-  const __half* sk = A.src_k + (size_t)blockIdx.z * A.src_layer_stride;
-  const __half* sv = A.src_v + (size_t)blockIdx.z * A.src_layer_stride;
-  const int row0 = b * G;
-  const int dblk = A.dst_block0 + b;
-
-  if (layer_sensitive(st, layer)) {
-    // sensitive layers archive fp rows instead of quantising (Q/cache.py:286-289)
-    int slot = sens_slot(st, layer);
-    int nsens = 0;
-    for (int i = 0; i < st.L; ++i) nsens += layer_sensitive(st, i) ? 1 : 0;
-    size_t cap = (size_t)st.max_blocks * G;
-    size_t base = ((((size_t)A.seq * nsens + slot) * H + h) * cap + (size_t)dblk * G) * HD;
-    __half* ak = reinterpret_cast<__half*>(st.arch_k) + base;
-    __half* av = reinterpret_cast<__half*>(st.arch_v) + base;
-    for (int i = tid; i < G * HD; i += blockDim.x) {
-      int r = i / HD, c = i % HD;
-      ak[i] = sk[(size_t)h * A.src_head_stride + (size_t)(row0 + r) * HD + c];
-      av[i] = sv[(size_t)h * A.src_head_stride + (size_t)(row0 + r) * HD + c];
+  const int cg0 = ((h * HD) / G) * G, cg1 = min(cg0 + G, kv), nv = cg1 - cg0;
+  __half* ks = reinterpret_cast<__half*>(smem);  // [G][HD]
+  __half* vs = ks + G * HD;                      // [G][nv]
+  float2* kpar = reinterpret_cast<float2*>(vs + G * nv);  // [HD]
+  float2* vpar = kpar + HD;                               // [G]
+  double* kinv = reinterpret_cast<double*>(vpar + G);     // [HD] 1/S_k
+  double* vinv = kinv + HD;                               // [G]  1/S_v
+  float* red = reinterpret_cast<float*>(vinv + G);        // [KQ_THREADS][2]
+  // ---- stage (16-byte loads; the block of one head is contiguous) ----
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(sk);
+    uint4* dst = reinterpret_cast<uint4*>(ks);
+    for (int i = tid; i < G * HD / 8; i += KQ_THREADS) dst[i] = src[i];
+    for (int i = tid; i < G * nv / 8; i += KQ_THREADS) {
+      const int r = i / (nv / 8), cc = (i % (nv / 8)) * 8;  // channel offset inside the group
+      const int c = cg0 + cc, hh = c / HD, ci = c % HD;
+      reinterpret_cast<uint4*>(vs)[i] =
+          reinterpret_cast<const uint4*>(sv_head0 + (size_t)hh * hs + (size_t)r * HD + ci)[0];
     }
-    return;
   }
-
-  uint8_t* cku = sm;             // [G][HD] codes
-  uint8_t* ckl = cku + G * HD;
-  uint8_t* cvu = ckl + G * HD;
-  uint8_t* cvl = cvu + G * HD;
+  __syncthreads();
   bool bad = false;
-
-  const size_t slh = ((size_t)A.seq * st.L + layer) * H + h;  // (seq, layer, head)
+  // ---- key params: channel c = tid % HD, token part tid / HD ----
+  {
+    const int parts = KQ_THREADS / HD;
+    const int c = tid % HD, part = tid / HD;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int r = part; r < G; r += parts) {
+      const float x = __half2float(ks[r * HD + c]);
+      bad |= !isfinite(x);
+      mn = fminf(mn, x);
+      mx = fmaxf(mx, x);
+    }
+    red[2 * tid] = mn;
+    red[2 * tid + 1] = mx;
+    __syncthreads();
+    if (part == 0) {
+      for (int p = 1; p < parts; ++p) {
+        mn = fminf(mn, red[2 * (p * HD + c)]);
+        mx = fmaxf(mx, red[2 * (p * HD + c) + 1]);
+      }
+      const UParams pr = asym_params((double)mn, (double)mx);
+      kpar[c] = make_float2(pr.s, pr.z);
+      kinv[c] = 1.0 / (double)pr.s;
+    }
+  }
+  // ---- value params: a warp per token, lanes over the group's channels ----
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int r = warp; r < G; r += KQ_THREADS / 32) {
+      float mn = INFINITY, mx = -INFINITY;
+      for (int c = lane; c < nv; c += 32) {
+        const float x = __half2float(vs[r * nv + c]);
+        bad |= !isfinite(x);
+        mn = fminf(mn, x);
+        mx = fmaxf(mx, x);
+      }
+      mn = warp_min_f(mn);
+      mx = warp_max(mx);
+      if (lane == 0) {
+        const UParams pr = asym_params((double)mn, (double)mx);
+        vpar[r] = make_float2(pr.s, pr.z);
+        vinv[r] = 1.0 / (double)pr.s;
+      }
+    }
+  }
+  if (__syncthreads_or(bad) && tid == 0 && flags) atomicOr(flags, 1);
+  const size_t slh = ((size_t)seq * st.L + layer) * H + h;
   float2* kp = reinterpret_cast<float2*>(st.kp) + (slh * st.max_blocks + dblk) * HD;
   float2* vp = reinterpret_cast<float2*>(st.vp) + (slh * st.max_blocks + dblk) * G;
-
-  // keys: one group per channel over the block's G tokens
-  for (int c = tid; c < HD; c += blockDim.x) {
-    const __half* col = sk + (size_t)h * A.src_head_stride + (size_t)row0 * HD + c;
-    double mn = INFINITY, mx = -INFINITY;
-    for (int r = 0; r < G; ++r) {
-      double x = (double)__half2float(col[(size_t)r * HD]);
-      bad |= !finite_d(x);
-      mn = fmin(mn, x);
-      mx = fmax(mx, x);
-    }
-    UParams p = asym_params(mn, mx);
-    kp[c] = make_float2(p.s, p.z);
-    for (int r = 0; r < G; ++r) {
-      double x = (double)__half2float(col[(size_t)r * HD]);
-      int cu = code_upper(x, p);
-      int cl = code_lower(x, cu, p);
-      cku[r * HD + c] = (uint8_t)cu;
-      ckl[r * HD + c] = (uint8_t)(cl + 8);
-    }
-  }
-  // values: per token, groups of G channels inside the token (row_len = kv_dim)
-  const int cg0 = ((h * HD) / G) * G;          // first channel of this head's value group
-  const int cg1 = min(cg0 + G, kv);
-  for (int r = tid; r < G; r += blockDim.x) {
-    double mn = INFINITY, mx = -INFINITY;
-    for (int c = cg0; c < cg1; ++c) {
-      int hh = c / HD, cc = c % HD;
-      double x = (double)__half2float(sv[(size_t)hh * A.src_head_stride + (size_t)(row0 + r) * HD + cc]);
-      bad |= !finite_d(x);
-      mn = fmin(mn, x);
-      mx = fmax(mx, x);
-    }
-    UParams p = asym_params(mn, mx);
-    vp[r] = make_float2(p.s, p.z);
-    for (int c = 0; c < HD; ++c) {
-      double x = (double)__half2float(sv[(size_t)h * A.src_head_stride + (size_t)(row0 + r) * HD + c]);
-      int cu = code_upper(x, p);
-      int cl = code_lower(x, cu, p);
-      cvu[r * HD + c] = (uint8_t)cu;
-      cvl[r * HD + c] = (uint8_t)(cl + 8);
-    }
-  }
-  if (__syncthreads_or(bad) && tid == 0 && A.flags) atomicOr(A.flags, 1);
-
-  // assemble frag4 words
-  const int NI = HD / 16;
+  for (int c = tid; c < HD; c += KQ_THREADS) kp[c] = kpar[c];
+  for (int r = tid; r < G; r += KQ_THREADS) vp[r] = vpar[r];
+  // ---- frag4 words: thread -> 4 consecutive words (inner tiles i4..i4+3 of one (outer, lane)) ----
+  const int NI = HD / 16, VEC = qs_vec(NI);
   const int nwords = G * HD / 8;
   const size_t pb = (size_t)G * HD / 2;
   const size_t poff = (slh * st.max_blocks + dblk) * pb;
@@ -419,33 +452,153 @@ __global__ void __launch_bounds__(128) kv_quant_kernel(const __grid_constant__ K
   uint32_t* okl = reinterpret_cast<uint32_t*>(st.kl + poff);
   uint32_t* ovu = reinterpret_cast<uint32_t*>(st.vu + poff);
   uint32_t* ovl = reinterpret_cast<uint32_t*>(st.vl + poff);
-  const int vec = qs_vec(NI);
-  for (int wi = tid; wi < nwords; wi += blockDim.x) {
-    int vp4 = wi % vec;
-    int rest = wi / vec;
-    int lane = rest % 32;
-    int rest2 = rest / 32;
-    int inner = (rest2 % (NI / vec)) * vec + vp4;
-    int outer = rest2 / (NI / vec);
-    int g = lane >> 2, t = lane & 3;
-    uint32_t wku = 0, wkl = 0, wvu = 0, wvl = 0;
+  const int vofs = h * HD - cg0;  // this head's first channel inside the staged value group
+  for (int w0 = tid * VEC; w0 < nwords; w0 += KQ_THREADS * VEC) {
+    uint32_t wku[4] = {0, 0, 0, 0}, wkl[4] = {0, 0, 0, 0}, wvu[4] = {0, 0, 0, 0}, wvl[4] = {0, 0, 0, 0};
+    for (int e = 0; e < VEC; ++e) {
+      const int wi = w0 + e;
+      const int vp4 = wi % VEC, rest = wi / VEC;
+      const int lane = rest % 32, rest2 = rest / 32;
+      const int inner = (rest2 % (NI / VEC)) * VEC + vp4, outer = rest2 / (NI / VEC);
+      const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      int j = p & 3, hb = p >> 2;
-      int row = g + 8 * (j & 1), col = 2 * t + 8 * (j >> 1) + hb;
-      // keys: outer = token tile, inner = channel tile; A[token][channel]
-      int tk = outer * 16 + row, ck = inner * 16 + col;
-      wku |= (uint32_t)cku[tk * HD + ck] << (4 * p);
-      wkl |= (uint32_t)ckl[tk * HD + ck] << (4 * p);
-      // values: outer = token tile, inner = channel tile; A[channel][token]
-      int tv = outer * 16 + col, cv = inner * 16 + row;
-      wvu |= (uint32_t)cvu[tv * HD + cv] << (4 * p);
-      wvl |= (uint32_t)cvl[tv * HD + cv] << (4 * p);
+      for (int p = 0; p < 8; ++p) {
+        const int j = p & 3, hb = p >> 2;
+        const int row = g + 8 * (j & 1), col = 2 * t + 8 * (j >> 1) + hb;
+        // keys: A = K[token][channel]
+        const int tk = outer * 16 + row, ck = inner * 16 + col;
+        const float2 pk = kpar[ck];
+        int cu, cl;
+        codes_pair((double)__half2float(ks[tk * HD + ck]), (double)pk.x, (double)pk.y, kinv[ck], cu, cl);
+        wku[e] |= (uint32_t)cu << (4 * p);
+        wkl[e] |= (uint32_t)(cl + 8) << (4 * p);
+        // values: A = V^T[channel][token]
+        const int tv = outer * 16 + col, cv = inner * 16 + row;
+        const float2 pv = vpar[tv];
+        codes_pair((double)__half2float(vs[tv * nv + vofs + cv]), (double)pv.x, (double)pv.y, vinv[tv], cu, cl);
+        wvu[e] |= (uint32_t)cu << (4 * p);
+        wvl[e] |= (uint32_t)(cl + 8) << (4 * p);
+      }
     }
-    oku[wi] = wku;
-    okl[wi] = wkl;
-    ovu[wi] = wvu;
-    ovl[wi] = wvl;
+    if (VEC == 4) {
+      reinterpret_cast<uint4*>(oku + w0)[0] = make_uint4(wku[0], wku[1], wku[2], wku[3]);
+      reinterpret_cast<uint4*>(okl + w0)[0] = make_uint4(wkl[0], wkl[1], wkl[2], wkl[3]);
+      reinterpret_cast<uint4*>(ovu + w0)[0] = make_uint4(wvu[0], wvu[1], wvu[2], wvu[3]);
+      reinterpret_cast<uint4*>(ovl + w0)[0] = make_uint4(wvl[0], wvl[1], wvl[2], wvl[3]);
+    } else {
+      for (int e = 0; e < VEC; ++e) {
+        oku[w0 + e] = wku[e];
+        okl[w0 + e] = wkl[e];
+        ovu[w0 + e] = wvu[e];
+        ovl[w0 + e] = wvl[e];
+      }
+    }
+  }
+}
+
+// sensitive layers archive fp rows instead of quantising (Q/cache.py:286-289)
+__device__ void kv_archive_job(const qs_kv_store& st, int seq, int layer, int h, int dblk, const __half* sk,
+                               const __half* sv) {
+  const int G = st.G, HD = st.hd, H = st.Hkv;
+  const size_t cap = (size_t)st.max_blocks * G;
+  const size_t base = ((((size_t)seq * sens_count(st) + sens_slot(st, layer)) * H + h) * cap + (size_t)dblk * G) * HD;
+  uint4* ak = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(st.arch_k) + base);
+  uint4* av = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(st.arch_v) + base);
+  for (int i = threadIdx.x; i < G * HD / 8; i += blockDim.x) {
+    ak[i] = reinterpret_cast<const uint4*>(sk)[i];
+    av[i] = reinterpret_cast<const uint4*>(sv)[i];
+  }
+}
+
+__host__ __device__ inline int kq_smem(int G, int hd) { return 2 * G * hd + 2 * G * G + 16 * (hd + G) + 8 * KQ_THREADS; }
+
+// prefill: blocks [0, nblk) of one (seq, layer) from head-major rows; grid (nblk, Hkv, nlayers)
+__global__ void __launch_bounds__(KQ_THREADS) kv_quant_kernel(const __grid_constant__ KVQArgs A) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int b = blockIdx.x, h = blockIdx.y, layer = A.layer0 + blockIdx.z;
+  const __half* sk = A.src_k + (size_t)blockIdx.z * A.src_layer_stride;
+  const __half* sv = A.src_v + (size_t)blockIdx.z * A.src_layer_stride;
+  const size_t row0 = (size_t)b * A.st.G * A.st.hd;
+  if (layer_sensitive(A.st, layer)) {
+    kv_archive_job(A.st, A.seq, layer, h, A.dst_block0 + b, sk + (size_t)h * A.src_head_stride + row0,
+                   sv + (size_t)h * A.src_head_stride + row0);
+    return;
+  }
+  kv_block_job(A.st, A.seq, layer, h, A.dst_block0 + b, sk + (size_t)h * A.src_head_stride + row0, sv + row0,
+               A.src_head_stride, A.flags, sm);
+}
+
+// ---------------------------------------------------------------------------
+// Decode-time flush (Q/cache.py:249-281, full-fp1 branch), device-conditioned per sequence so it
+// runs inside the captured decode cycle: sequence s flushes iff fp2_len[s] == G and fp1_len[s]
+// == G.  Three launches (each reads the lengths the previous one left untouched):
+//   kv_flush_quant_kernel  grid (Hkv, L, B): fp1 -> block n_blocks[s] (or the fp16 archive)
+//   kv_flush_rotate_kernel grid (Hkv, L, B): fp1 <- fp2 rows [0, G)
+//   kv_flush_lengths_kernel: n_blocks[s] += 1, fp2_len[s] -= G
+// ---------------------------------------------------------------------------
+struct FlushArgs {
+  qs_kv_store st;
+  const int* n_blocks;
+  const int* fp1_len;
+  const int* fp2_len;
+  int* n_blocks_w;
+  int* fp2_len_w;
+  int* flags;
+};
+
+__device__ __forceinline__ bool flush_due(const FlushArgs& A, int seq) {
+  return A.fp2_len[seq] == A.st.G && A.fp1_len[seq] == A.st.G;
+}
+
+__global__ void __launch_bounds__(KQ_THREADS) kv_flush_quant_kernel(const __grid_constant__ FlushArgs A) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  pdl_wait();
+  pdl_trigger();
+  const int h = blockIdx.x, layer = blockIdx.y, seq = blockIdx.z;
+  if (!flush_due(A, seq)) return;
+  const qs_kv_store& st = A.st;
+  const int dblk = A.n_blocks[seq];
+  if (dblk >= st.max_blocks) {
+    if (threadIdx.x == 0 && A.flags) atomicOr(A.flags, 4);  // arena full: BufferOverflowError
+    return;
+  }
+  const size_t hs = (size_t)st.fp_rows * st.hd;
+  const size_t lbase = (((size_t)seq * st.L + layer) * 2 + 0) * st.Hkv * hs;  // fp1 of (seq, layer)
+  const __half* fk = reinterpret_cast<const __half*>(st.fp_k) + lbase;
+  const __half* fv = reinterpret_cast<const __half*>(st.fp_v) + lbase;
+  if (layer_sensitive(st, layer)) {
+    kv_archive_job(st, seq, layer, h, dblk, fk + h * hs, fv + h * hs);
+    return;
+  }
+  kv_block_job(st, seq, layer, h, dblk, fk + h * hs, fv, (long long)hs, A.flags, sm);
+}
+
+__global__ void __launch_bounds__(256) kv_flush_rotate_kernel(const __grid_constant__ FlushArgs A) {
+  pdl_wait();
+  pdl_trigger();
+  const int h = blockIdx.x, layer = blockIdx.y, seq = blockIdx.z;
+  if (!flush_due(A, seq) || A.n_blocks[seq] >= A.st.max_blocks) return;
+  const qs_kv_store& st = A.st;
+  const size_t hs = (size_t)st.fp_rows * st.hd;
+  const size_t b1 = ((((size_t)seq * st.L + layer) * 2 + 0) * st.Hkv + h) * hs;
+  const size_t b2 = b1 + (size_t)st.Hkv * hs;
+  uint4* k1 = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(st.fp_k) + b1);
+  uint4* v1 = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(st.fp_v) + b1);
+  const uint4* k2 = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(st.fp_k) + b2);
+  const uint4* v2 = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(st.fp_v) + b2);
+  for (int i = threadIdx.x; i < st.G * st.hd / 8; i += blockDim.x) {
+    k1[i] = k2[i];
+    v1[i] = v2[i];
+  }
+}
+
+__global__ void kv_flush_lengths_kernel(const __grid_constant__ FlushArgs A) {
+  pdl_wait();
+  pdl_trigger();
+  for (int seq = threadIdx.x; seq < A.st.B; seq += blockDim.x) {
+    if (!flush_due(A, seq) || A.n_blocks[seq] >= A.st.max_blocks) continue;
+    A.n_blocks_w[seq] += 1;
+    A.fp2_len_w[seq] -= A.st.G;
   }
 }
 
@@ -490,21 +643,6 @@ __global__ void kv_dequant_kernel(qs_kv_store st, int seq, int layer, int target
     if (target) x = __dadd_rn(x, __dmul_rn((double)cl, __ddiv_rn(se, 16.0)));
     x = __dadd_rn(x, ze);
     ov[((size_t)b * G + r) * kvd + h * HD + c] = __double2float_rn(x);
-  }
-}
-
-// fp1 <- fp2 for every layer of one sequence (the rotation of Q/cache.py:263-264)
-__global__ void fp_rotate_kernel(__half* fk, __half* fv, size_t seq_off, int L, size_t buf_elems) {
-  size_t n = (size_t)L * buf_elems / 8;  // uint4 = 8 halves
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    size_t l = i / (buf_elems / 8), j = i % (buf_elems / 8);
-    size_t base = seq_off + l * 2 * buf_elems;
-    uint4* k1 = reinterpret_cast<uint4*>(fk + base);
-    const uint4* k2 = reinterpret_cast<const uint4*>(fk + base + buf_elems);
-    uint4* v1 = reinterpret_cast<uint4*>(fv + base);
-    const uint4* v2 = reinterpret_cast<const uint4*>(fv + base + buf_elems);
-    k1[j] = k2[j];
-    v1[j] = v2[j];
   }
 }
 
@@ -555,6 +693,15 @@ cudaError_t launch_pack_f16(const float* w, int d_in, int d_out, __half* out, cu
   return cudaGetLastError();
 }
 
+static cudaError_t kq_configure(const void* kern, int smem, int& configured) {
+  if (smem > 48 * 1024 && configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_kv_quantize(const qs_kv_store& stt, int seq, int layer0, int nlayers, const __half* sk,
                                const __half* sv, long long layer_stride, long long head_stride, int nblk,
                                int dst_block, int* flags, cudaStream_t s) {
@@ -568,16 +715,35 @@ cudaError_t launch_kv_quantize(const qs_kv_store& stt, int seq, int layer0, int 
   a.src_layer_stride = layer_stride;
   a.src_head_stride = head_stride;
   a.flags = flags;
-  int smem = 4 * stt.G * stt.hd;
+  const int smem = kq_smem(stt.G, stt.hd);
   static int configured = 0;
-  if (smem > 48 * 1024 && configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(kv_quant_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  cudaError_t e = kq_configure((const void*)kv_quant_kernel, smem, configured);
+  if (e != cudaSuccess) return e;
   dim3 grid(nblk, stt.Hkv, nlayers);
-  kv_quant_kernel<<<grid, 128, smem, s>>>(a);
+  kv_quant_kernel<<<grid, KQ_THREADS, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_kv_flush(const qs_kv_store& st, int* n_blocks, int* fp1_len, int* fp2_len, int* flags,
+                            cudaStream_t s) {
+  FlushArgs a;
+  a.st = st;
+  a.n_blocks = n_blocks;
+  a.fp1_len = fp1_len;
+  a.fp2_len = fp2_len;
+  a.n_blocks_w = n_blocks;
+  a.fp2_len_w = fp2_len;
+  a.flags = flags;
+  const int smem = kq_smem(st.G, st.hd);
+  static int configured = 0;
+  cudaError_t e = kq_configure((const void*)kv_flush_quant_kernel, smem, configured);
+  if (e != cudaSuccess) return e;
+  dim3 grid(st.Hkv, st.L, st.B);
+  e = launch_pdl(kv_flush_quant_kernel, grid, dim3(KQ_THREADS), smem, s, a);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(kv_flush_rotate_kernel, grid, dim3(256), 0, s, a);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(kv_flush_lengths_kernel, dim3(1), dim3(32), 0, s, a);
 }
 
 cudaError_t launch_kv_dequant(const qs_kv_store& st, int seq, int layer, int nblk, int target, float* ok,
@@ -585,17 +751,6 @@ cudaError_t launch_kv_dequant(const qs_kv_store& st, int seq, int layer, int nbl
   if (nblk <= 0) return cudaSuccess;
   dim3 grid(nblk, st.Hkv);
   kv_dequant_kernel<<<grid, 256, 0, s>>>(st, seq, layer, target, ok, ov);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_fp_rotate(const qs_kv_store& st, int seq, cudaStream_t s) {
-  size_t buf = (size_t)st.Hkv * st.G * st.hd;
-  size_t seq_off = (size_t)seq * st.L * 2 * buf;
-  size_t n = (size_t)st.L * buf / 8;
-  unsigned nb = (unsigned)((n + 255) / 256);
-  if (nb > 4096) nb = 4096;
-  fp_rotate_kernel<<<nb, 256, 0, s>>>(reinterpret_cast<__half*>(st.fp_k), reinterpret_cast<__half*>(st.fp_v),
-                                      seq_off, st.L, buf);
   return cudaGetLastError();
 }
 

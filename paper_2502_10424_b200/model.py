@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _lib, quant
 from .cache import CacheLayout, CacheView, FpKVCache, HierarchicalKVCache
-from .errors import ConfigError, DataError, DimensionError, EmptyPromptError, FormatError
+from .errors import BufferOverflowError, ConfigError, DataError, DimensionError, EmptyPromptError, FormatError
 from .runtime import DeviceWeights, Geometry, Runner, build_device_weights, rope_table
 
 WEIGHT_MAGIC = b"QSPW"
@@ -257,12 +257,12 @@ def _view_kind(cache, view: str) -> int:
     return {"draft": _lib.VIEW_DRAFT, "target": _lib.VIEW_TARGET}[view]
 
 
-def modeled_view_cost(cache, view: str, cfg: ModelConfig, t_ctx_after: int) -> StepCost:
+def modeled_view_cost(cache, view: str, cfg: ModelConfig, t_ctx_after: int, seq: int = 0) -> StepCost:
     """Per-forward modeled bytes/flops exactly as decode_step accumulates them."""
     c = StepCost()
     d, m = cfg.hidden, cfg.mlp_hidden
     for layer in range(cfg.num_layers):
-        qb, pb, fb, qe = _view_bytes(cache, layer, view)
+        qb, pb, fb, qe = _view_bytes(cache, layer, view, seq)
         c.kv_quantized_bytes += qb
         c.kv_param_bytes += pb
         c.kv_fp_bytes += fb
@@ -275,13 +275,13 @@ def modeled_view_cost(cache, view: str, cfg: ModelConfig, t_ctx_after: int) -> S
     return c
 
 
-def _view_bytes(cache, layer: int, view: str):
+def _view_bytes(cache, layer: int, view: str, seq: int = 0):
     """CacheView byte fields (Q/cache.py:345-378) from the host length mirror."""
     if isinstance(cache, FpKVCache):
-        n = int(cache._len[layer])
+        n = int(cache._lens[seq, layer])
         return 0.0, 0.0, 4.0 * 2 * n * cache.kv_dim, 0
     lay = cache.layout
-    nq = cache.quantized_token_count
+    nq = int(cache._nq[seq])
     qb = pb = fb = 0.0
     qe = 0
     if layer in lay.sensitive_layers:
@@ -291,7 +291,7 @@ def _view_bytes(cache, layer: int, view: str):
         qb = (0.5 if view == "draft" else 1.0) * qe
         groups = cache._groups_per_block() * (nq // lay.group_size)
         pb = 8.0 * groups * (2 if view == "target" else 1)
-    for n in (cache._fp1_len, int(cache._fp2_len[layer])):
+    for n in (int(cache._fp1[seq]), int(cache._fp2[seq, layer])):
         fb += 4.0 * 2 * n * lay.kv_dim
     return qb, pb, fb, qe
 
@@ -338,18 +338,24 @@ def verify_step(weights: ModelWeights, tokens, cache, *, view: str = "target", w
     if cache.seq_len + T > cfg.max_positions:
         raise ConfigError(f"position {cache.seq_len + T - 1} exceeds max positions {cfg.max_positions}")
     if not isinstance(cache, FpKVCache) and cache.fp2_len + T > cache.layout.group_size:
-        from .errors import BufferOverflowError
-
         raise BufferOverflowError("fp2 is full; the engine must flush before appending")
+    if getattr(cache, "batch", 1) != 1:
+        raise ConfigError("decode_step / verify_step drive a single-sequence cache; batches run through SpecEngine")
     fw, _ = weights.device()
     w = draft_weights.device if weight_mode == "int4" else fw
+    if isinstance(cache, FpKVCache):
+        cache.ensure_tokens(cache.seq_len + T)  # grows like the reference's FpKVCache (Q/cache.py:606-612)
     run = runner_for(cfg, cache, T)
-    run.tok[:T] = torch.tensor(toks, dtype=torch.int32, device="cuda")
+    run.tok[0, :T] = torch.tensor(toks, dtype=torch.int32, device="cuda")
     run.forward(w, T, _view_kind(cache, view))
     flags = int(run.flags.item())
     if flags:
         run.flags.zero_()
-        raise DataError("token id outside vocab")
+        if flags & _lib.FLAG_VOCAB:
+            raise DataError("token id outside vocab")
+        if flags & _lib.FLAG_POSITION:
+            raise ConfigError(f"position beyond the rope table ({cfg.max_positions})")
+        raise BufferOverflowError(f"device status {flags:#x}")
     logits = run.logits[:T].cpu().numpy().copy()
     cost = StepCost()
     wbytes = draft_weights.int4_weight_bytes if weight_mode == "int4" else F32_BYTES * _weight_elem_count(cfg)
@@ -380,6 +386,25 @@ def prefill(weights: ModelWeights, tokens, cache_mode: str = "fp", *, group_size
         raise ConfigError(f"unknown cache mode {cache_mode!r}")
     return prefill_device(weights, ids, cache_mode, group_size=group_size, sensitive_layers=sensitive_layers,
                           max_tokens=max_tokens)
+
+
+def prefill_batch(weights: ModelWeights, prompts, *, group_size: int | None = None,
+                  sensitive_layers: frozenset = frozenset(), max_tokens: int | None = None):
+    """Prefill independent prompts (any lengths) into one batched HierarchicalKVCache for the
+    ragged-batch SpecEngine (config 4); returns (list of last-token logits, cache)."""
+    from ._prefill import prefill_batch_device
+
+    cfg = weights.config
+    ps = [np.asarray(p, dtype=np.int64).ravel() for p in prompts]
+    for ids in ps:
+        if ids.size == 0:
+            raise EmptyPromptError("prompt must contain at least one token")
+        if ids.size > cfg.max_positions:
+            raise ConfigError(f"prompt of {ids.size} tokens exceeds max positions {cfg.max_positions}")
+        if ids.min() < 0 or ids.max() >= cfg.vocab:
+            raise DataError(f"token ids must lie in [0, {cfg.vocab})")
+    return prefill_batch_device(weights, ps, group_size=group_size, sensitive_layers=sensitive_layers,
+                                max_tokens=max_tokens)
 
 
 def chunked_attention(q: np.ndarray, chunks, scale: float | None = None) -> np.ndarray:

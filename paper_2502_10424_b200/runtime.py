@@ -199,32 +199,6 @@ def build_device_weights(geo: Geometry, layer_mats, embedding, final_norm, lm_he
 # ---------------------------------------------------------------------------
 
 
-_LIN_GRID: dict = {}
-
-
-def linear_grid(wmode: int, group: int = 16, ncols: int = 1) -> int:
-    """Stream-K grid of the linear kernel: every resident CTA slot.  f16 weights
-    (the target) use one grid for every activation-row count, so their results
-    are batch-invariant; INT4 (draft-only) sizes its grid per row count."""
-    key = (wmode, group, 16 if wmode == _lib.W_F16 else ncols)
-    n = _LIN_GRID.get(key)
-    if n is None:
-        occ = _lib.load().qs_linear_occupancy(wmode, group, key[2])
-        n = SM_COUNT * max(1, occ)
-        _LIN_GRID[key] = n
-    return n
-
-
-def linear_plan(pl: PackedLinear, ncols: int = 1) -> tuple[int, int]:
-    """(nctas, maxc) for one packed linear layer at ``ncols`` activation rows."""
-    import ctypes
-
-    nctas = linear_grid(pl.wmode, pl.group if pl.wmode == _lib.W_INT4 else 16, ncols)
-    mx = ctypes.c_int(0)
-    _lib.call("qs_linear_plan", pl.wmode, pl.N, pl.K, nctas, ctypes.byref(mx))
-    return nctas, mx.value
-
-
 def plan_attention_splits(n_heads_total: int, max_chunks: int, ctas_per_sm: int = 2) -> int:
     """Main-region splits per head so every main CTA is resident in one wave
     (the two short tail CTAs per head are scheduled after them)."""
@@ -245,7 +219,11 @@ def plan_attention_splits(n_heads_total: int, max_chunks: int, ctas_per_sm: int 
 
 
 class Runner:
-    """Scratch buffers + kernel sequence for forwards against one cache."""
+    """Scratch buffers + kernel sequence for forwards against one cache.
+
+    Token buffer ``tok`` is [B][TS] (TS = max_T + 1): column 0 holds each sequence's pending
+    token, columns 1.. its drafts; a forward over T rows reads columns [col, col + T).
+    """
 
     def __init__(self, geo: Geometry, cache, *, max_cols: int = 16, attn_splits: int | None = None,
                  shard: tuple | None = None):
@@ -258,6 +236,8 @@ class Runner:
         self.geo = geo
         self.cache = cache
         self.B = cache.batch
+        if max_cols > _lib.MAX_COLS:
+            raise ConfigError(f"{max_cols} activation rows exceed the linear kernels' {_lib.MAX_COLS}")
         self.max_cols = max_cols
         self.shard = shard
         if shard is not None:
@@ -285,40 +265,51 @@ class Runner:
         self.hh = torch.zeros((max_cols, (m + 64 + 7) // 8 * 8), dtype=torch.float16, device=dev)
         self.hs = torch.zeros((max_cols, (m // 16 + 8 + 3) // 4 * 4), dtype=torch.float32, device=dev)
         self.logits = torch.zeros((max_cols, geo.vocab), dtype=torch.float32, device=dev)
-        self.tok = torch.zeros(max_cols + 1, dtype=torch.int32, device=dev)
+        self.max_T = max(1, max_cols // self.B)
+        self.TS = self.max_T + 1
+        self.tok = torch.zeros((self.B, self.TS), dtype=torch.int32, device=dev)
         self.amax = torch.zeros(max_cols, dtype=torch.int32, device=dev)
-        self.res = torch.zeros(4, dtype=torch.int32, device=dev)
-        self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.res = torch.zeros(2 * self.B, dtype=torch.int32, device=dev)
         self.is_fp = not hasattr(cache, "d_n_blocks")
+        self.flags = cache.d_flags
         r = lgeo.num_heads // lgeo.num_kv_heads
         self.r = r
-        # attention: split-K grid per view, fixed for every T so row results are
-        # batch-invariant (a T-row verify == T single-row steps, bit for bit)
+        self._attn_splits_override = attn_splits
+        ncols_q = self.max_T * r
+        self.n_qgroups_max = max(1, -(-ncols_q // 12))
+        self._lin_cache: dict = {}
+        self._gen = None
+        self._plan()
+
+    def _plan(self) -> None:
+        """Capacity-dependent launch plan (re-run when the cache reallocates): split-K grid per
+        view -- fixed for every T, so row results are batch-invariant (a T-row verify == T
+        single-row steps, bit for bit) -- and the partials scratch it needs."""
+        torch = _torch()
+        cache = self.cache
         if self.is_fp:
             self.max_chunks = -(-cache.capacity // 64)
         else:
             self.max_chunks = -(-cache.max_blocks * cache.layout.group_size // 128)
-        self.max_T = max(1, max_cols // self.B)
-        self._attn_splits_override = attn_splits
         self._splits: dict = {}
-        ncols_q = self.max_T * r
-        self.n_qgroups_max = max(1, -(-ncols_q // 12))
+        ncols_q = self.max_T * self.r
         per = -(-ncols_q // self.n_qgroups_max)
         # queries per CTA: 8 per tile in the quantised views, 4 in the fp16 view (qs_attn_partials_floats)
         nq_cta = max(8 * max(1, -(-per // 8)), 4 * max(1, -(-per // 4)))
-        max_splits = attn_splits or max(1, min(self.max_chunks, 4 * SM_COUNT))
-        nparts = self.B * lgeo.num_kv_heads * self.n_qgroups_max * (max_splits + 2) * nq_cta * (geo.head_dim + 2)
-        self.partials = torch.zeros(nparts, dtype=torch.float32, device=dev)
-        self.attn_counters = torch.zeros(self.B * lgeo.num_kv_heads * self.n_qgroups_max, dtype=torch.int32, device=dev)
+        max_splits = self._attn_splits_override or max(1, min(self.max_chunks, 4 * SM_COUNT))
+        nparts = self.B * self.lgeo.num_kv_heads * self.n_qgroups_max * (max_splits + 2) * nq_cta * (self.geo.head_dim + 2)
+        self.partials = torch.zeros(nparts, dtype=torch.float32, device="cuda")
+        self.attn_counters = torch.zeros(self.B * self.lgeo.num_kv_heads * self.n_qgroups_max, dtype=torch.int32,
+                                         device="cuda")
         self.fp_cps = 0
         if self.is_fp:
             self.fp_cps = -(-self.max_chunks // self.splits_for(_lib.VIEW_FP16))
-        # linear scratch: per 64-row tile, maxc partial slots of [16 cols][64 rows] (grown on demand,
-        # always before any CUDA graph is captured: the first use of a shape runs eagerly)
-        nmax = max(geo.nq + 2 * geo.nk, 2 * geo.mlp_hidden, geo.vocab, geo.hidden)
-        self.work = torch.zeros(1 << 16, dtype=torch.float32, device=dev)
-        self.lin_counters = torch.zeros(-(-nmax // 64), dtype=torch.int32, device=dev)
-        self._lin_cache: dict = {}
+        self._lin_cache.clear()
+        self._gen = cache.generation
+
+    def sync_generation(self) -> None:
+        if self._gen != self.cache.generation:
+            self._plan()
 
     def splits_for(self, view: int) -> int:
         """Main-region splits of the attention grid for one view (cached)."""
@@ -330,7 +321,9 @@ class Runner:
                 cols = self.r if view == _lib.VIEW_DRAFT else min(12, self.max_T * self.r)
                 occ = _lib.load().qs_attn_occupancy(self.geo.head_dim, cols, view)
                 occ = occ if occ > 0 else 1
-                n = plan_attention_splits(self.B * self.lgeo.num_kv_heads * self.n_qgroups_max, self.max_chunks, occ)
+                # per-sequence plan (never scaled by the batch): a sequence's rows are bit-identical whatever
+                # batch it decodes in (batch-3 == three batch-1 runs)
+                n = plan_attention_splits(self.lgeo.num_kv_heads * self.n_qgroups_max, self.max_chunks, occ)
             self._splits[view] = n
         return n
 
@@ -342,21 +335,15 @@ class Runner:
 
     def _linear(self, pl: PackedLinear, src, y, ncols: int, epi: int, *, ldy: int | None = None, layer: int = 0,
                 T: int = 1, row_offset: int = 0, yh=None, stream: int, xf=None, gain=None) -> None:
-        """One stream-K linear launch.  ``src`` = (f16 rows, 16-sums) written by
+        """One persistent linear launch.  ``src`` = (f16 rows, 16-sums) written by
         ``qs_prep_act`` or a SiLU epilogue; ``yh`` = (f16 rows, 16-sums) output
         of the SiLU epilogue."""
-        key = (id(pl), ncols, epi, layer, T, row_offset, self.cache.generation)
+        key = (id(pl), ncols, epi, layer, T, row_offset, xf is not None)
         a = self._lin_cache.get(key)
         if a is None:
             geo = self.geo
             a = _lib.LinearArgs()
             a.wmode, a.epi, a.N, a.K, a.ncols = pl.wmode, epi, pl.N, pl.K, ncols
-            a.nctas, a.maxc = linear_plan(pl, ncols)
-            need = -(-pl.N // 64) * a.maxc * 16 * 64
-            if need > self.work.numel():
-                torch = _torch()
-                self.work = torch.zeros(need, dtype=torch.float32, device=self.work.device)
-                self._relink_work()
             a.wgroup = pl.group if pl.wmode == _lib.W_INT4 else 16
             a.w = pl.w.data_ptr()
             a.wparams = pl.params.data_ptr() if pl.params is not None else None
@@ -368,8 +355,6 @@ class Runner:
             if yh is not None:
                 a.yh, a.ldyh = yh[0].data_ptr(), yh[0].shape[1]
                 a.ys, a.ldys = yh[1].data_ptr(), yh[1].shape[1]
-            a.work = self.work.data_ptr()
-            a.counters = self.lin_counters.data_ptr()
             if xf is not None:
                 a.xf, a.ldxf = xf.data_ptr(), xf.shape[1]
                 a.gain = gain.data_ptr() if gain is not None else None
@@ -380,31 +365,29 @@ class Runner:
                 a.q_out = self.q.data_ptr()
                 a.row_offset = row_offset
                 a.rope = self._rope.data_ptr()
-                a.max_pos = geo.max_positions
+                a.max_pos = int(self._rope.shape[0])
+                a.flags = self.flags.data_ptr()
                 if self.is_fp:
                     L, H, cap, hd = c.num_layers, c.kv_heads, c.capacity, c.head_dim
                     a.k_dst = c.k[0, layer].data_ptr()
                     a.v_dst = c.v[0, layer].data_ptr()
                     a.kv_seq_stride = L * H * cap * hd
                     a.kv_head_stride = cap * hd
+                    a.row_cap = cap
                     a.row_base = c.d_len.data_ptr()
                     a.pos_base = c.d_len.data_ptr()
                 else:
                     lay = c.layout
-                    L, H, G, hd = lay.num_layers, lay.kv_heads, lay.group_size, lay.head_dim
+                    L, H, hd, R = lay.num_layers, lay.kv_heads, lay.head_dim, c.fp_rows
                     a.k_dst = c.fp_k[0, layer, 1].data_ptr()
                     a.v_dst = c.fp_v[0, layer, 1].data_ptr()
-                    a.kv_seq_stride = L * 2 * H * G * hd
-                    a.kv_head_stride = G * hd
+                    a.kv_seq_stride = L * 2 * H * R * hd
+                    a.kv_head_stride = R * hd
+                    a.row_cap = R
                     a.row_base = c.d_fp2_len.data_ptr()
                     a.pos_base = c.d_pos.data_ptr()
             self._lin_cache[key] = a
         _lib.check(_lib.load().qs_linear(a, stream), "qs_linear")
-
-    def _relink_work(self) -> None:
-        for v in self._lin_cache.values():
-            if isinstance(v, _lib.LinearArgs):
-                v.work = self.work.data_ptr()
 
     def _prep(self, x, gain, dst, ncols: int, stream: int) -> None:
         xh, xs = dst
@@ -414,7 +397,7 @@ class Runner:
 
     # -- attention --------------------------------------------------------------
     def _attention(self, layer: int, view: int, T: int, row_offset: int, stream: int) -> None:
-        key = ("attn", layer, view, T, row_offset, self.cache.generation)
+        key = ("attn", layer, view, T, row_offset)
         a = self._lin_cache.get(key)
         if a is None:
             geo, c = self.geo, self.cache
@@ -447,7 +430,8 @@ class Runner:
                 a.n_blocks, a.fp1_len, a.fp2_len = c.d_n_blocks.data_ptr(), c.d_fp1_len.data_ptr(), c.d_fp2_len.data_ptr()
                 a.fp1_k, a.fp1_v = c.fp_k[0, layer, 0].data_ptr(), c.fp_v[0, layer, 0].data_ptr()
                 a.fp2_k, a.fp2_v = c.fp_k[0, layer, 1].data_ptr(), c.fp_v[0, layer, 1].data_ptr()
-                a.fp_seq_stride = L * 2 * H * G * hd
+                a.fp_seq_stride = L * 2 * H * c.fp_rows * hd
+                a.fp_rows = c.fp_rows
                 if layer in lay.sensitive_layers:
                     slot = c._sens.index(layer)
                     a.main_k, a.main_v = c.arch_k[0, slot].data_ptr(), c.arch_v[0, slot].data_ptr()
@@ -470,20 +454,22 @@ class Runner:
         _lib.check(_lib.load().qs_attn_decode(a, mode, stream), "qs_attn_decode")
 
     # -- full forward -------------------------------------------------------------
-    def forward(self, w: DeviceWeights, T: int, view: int, *, row_offset: int = 0, tok_offset: int = 0,
+    def forward(self, w: DeviceWeights, T: int, view: int, *, row_offset: int = 0, tok_col: int = 0,
                 argmax_to=None, stream=None) -> None:
-        """Run one forward over ``T`` rows per sequence reading tokens from
-        ``self.tok[tok_offset:]``; logits land in ``self.logits[:B*T]``."""
+        """Run one forward over ``T`` rows per sequence reading tokens ``tok[:, tok_col:tok_col+T]``;
+        logits land in ``self.logits[:B*T]`` (row b*T + t).  ``argmax_to = (ptr, stride)`` stores
+        each row's argmax at ptr[row * stride]."""
         geo = self.geo
+        self.sync_generation()
         s = _lib.stream_ptr(stream)
         lib = _lib.load()
         ncols = self.B * T
-        if ncols > self.max_cols:
-            raise ConfigError(f"forward of {ncols} rows exceeds runner capacity {self.max_cols}")
+        if ncols > self.max_cols or tok_col + T > self.TS:
+            raise ConfigError(f"forward of {self.B} x {T} rows exceeds runner capacity {self.max_cols}")
         self._rope = w.rope
         d = geo.hidden
-        tok_ptr = self.tok.data_ptr() + 4 * tok_offset
-        _lib.check(lib.qs_embed(w.embedding.data_ptr(), tok_ptr, self.x.data_ptr(), ncols, d, geo.vocab,
+        tok_ptr = self.tok.data_ptr() + 4 * tok_col
+        _lib.check(lib.qs_embed(w.embedding.data_ptr(), tok_ptr, self.TS, T, self.x.data_ptr(), ncols, d, geo.vocab,
                                 self.flags.data_ptr(), s), "qs_embed")
         X, H = (self.xh, self.xs), (self.hh, self.hs)
         for li, lw in enumerate(w.layers):
@@ -511,7 +497,8 @@ class Runner:
             self._prep(self.x, w.final_norm, X, ncols, s)
             self._linear(w.lm_head, X, self.logits, ncols, _lib.EPI_STORE, stream=s)
         if argmax_to is not None:
-            _lib.check(lib.qs_argmax(self.logits.data_ptr(), ncols, geo.vocab, argmax_to, 1, s), "qs_argmax")
+            ptr, stride = argmax_to if isinstance(argmax_to, tuple) else (argmax_to, 1)
+            _lib.check(lib.qs_argmax(self.logits.data_ptr(), ncols, geo.vocab, ptr, stride, s), "qs_argmax")
 
     def _gather_heads(self, ncols: int) -> None:
         """All-gather every rank's attention rows [ncols, H_local*hd] into [ncols, H*hd]

@@ -16,7 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2502_10424_b200 import _lib  # noqa: E402
-from paper_2502_10424_b200.runtime import PackedLinear, linear_grid  # noqa: E402
+from paper_2502_10424_b200.runtime import PackedLinear  # noqa: E402
 
 
 def timeit(fn, iters=40):
@@ -40,13 +40,10 @@ def timeit(fn, iters=40):
 
 
 def main():
-    import ctypes
-
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", default="4096,12288;4096,4096;4096,22016;11008,4096;4096,32000")
     ap.add_argument("--ncols", type=int, default=1)
     ap.add_argument("--groups", default="32,128")
-    ap.add_argument("--nctas", type=int, default=0)
     ap.add_argument("--modes", default="f16,int4")
     ap.add_argument("--copies", type=int, default=4, help="distinct weight copies rotated (defeats L2)")
     ap.add_argument("--dbg", type=int, default=0, help="diagnostic bits (1: consumers skip the MMA work)")
@@ -68,22 +65,14 @@ def main():
                                                    xs.shape[1], a.ncols, K, _lib.stream_ptr()))
                 y = torch.zeros(a.ncols, N, device="cuda")
                 args = []
-                nct = a.nctas or linear_grid(pls[0].wmode, grp, a.ncols)
-                mx = ctypes.c_int(0)
-                _lib.call("qs_linear_plan", pls[0].wmode, N, K, nct, ctypes.byref(mx))
-                mg = -(-N // 64)
-                work = torch.zeros(mg * mx.value * 16 * 64, device="cuda")
-                cnt = torch.zeros(mg + 1, dtype=torch.int32, device="cuda")
                 for pl in pls:
                     ar = _lib.LinearArgs()
                     ar.wmode, ar.epi, ar.N, ar.K, ar.ncols = pl.wmode, _lib.EPI_STORE, N, K, a.ncols
-                    ar.nctas, ar.maxc = nct, mx.value
                     ar.wgroup = pl.group if pl.wmode == _lib.W_INT4 else 16
                     ar.w = pl.w.data_ptr()
                     ar.wparams = pl.params.data_ptr() if pl.params is not None else None
                     ar.xh, ar.ldxh, ar.xs, ar.ldxs = xh.data_ptr(), xh.shape[1], xs.data_ptr(), xs.shape[1]
                     ar.y, ar.ldy = y.data_ptr(), N
-                    ar.work, ar.counters = work.data_ptr(), cnt.data_ptr()
                     ar.dbg = a.dbg
                     args.append(ar)
                 lib = _lib.load()
@@ -96,7 +85,7 @@ def main():
                 us = timeit(run)
                 algo = pls[0].algorithmic_bytes() + 2.0 * K * a.ncols + 4.0 * N * a.ncols
                 gbs = algo / us / 1e3
-                print(f"{mode:5s} g={grp:4d} K={K:6d} N={N:6d} ncols={a.ncols:2d} nctas={nct:4d} maxc={mx.value:2d}  "
+                print(f"{mode:5s} g={grp:4d} K={K:6d} N={N:6d} ncols={a.ncols:2d}  "
                       f"{us:8.2f} us  {algo / 1e6:8.2f} MB  {gbs:7.1f} GB/s  {gbs / peak:5.1%}", flush=True)
                 del pls, args
                 torch.cuda.empty_cache()

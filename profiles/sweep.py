@@ -93,10 +93,23 @@ def main():
     c.fp_k.normal_()
     c.fp_v.normal_()
     st = c.store_struct()
-    us = timed(lambda: _lib.call("qs_kv_flush", st, 0, 0, c.d_flags.data_ptr(), _lib.stream_ptr()))
     rd = L * 2 * G * kv * 2.0
     wr = L * (G * kv * 2 * 1.0 + 16.0 * kv)
-    print(f"# flush-quantise, {L} layers x {H} heads, one block each: {us:.1f} us "
+    # the K1 kernel alone on the same work (32 blocks x H heads, one launch)
+    src_k = torch.randn(H, L * G, hd, device="cuda").half()
+    src_v = torch.randn(H, L * G, hd, device="cuda").half()
+    us_q = timed(lambda: _lib.call("qs_kv_quantize_blocks", st, 0, 0, src_k.data_ptr(), src_v.data_ptr(), L * G * hd, L,
+                                   0, c.d_flags.data_ptr(), _lib.stream_ptr()))
+    print(f"# K1 quantise kernel, {L} blocks x {H} heads: {us_q:.1f} us ({(rd + wr) / us_q / 1e3:.0f} GB/s)")
+
+    def flush():  # the decode-time flush (device-conditioned: quantise + rotate + lengths), lengths re-armed
+        c.d_fp1_len.fill_(G)
+        c.d_fp2_len.fill_(G)
+        c.d_n_blocks.zero_()
+        c.launch_device_flush()
+
+    us = timed(flush)
+    print(f"# flush-quantise, {L} layers x {H} heads, one block each (incl. 3 length re-arm fills): {us:.1f} us "
           f"({(rd + wr) / us / 1e3:.0f} GB/s; reads {rd / 1e6:.1f} MB fp16, writes {wr / 1e6:.1f} MB planes+params)")
 
 

@@ -241,7 +241,7 @@ def _run_attention(cache, q, view, T, row_offset=0, r=1):
     return run.attn[:T].cpu().numpy()
 
 
-@pytest.mark.parametrize("H,hd,G,n_prompt", [(4, 128, 128, 5 * 128 + 40), (4, 16, 16, 300), (4, 16, 128, 700),
+@pytest.mark.parametrize("H,hd,G,n_prompt", [(4, 128, 128, 5 * 128 + 40), (4, 16, 16, 291), (4, 16, 128, 700),
                                              (2, 64, 64, 64 * 9 + 3)])
 @pytest.mark.parametrize("view", ["draft", "target"])
 @pytest.mark.parametrize("T", [1, 5, 9])
@@ -357,18 +357,10 @@ def _act_buffers(x):
     return xh, xs
 
 
-def _run_linear(pl, x, ncols, *, epi=None, nctas=None, y=None, yh=None, xf=None, gain=None, eps=1e-5):
-    import ctypes
-
-    from paper_2502_10424_b200.runtime import linear_grid
-
+def _run_linear(pl, x, ncols, *, epi=None, y=None, yh=None, xf=None, gain=None, eps=1e-5):
     xh, xs = _act_buffers(x)
     a = _lib.LinearArgs()
     a.wmode, a.epi, a.N, a.K, a.ncols = pl.wmode, _lib.EPI_STORE if epi is None else epi, pl.N, pl.K, ncols
-    a.nctas = nctas or linear_grid(pl.wmode, pl.group if pl.wmode == _lib.W_INT4 else 16, ncols)
-    mx = ctypes.c_int(0)
-    _lib.call("qs_linear_plan", pl.wmode, pl.N, pl.K, a.nctas, ctypes.byref(mx))
-    a.maxc = mx.value
     a.wgroup = pl.group if pl.wmode == _lib.W_INT4 else 16
     a.w = pl.w.data_ptr()
     a.wparams = pl.params.data_ptr() if pl.params is not None else None
@@ -379,24 +371,22 @@ def _run_linear(pl, x, ncols, *, epi=None, nctas=None, y=None, yh=None, xf=None,
         a.y, a.ldy = y.data_ptr(), y.shape[1]
     if yh is not None:
         a.yh, a.ldyh, a.ys, a.ldys = yh[0].data_ptr(), yh[0].shape[1], yh[1].data_ptr(), yh[1].shape[1]
-    mg = -(-pl.N // 64)
-    work = torch.full((mg * a.maxc * 16 * 64,), float("nan"), device="cuda")
-    cnt = torch.zeros(mg + 1, dtype=torch.int32, device="cuda")
-    a.work, a.counters = work.data_ptr(), cnt.data_ptr()
     if xf is not None:  # INT4 in-kernel activation prep (xh / xs are then not read)
         a.xf, a.ldxf, a.eps = xf.data_ptr(), xf.shape[1], eps
         a.gain = gain.data_ptr() if gain is not None else None
     _lib.check(_lib.load().qs_linear(a, _lib.stream_ptr()))
     torch.cuda.synchronize()
-    assert int(cnt.sum().item()) == 0  # the kernels need no cross-CTA workspace
     return y
 
 
 @pytest.mark.parametrize("K,N,ncols", [(64, 48 * 4, 1), (4096, 4096, 1), (176, 64, 5), (4096, 11008 * 2, 9),
                                        (11008, 4096, 5), (4096, 32000, 16), (1024, 576, 2), (176, 64, 3),
-                                       (11008, 128, 4), (272, 4096, 1)])
+                                       (11008, 128, 4), (272, 4096, 1), (4096, 6144, 24), (1024, 512, 40),
+                                       (4096, 4096, 48), (4096, 1024, 33)])
 @pytest.mark.parametrize("mode", ["f16", "int4"])
 def test_linear_vs_torch(K, N, ncols, mode):
+    if mode == "int4" and ncols > 16:
+        pytest.skip("INT4 weights are draft-only: one row per sequence, at most 16 sequences")
     from paper_2502_10424_b200.runtime import PackedLinear
 
     g = torch.Generator(device="cuda").manual_seed(K + N)
@@ -472,16 +462,18 @@ def test_linear_batch_invariant(mode):
     K, N = 4096, 4096
     g = torch.Generator(device="cuda").manual_seed(3)
     w = torch.randn(K, N, device="cuda", generator=g) / math.sqrt(K)
-    x = torch.randn(9, K, device="cuda", generator=g)
+    big = 40 if mode == "f16" else 9  # f16: up to the 8-sequence x 5-row verify of config 4
+    x = torch.randn(big, K, device="cuda", generator=g)
     pl = PackedLinear.f16(w) if mode == "f16" else PackedLinear.int4(w, 64)
-    y9 = _run_linear(pl, x, 9)
-    for c in (0, 4, 8):
-        for n in (1, 2, 3, 6):
-            yn = _run_linear(pl, x[c:c + n].contiguous(), min(n, 9 - c))
+    yb = _run_linear(pl, x, big)
+    for c in (0, 4, 8, big - 1):
+        for n in (1, 2, 3, 6, 17):
+            n = min(n, big - c)
+            yn = _run_linear(pl, x[c:c + n].contiguous(), n)
             if mode == "f16":
-                assert torch.equal(yn[0], y9[c])
+                assert torch.equal(yn[0], yb[c])
             else:
-                assert (yn[0] - y9[c]).abs().max().item() <= 1e-4 * y9[c].abs().max().item()
+                assert (yn[0] - yb[c]).abs().max().item() <= 1e-4 * yb[c].abs().max().item()
 
 
 @pytest.mark.parametrize("mode", ["f16", "int4"])
@@ -541,14 +533,22 @@ def toy():
 
 
 def _oracle_cache_like(dev_cache):
-    """Oracle cache holding exactly the device cache's contents (fp16 values)."""
+    """Oracle cache holding exactly the device cache's contents (fp16 values; sensitive
+    layers' archived fp16 rows)."""
     lay = dev_cache.layout
-    olay = O.Layout(lay.num_layers, lay.num_heads, lay.head_dim, lay.group_size)
+    olay = O.Layout(lay.num_layers, lay.kv_heads, lay.head_dim, lay.group_size, frozenset(lay.sensitive_layers))
     oc = O.OracleKVCache(olay)
     G = lay.group_size
     nb = dev_cache.quantized_token_count // G
     for layer in range(lay.num_layers):
-        for b in range(nb):
+        if layer in lay.sensitive_layers:
+            slot = sorted(lay.sensitive_layers).index(layer)
+            for b in range(nb):
+                rows = slice(b * G, (b + 1) * G)
+                k = dev_cache.arch_k[0, slot, :, rows].permute(1, 0, 2).reshape(G, lay.kv_dim).float().cpu().numpy()
+                v = dev_cache.arch_v[0, slot, :, rows].permute(1, 0, 2).reshape(G, lay.kv_dim).float().cpu().numpy()
+                oc.archived[layer].append((k, v))
+        for b in range(nb if layer not in lay.sensitive_layers else 0):
             ku, kl, vu, vl = dev_cache.export_block_planes(layer, b)
             oc.blocks[layer].append(O.Block(*(O.Plane(p.codes, p.count, p.group_size, p.scales, p.zeros, p.mode, p.axis, p.row_len) for p in (ku, kl, vu, vl))))
         for which, n in ((0, dev_cache.fp1_len), (1, dev_cache.fp2_len)):
@@ -593,6 +593,55 @@ def test_decode_step_logits_vs_oracle(toy, view):
                                             ocost.kv_param_bytes, ocost.kv_fp_bytes, ocost.kv_quantized_elements]
 
 
+def _f16_weights(ow):
+    ow16 = copy.deepcopy(ow)
+    for olw in ow16["layers"]:
+        for n in O.MATS:
+            olw[n] = f16(olw[n])
+    ow16["lm_head"] = f16(ow16["lm_head"])
+    return ow16
+
+
+def test_int4_decode_step_vs_oracle(toy):
+    """INT4-weight draft forward (W4A16 GEMV, f16 activations) vs O.decode_step(..., "int4") with
+    the oracle's dequantised INT4 weights (Q/model.py:141-168) on the same cache contents; the
+    codes and (S, Z) are bit-exact on both sides, so the bar is the f16-activation tolerance:
+    max |err| <= 1e-2 * max |logit|."""
+    w, ow = toy
+    prompt = np.random.default_rng(33).integers(0, 64, size=300)
+    _, cache = qs.prefill(w, prompt, "hierarchical", group_size=16)
+    oc = _oracle_cache_like(cache)
+    q = qs.quantize_model_weights(w, 32)
+    draft = O.quantize_model(ow, 32)
+    for tok in (11, 40):
+        lg, cost = qs.decode_step(w, tok, cache, view="draft", weight_mode="int4", draft_weights=q)
+        olg, ocost = O.decode_step(ow, tok, oc, "draft", "int4", draft)
+        scale = max(1.0, float(np.abs(olg).max()))
+        assert np.abs(lg - olg).max() <= 1e-2 * scale, np.abs(lg - olg).max()
+        assert cost.weight_bytes == ocost.weight_bytes == draft["int4_weight_bytes"]
+
+
+@pytest.mark.parametrize("view", ["draft", "target"])
+def test_sensitive_layer_decode_vs_oracle(toy, view):
+    """Sensitive layers (Q/cache.py:286-289, :351-356) keep fp history: the device archives fp16
+    rows and routes the layer to the fp16 attention kernel (K4) over the archive + fp1/fp2; the
+    other layer reads the planes.  Logits vs the oracle on identical contents (2e-2 bar as above)."""
+    w, ow = toy
+    prompt = np.random.default_rng(34).integers(0, 64, size=150)
+    _, cache = qs.prefill(w, prompt, "hierarchical", group_size=16, sensitive_layers=frozenset({0}))
+    assert cache.quantized_token_count > 0
+    oc = _oracle_cache_like(cache)
+    ow16 = _f16_weights(ow)
+    for tok in (3, 17, 60):
+        lg, cost = qs.decode_step(w, tok, cache, view=view)
+        olg, ocost = O.decode_step(ow16, tok, oc, view)
+        scale = max(1.0, float(np.abs(olg).max()))
+        assert np.abs(lg - olg).max() <= 2e-2 * scale, np.abs(lg - olg).max()
+        assert cost.kv_fp_bytes == ocost.kv_fp_bytes and cost.kv_quantized_bytes == ocost.kv_quantized_bytes
+        cache.flush_if_full()
+        oc.flush_if_full()
+
+
 @pytest.mark.parametrize("V", [32000, 32003, 128256])
 def test_argmax_first_max_wide_rows(V):
     """qs_argmax == np.argmax (first maximum; first NaN) on vocabulary-sized rows: the
@@ -611,29 +660,40 @@ def test_argmax_first_max_wide_rows(V):
 
 
 def test_greedy_accept_kernel_matches_oracle_rule():
+    """Batched accept kernel vs the reference rule (Q/specdec.py:276-298), one ragged batch of B
+    sequences per trial: each sequence has its own gamma_step (padding rows past it ignored)."""
     rng = np.random.default_rng(9)
     dev = torch.device("cuda")
-    for trial in range(200):
-        gamma = int(rng.integers(0, 9))
+    for trial in range(100):
+        B = int(rng.integers(1, 6))
+        T = int(rng.integers(1, 10))
+        gs = rng.integers(0, T, size=B)
         V = 37
-        logits = rng.standard_normal((gamma + 1, V)).astype(np.float32)
+        logits = rng.standard_normal((B, T, V)).astype(np.float32)
         if trial % 3 == 0:
-            logits[:, 5] = logits.max(axis=1) + 0.0  # exact ties -> lowest index wins
-        tgt = logits.argmax(axis=1)
-        drafts = [int(tgt[i]) if rng.random() < 0.7 else int(rng.integers(0, V)) for i in range(gamma)]
-        want_v, corr, bonus = O.greedy_accept(drafts, list(logits))
-        lg = torch.from_numpy(logits).to(dev)
-        am = torch.zeros(gamma + 1, dtype=torch.int32, device=dev)
-        _lib.check(_lib.load().qs_argmax(lg.data_ptr(), gamma + 1, V, am.data_ptr(), 1, _lib.stream_ptr()))
-        toks = torch.tensor([0] + drafts + [0], dtype=torch.int32, device=dev)
-        res = torch.zeros(4, dtype=torch.int32, device=dev)
-        l1 = torch.zeros(1, dtype=torch.int32, device=dev)
-        _lib.check(_lib.load().qs_greedy_accept(toks.data_ptr() + 4, am.data_ptr(), gamma, res.data_ptr(),
-                                                toks.data_ptr(), l1.data_ptr(), None, _lib.stream_ptr()))
-        r = res.cpu().tolist()
-        assert am.cpu().tolist() == tgt.tolist()
-        assert r[0] == want_v and r[1] == (corr if corr is not None else bonus)
-        assert int(l1.item()) == want_v + 1 and int(toks[0].item()) == r[1]
+            logits[:, :, 5] = logits.max(axis=2) + 0.0  # exact ties -> lowest index wins
+        tgt = logits.argmax(axis=2)
+        TS = T + 1
+        toks = np.zeros((B, TS), np.int32)
+        want = []
+        for b in range(B):
+            drafts = [int(tgt[b, i]) if rng.random() < 0.7 else int(rng.integers(0, V)) for i in range(T - 1)]
+            toks[b, 1:T] = drafts
+            want.append(O.greedy_accept(drafts[: gs[b]], list(logits[b, : gs[b] + 1])))
+        lg = torch.from_numpy(logits.reshape(B * T, V)).to(dev)
+        am = torch.zeros(B * T, dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().qs_argmax(lg.data_ptr(), B * T, V, am.data_ptr(), 1, _lib.stream_ptr()))
+        dtok = torch.from_numpy(toks).to(dev)
+        dgs = torch.from_numpy(gs.astype(np.int32)).to(dev)
+        res = torch.zeros(2 * B, dtype=torch.int32, device=dev)
+        f2 = torch.full((B,), 3, dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().qs_greedy_accept(dtok.data_ptr(), TS, am.data_ptr(), T, dgs.data_ptr(), B,
+                                                res.data_ptr(), f2.data_ptr(), None, _lib.stream_ptr()))
+        r = res.cpu().numpy().reshape(B, 2)
+        assert am.cpu().numpy().reshape(B, T).tolist() == tgt.tolist()
+        for b, (v, corr, bonus) in enumerate(want):
+            assert r[b, 0] == v and r[b, 1] == (corr if corr is not None else bonus), (trial, b)
+            assert int(f2[b]) == 3 + v + 1 and int(dtok[b, 0]) == r[b, 1]
 
 
 @pytest.mark.parametrize("gamma", [1, 2, 4, 6])

@@ -66,7 +66,7 @@ def _worker(rank: int, world: int, port: int, out):
         errs = []
         for view, T, toks in ((_lib.VIEW_DRAFT, 1, [7]), (_lib.VIEW_TARGET, 3, [11, 40, 2])):
             for run, weights in ((full, fw), (part, fw_l)):
-                run.tok[:T] = torch.tensor(toks, dtype=torch.int32, device="cuda")
+                run.tok[0, :T] = torch.tensor(toks, dtype=torch.int32, device="cuda")
                 run.forward(weights, T, view)
             torch.cuda.synchronize()
             a, b = full.logits[:T].cpu().numpy(), part.logits[:T].cpu().numpy()

@@ -83,20 +83,6 @@ def test_attention_split_plan(heads, occ):
     assert plan_attention_splits(heads, 3, occ) <= 3
 
 
-@pytest.mark.parametrize("N,K,nctas", [(4096, 4096, 296), (22016, 4096, 444), (4096, 11008, 148), (192, 64, 1000),
-                                       (64, 176, 7), (32000, 4096, 296)])
-def test_linear_plan_needs_no_workspace(N, K, nctas):
-    """Both linear kernels own whole tile pairs over the full K range: no cross-CTA
-    partials, one (unused) workspace slot per tile whatever the grid."""
-    from paper_2502_10424_b200 import _build
-
-    lib = ctypes.CDLL(_build.build())
-    mx = ctypes.c_int(0)
-    for wmode in (0, 1):
-        assert lib.qs_linear_plan(wmode, N, K, nctas, ctypes.byref(mx)) == 0
-        assert mx.value == 1
-
-
 def test_interleave_cols_gate_up_tiles():
     import torch
 
