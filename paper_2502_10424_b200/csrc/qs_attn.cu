@@ -46,7 +46,10 @@ __device__ __forceinline__ void mma_nv(float (&d)[4], const uint32_t (&a)[4], ui
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-constexpr int PSTRIDE = 24;  // halves per P row (16 tokens + pad: conflict-free transposes)
+constexpr int PSTRIDE = 24;
+#ifndef QS_DRAFT_NPC
+#define QS_DRAFT_NPC 1
+#endif  // halves per P row (16 tokens + pad: conflict-free transposes)
 
 // NT: quantised modes -> query tiles of 8 queries (QK runs queries on the MMA M rows:
 // hi parts in rows 0-7, lo parts in rows 8-15); fp16 mode -> n-tiles of 4 queries
@@ -87,7 +90,11 @@ struct AttnCfg {
   static constexpr int MERGE_BYTES = NCW * NQ * MS * 4;
   static constexpr int BQF_WORDS = ROWQ ? KS * NT * AQ : KS * NTO * 64;  // query fragments of fp16 chunks
   static constexpr int PW_HALVES = NTO * 8 * PSTRIDE;
-  static constexpr int FIXED = BQF_WORDS * 4 + NQ * HD * 4 + (ROWQ ? 0 : NCW * PW_HALVES * 2) + 3 * 8 * 8 + 16;
+  // chunks a draft consumer warp carries per loop iteration (its tile of each): one online-softmax
+  // update, one P transpose round trip and one barrier round per NPC chunks, twice the MMA chains
+  static constexpr int NPC = (QUANT && !ROWQ && NT == 1) ? QS_DRAFT_NPC : 1;
+  static constexpr int PW_WARP = PW_HALVES * NPC;  // halves of P transpose buffer per warp
+  static constexpr int FIXED = BQF_WORDS * 4 + NQ * HD * 4 + (ROWQ ? 0 : NCW * PW_WARP * 2) + 3 * 8 * 8 + 16;
   // TMA ring: two CTAs per SM when at least 4 stages fit each (of 228 KB, 1 KB reserved per CTA),
   // else one CTA with the deepest ring that fits; at most 6 stages
   static constexpr int S2 = (233472 / 2 - 1024 - FIXED) / QSTAGE;
@@ -148,14 +155,16 @@ __device__ __forceinline__ float softmax_update(Softmax& st, const float (&s)[NS
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
   float alpha = 1.0f;
   if (mx > st.m) {
-    alpha = exp2f(st.m - mx);  // st.m == -inf -> 0
+    alpha = ex2_approx(st.m - mx);  // st.m == -inf -> 0
     st.l *= alpha;
     st.z *= alpha;
     st.ps *= alpha;
     st.m = mx;
   }
 #pragma unroll
-  for (int i = 0; i < NS; ++i) p[i] = (s[i] == kNegInf) ? 0.0f : exp2f(s[i] - st.m);
+  const float mu = st.m == kNegInf ? 0.f : st.m;  // every score -inf: p = ex2(-inf) = 0, not NaN
+#pragma unroll
+  for (int i = 0; i < NS; ++i) p[i] = ex2_approx(s[i] - mu);
   return alpha;
 }
 
@@ -461,7 +470,7 @@ __device__ __forceinline__ void fp16_region_q(uint8_t* region, uint32_t* aqf, co
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         float alpha = 1.0f;
         if (mx > st[nt].m) {
-          alpha = exp2f(st[nt].m - mx);
+          alpha = ex2_approx(st[nt].m - mx);
           st[nt].l *= alpha;
           st[nt].m = mx;
         }
@@ -476,12 +485,12 @@ __device__ __forceinline__ void fp16_region_q(uint8_t* region, uint32_t* aqf, co
             acc[cm][nt][3] *= a1;
           }
         }
-        const float m = st[nt].m;
+        const float m = st[nt].m == kNegInf ? 0.f : st[nt].m;
         float p[2][2];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) p[j][e] = sv[j][e] == kNegInf ? 0.f : exp2f(sv[j][e] - m);
+          for (int e = 0; e < 2; ++e) p[j][e] = ex2_approx(sv[j][e] - m);
         st[nt].l += (p[0][0] + p[0][1]) + (p[1][0] + p[1][1]);
         const __half2 h0 = __floats2half2_rn(p[0][0], p[0][1]), h1 = __floats2half2_rn(p[1][0], p[1][1]);
         const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
@@ -535,8 +544,12 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       if (warp == C::NCW) {
         // dedicated TMA warp: chunk c >= S goes into the stage chunk c - S vacated (whole warp
         // loops, lane 0 issues, so it reaches the kernel's CTA barriers converged)
-        for (int c = S; c < nchunk; ++c) {
-          mbar_wait(&empty_b[c % S], ((c - S) / S) & 1);
+        for (int c = S, st_ = 0, ph_ = 0; c < nchunk; ++c) {
+          mbar_wait(&empty_b[st_], ph_);
+          if (++st_ == S) {
+            st_ = 0;
+            ph_ ^= 1;
+          }
           if (lane == 0) issue(c);
           __syncwarp();
         }
@@ -562,10 +575,11 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         }
     }
     // chunks 0..S-1 were issued by the kernel prologue (before pdl_wait)
+    static_assert(NPW <= S, "fold warps step through the ring");
+    int s = pwid % S, ph = (pwid / S) & 1, s_prev = 0, ph_prev = 0;
     for (int j = pwid; j < nchunk; j += NPW) {
-      const int s = j % S;
       uint8_t* sp = stage_ptr(s);
-      mbar_wait(&tma_b[s], (j / S) & 1);
+      mbar_wait(&tma_b[s], ph);
       const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + j) * QS_CHUNK_Q);
       const int nbl = (ntok_chunk + G - 1) >> lgG;
       const float2* kps = reinterpret_cast<const float2*>(sp + C::KP_OFF);
@@ -654,8 +668,15 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       // refill the stage of this warp's previous chunk (every chunk >= S is issued exactly once)
       const int jp = j - NPW;
       if (!C::TMAW && jp >= 0 && jp + S < nchunk) {
-        mbar_wait(&empty_b[jp % S], (jp / S) & 1);
+        mbar_wait(&empty_b[s_prev], ph_prev);
         if (lane == 0) issue(jp + S);
+      }
+      s_prev = s;
+      ph_prev = ph;
+      s += NPW;
+      if (s >= S) {
+        s -= S;
+        ph ^= 1;
       }
     }
     return;
@@ -671,10 +692,9 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   //   P.V (channels on M): A = V^T codes, B = p' = p * S_v (hi, and lo for the target).
   const float sl2 = P.sm_scale_log2;
   const int mt = warp;
-  for (int i = 0; i < nchunk; ++i) {
-    const int s = i % S;
+  for (int i = 0, s = 0, ph = 0; i < nchunk; ++i) {
     const uint8_t* sp = stage_ptr(s);
-    mbar_wait(&full_b[s], (i / S) & 1);
+    mbar_wait(&full_b[s], ph);
     const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
     const bool live = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
     if (live) {
@@ -723,7 +743,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         float alpha = 1.0f;
         if (mx > st[nt].m) {
-          alpha = exp2f(st[nt].m - mx);  // st.m == -inf -> 0
+          alpha = ex2_approx(st[nt].m - mx);  // st.m == -inf -> 0
           st[nt].l *= alpha;
           st[nt].z *= alpha;
           st[nt].ps *= alpha;
@@ -742,8 +762,8 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
           }
         }
         const float m = st[nt].m;
-        const float p00 = exp2f(sv[0][0] - m), p01 = exp2f(sv[0][1] - m);
-        const float p10 = exp2f(sv[1][0] - m), p11 = exp2f(sv[1][1] - m);
+        const float p00 = ex2_approx(sv[0][0] - m), p01 = ex2_approx(sv[0][1] - m);
+        const float p10 = ex2_approx(sv[1][0] - m), p11 = ex2_approx(sv[1][1] - m);
         st[nt].l += (p00 + p01) + (p10 + p11);
         st[nt].z += (p00 * vz0.y + p01 * vz0.w) + (p10 * vz1.y + p11 * vz1.w);
         const float v00 = p00 * (vz0.x * kvs), v01 = p01 * (vz0.z * kvs);
@@ -780,89 +800,137 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_b[s]);
+    if (++s == S) {
+      s = 0;
+      ph ^= 1;
+    }
   }
   } else {
   // ======================= consumer warps =======================
+  // Warp mt owns the 16-token tile mt of every chunk and carries NPC consecutive chunks per
+  // iteration: their Q.K^T chains run interleaved, one online-softmax update covers all of them,
+  // and their P.V k-steps accumulate into the same registers in chunk order (the per-chunk
+  // latency chain -- barrier wait, shuffles, P transpose -- is paid once per NPC chunks).
+  constexpr int NP = C::NPC;
   const float sl2 = P.sm_scale_log2;
   const int mt = warp;  // this warp's 16-token tile of every chunk
   // P' feeds P.V as f16 hi parts only (the lo columns stay zero): |error| <= 2^-12 |p'|, inside
   // the draft's fp16-level tolerance, and one split fewer per score
-  for (int i = 0, s = 0, ph = 0; i < nchunk; ++i) {
-    const uint8_t* sp = stage_ptr(s);
-    mbar_wait(&full_b[s], ph);
-    const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
-    const bool live = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
-    if (live) {
+  for (int i0 = 0, s = 0, ph = 0; i0 < nchunk; i0 += NP) {
+    const uint8_t* sp[NP];
+    bool live[NP];
+    int stg[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int i = i0 + k;
+      stg[k] = s;
+      sp[k] = stage_ptr(s);
+      live[k] = false;
+      if (i < nchunk) {
+        mbar_wait(&full_b[s], ph);
+        const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
+        live[k] = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
+      }
+      if (++s == S) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    if (live[0]) {  // live[k] implies live[k - 1]
       const int bl = (mt * 16) >> lgG;
-      const uint32_t* bqb = reinterpret_cast<const uint32_t*>(sp + C::BQ_OFF);
-      const float* bias = reinterpret_cast<const float*>(sp + C::BIAS_OFF);
-      const float2* vps = reinterpret_cast<const float2*>(sp + C::VP_OFF);
-      // ---- Q.K^T: A = K codes [tokens x channels], two accumulator chains ----
-      uint32_t wu[KS], wl[KS];
-      load_words<KS>(reinterpret_cast<const uint32_t*>(sp), mt, lane, wu);
-      if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp + 2 * C::PLANE_CHUNK), mt, lane, wl);
-      float d0[NT][4], d1[NT][4];
+      // ---- Q.K^T: A = K codes [tokens x channels], two accumulator chains per chunk ----
+      float d[NP][2][NT][4];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+      for (int k = 0; k < NP; ++k)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) d0[nt][e] = d1[nt][e] = 0.f;
-      const uint2* bqt = reinterpret_cast<const uint2*>(bqb) + (size_t)bl * KS * NT * 32 + lane;
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[k][j][nt][e] = 0.f;
+      // both chunks' chains run unconditionally (a dead second chunk -- past the range or a
+      // partial tile -- reads finite codes and is masked to -inf below), so they interleave
+      uint32_t wu[NP][KS], wl[NP][KS];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        load_words<KS>(reinterpret_cast<const uint32_t*>(sp[k]), mt, lane, wu[k]);
+        if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp[k] + 2 * C::PLANE_CHUNK), mt, lane, wl[k]);
+      }
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
-        uint32_t a[4];
-        if constexpr (TGT) unpack_u4l4_raw(wu[ks], wl[ks], a);
-        else unpack_u4_raw(wu[ks], a);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const uint2 b = bqt[(ks * NT + nt) * 32];
-          if (ks & 1) mma_nv(d1[nt], a, b.x, b.y);
-          else mma_nv(d0[nt], a, b.x, b.y);
+        for (int k = 0; k < NP; ++k) {
+          const uint2* bqt = reinterpret_cast<const uint2*>(sp[k] + C::BQ_OFF) + (size_t)bl * KS * NT * 32 + lane;
+          uint32_t a[4];
+          if constexpr (TGT) unpack_u4l4_raw(wu[k][ks], wl[k][ks], a);
+          else unpack_u4_raw(wu[k][ks], a);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint2 b = bqt[(ks * NT + nt) * 32];
+            mma_nv(d[k][ks & 1][nt], a, b.x, b.y);
+          }
         }
       }
-      const float2 sz0 = vps[mt * 16 + g], sz1 = vps[mt * 16 + g + 8];
-      // the value plane of this tile, loaded early (draft; the target reloads later to save registers)
-      uint32_t vw[KS], vwl[KS];
-      if constexpr (!TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp + C::PLANE_CHUNK), mt, lane, vw);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const float2 bb = *reinterpret_cast<const float2*>(bias + (bl * NQ + nt * 4 + t4) * 2);
-        const float r0 = (d0[nt][0] + d0[nt][1]) + (d1[nt][0] + d1[nt][1]);
-        const float r1 = (d0[nt][2] + d0[nt][3]) + (d1[nt][2] + d1[nt][3]);
-        float sv[2], p[2];
-        sv[0] = (r0 + bb.x) * sl2;
-        sv[1] = (TGT ? (r1 + bb.y) : fmaf(r1, 0.0625f, bb.y)) * sl2;
-        const float alpha = softmax_update<2>(st[nt], sv, p);
+        float sv[2 * NP], p[2 * NP];
+        float2 sz[NP][2];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const float* bias = reinterpret_cast<const float*>(sp[k] + C::BIAS_OFF);
+          const float2* vps = reinterpret_cast<const float2*>(sp[k] + C::VP_OFF);
+          const float2 bb = *reinterpret_cast<const float2*>(bias + (bl * NQ + nt * 4 + t4) * 2);
+          sz[k][0] = vps[mt * 16 + g];
+          sz[k][1] = vps[mt * 16 + g + 8];
+          const float r0 = (d[k][0][nt][0] + d[k][0][nt][1]) + (d[k][1][nt][0] + d[k][1][nt][1]);
+          const float r1 = (d[k][0][nt][2] + d[k][0][nt][3]) + (d[k][1][nt][2] + d[k][1][nt][3]);
+          sv[2 * k] = live[k] ? (r0 + bb.x) * sl2 : kNegInf;
+          sv[2 * k + 1] = live[k] ? (TGT ? (r1 + bb.y) : fmaf(r1, 0.0625f, bb.y)) * sl2 : kNegInf;
+        }
+        const float alpha = softmax_update<2 * NP>(st[nt], sv, p);
         if (alpha != 1.0f) rescale<KS, NT>(acc, nt, alpha);
-        st[nt].l += p[0] + p[1];
-        st[nt].z += p[0] * sz0.y + p[1] * sz1.y;
-        const __half h0 = __float2half_rn(p[0] * (sz0.x * kvs)), h1 = __float2half_rn(p[1] * (sz1.x * kvs));
-        st[nt].ps += __half2float(h0) + __half2float(h1);
-        __half* prow = pw + (nt * 8 + 2 * t4) * PSTRIDE;
-        prow[g] = h0;
-        prow[g + 8] = h1;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          if (k > 0 && !live[k]) {  // dead chunk: p' = 0 feeds its (finite) codes
+            __half* prow = pw + k * C::PW_HALVES + (nt * 8 + 2 * t4) * PSTRIDE;
+            prow[g] = prow[g + 8] = __float2half_rn(0.f);
+            continue;
+          }
+          st[nt].l += p[2 * k] + p[2 * k + 1];
+          st[nt].z += p[2 * k] * sz[k][0].y + p[2 * k + 1] * sz[k][1].y;
+          const __half h0 = __float2half_rn(p[2 * k] * (sz[k][0].x * kvs));
+          const __half h1 = __float2half_rn(p[2 * k + 1] * (sz[k][1].x * kvs));
+          st[nt].ps += __half2float(h0) + __half2float(h1);
+          __half* prow = pw + k * C::PW_HALVES + (nt * 8 + 2 * t4) * PSTRIDE;
+          prow[g] = h0;
+          prow[g + 8] = h1;
+        }
       }
       __syncwarp();
-      // ---- P.V: A = V^T codes [channels x tokens] of this token k-step ----
-      uint32_t bpv[NT][2];
-      get_pv_b<NT>(pw, g, t4, bpv);
-      if constexpr (TGT) {
-        load_words<KS>(reinterpret_cast<const uint32_t*>(sp + C::PLANE_CHUNK), mt, lane, vw);
-        load_words<KS>(reinterpret_cast<const uint32_t*>(sp + 3 * C::PLANE_CHUNK), mt, lane, vwl);
-      }
+      // ---- P.V: A = V^T codes [channels x tokens] of this token k-step, chunk by chunk ----
+      uint32_t bpv[NP][NT][2];
 #pragma unroll
-      for (int cm = 0; cm < KS; ++cm) {
-        uint32_t a[4];
-        if constexpr (TGT) unpack_u4l4_raw(vw[cm], vwl[cm], a);
-        else unpack_u4_raw(vw[cm], a);
+      for (int k = 0; k < NP; ++k) get_pv_b<NT>(pw + k * C::PW_HALVES, g, t4, bpv[k]);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) mma_nv(acc[cm][nt], a, bpv[nt][0], bpv[nt][1]);
+      for (int k = 0; k < NP; ++k) {
+        uint32_t vw[KS], vwl[KS];
+        load_words<KS>(reinterpret_cast<const uint32_t*>(sp[k] + C::PLANE_CHUNK), mt, lane, vw);
+        if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp[k] + 3 * C::PLANE_CHUNK), mt, lane, vwl);
+#pragma unroll
+        for (int cm = 0; cm < KS; ++cm) {
+          uint32_t a[4];
+          if constexpr (TGT) unpack_u4l4_raw(vw[cm], vwl[cm], a);
+          else unpack_u4_raw(vw[cm], a);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) mma_nv(acc[cm][nt], a, bpv[k][nt][0], bpv[k][nt][1]);
+        }
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_b[s]);
-    if (++s == S) {
-      s = 0;
-      ph ^= 1;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        if (i0 + k < nchunk) mbar_arrive(&empty_b[stg[k]]);
     }
   }
   }
@@ -961,7 +1029,7 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
   float* q_s = reinterpret_cast<float*>(bqf + C::BQF_WORDS);          // [NQ][HD]
   __half* pw_all = reinterpret_cast<__half*>(q_s + NQ * HD);           // [NCW][PW_HALVES]
   // tma[8] full[8] empty[8] (the row-query kernels have no P transpose buffers)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(C::ROWQ ? reinterpret_cast<__half*>(q_s + NQ * HD) : pw_all + NCW * C::PW_HALVES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(C::ROWQ ? reinterpret_cast<__half*>(q_s + NQ * HD) : pw_all + NCW * C::PW_WARP);
   int* ticket_s = reinterpret_cast<int*>(bars + 24);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -971,10 +1039,10 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
   const int n_main = P.n_main;
   const int n_split_tot = n_main + 2;
   const int nq = min(NQ, P.n_queries - qg * NQ);
-  __half* pw = pw_all + min(warp, NCW - 1) * C::PW_HALVES;
+  __half* pw = pw_all + min(warp, NCW - 1) * C::PW_WARP;
 
   if constexpr (C::QUANT && !C::ROWQ) {
-    for (int i = tid; i < NCW * C::PW_HALVES / 2; i += NTH) reinterpret_cast<uint32_t*>(pw_all)[i] = 0u;
+    for (int i = tid; i < NCW * C::PW_WARP / 2; i += NTH) reinterpret_cast<uint32_t*>(pw_all)[i] = 0u;
   }
   if constexpr (C::QUANT) {
     // per-stage B fragment buffers: the unused query columns stay zero

@@ -111,6 +111,14 @@ __device__ __forceinline__ void unpack_u4l4_raw(uint32_t x, uint32_t y, uint32_t
   a[3] = prmt(od, M, 0x4341u);
 }
 
+// 2^x on the SFU alone (ex2.approx.ftz: one MUFU, 2 ulp; exp2f adds the denormal-range fix-up
+// around it).  ex2(-inf) = +0.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // split an f32 into f16 hi + f16 lo (hi + lo reproduces ~22 bits)
 __device__ __forceinline__ void split_hl(float v, __half& hi, __half& lo) {
   hi = __float2half_rn(v);
