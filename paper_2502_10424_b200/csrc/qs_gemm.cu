@@ -242,6 +242,12 @@ __device__ __forceinline__ void act_prep_row(const float* __restrict__ xr, const
 // stage; the four k-quarters of a tile are summed through shared memory in fixed order at the
 // pair's end.  PDL overlaps the first weight stages with the previous kernel.
 // ---------------------------------------------------------------------------
+#ifndef QS_I4_BREG
+#define QS_I4_BREG 0  // A/B builds: single-row B words held in registers per window (measured -1%: off)
+#endif
+#ifndef QS_I4_CHAINS
+#define QS_I4_CHAINS 2  // A/B builds: MMA accumulator chains per window (power of two)
+#endif
 #ifndef QS_I4_KCH1
 #define QS_I4_KCH1 128  // A/B builds: k-steps per stage of the single-row INT4 config
 #endif
@@ -294,13 +300,43 @@ __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uin
   for (int w = 0; w < C::HKS / WIN; ++w) {
     const int k0 = w * WIN;
     if (k0 >= nks) break;
-    float D2[2][NTC][4];
+    constexpr int NCH = QS_I4_CHAINS;  // independent MMA accumulator chains per window
+    float D2[NCH][NTC][4];
 #pragma unroll
-    for (int c2 = 0; c2 < 2; ++c2)
+    for (int c2 = 0; c2 < NCH; ++c2)
 #pragma unroll
       for (int nt = 0; nt < NTC; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) D2[c2][nt][e] = 0.f;
+    if constexpr (NTC == 1 && CW == 1 && !NOMMA && QS_I4_BREG) {
+      // one activation row: this lane only ever feeds its own slot (g) -> load those GKS k-steps'
+      // B words once per window and select them (or zero) per k-step, instead of a predicated
+      // pair of shared loads + zeroing per k-step
+      uint32_t xb[GKS][2];
+      const uint8_t* brow = bbase + 4 * t4;
+#pragma unroll
+      for (int j = 0; j < GKS; ++j) {
+        const int ks = k0 + my_slot * GKS + j;
+        const bool ok = my_slot < NSLOT && ks < nks;
+        xb[j][0] = ok ? *reinterpret_cast<const uint32_t*>(brow + ks * 32) : 0u;
+        xb[j][1] = ok ? *reinterpret_cast<const uint32_t*>(brow + ks * 32 + 16) : 0u;
+      }
+#pragma unroll
+      for (int sl = 0; sl < NSLOT; ++sl) {
+        const bool mine = my_slot == sl;
+#pragma unroll
+        for (int j = 0; j < GKS; ++j) {
+          const int ks = k0 + sl * GKS + j;
+          if (ks < nks) {
+            const uint4 w4 = wa[(ks >> 2) * 64];
+            const uint32_t wv = (ks & 3) == 0 ? w4.x : (ks & 3) == 1 ? w4.y : (ks & 3) == 2 ? w4.z : w4.w;
+            uint32_t a[4];
+            unpack_u4_raw(wv, a);
+            mma_acc(D2[(sl * GKS + j) % NCH][0], a, mine ? xb[j][0] : 0u, mine ? xb[j][1] : 0u);
+          }
+        }
+      }
+    } else {
 #pragma unroll
     for (int sl = 0; sl < NSLOT; ++sl) {
       const bool mine = my_slot == sl;
@@ -323,18 +359,29 @@ __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uin
               b1 = *reinterpret_cast<const uint32_t*>(brow[nt] + ks * 32 + 16);
             }
             if constexpr (NOMMA)  // diagnostic (dbg bit 2): same operand traffic, no tensor-core op
-              D2[(sl * GKS + j) & 1][nt][0] += __uint_as_float((a[0] ^ a[1] ^ a[2] ^ a[3] ^ b0 ^ b1) & 0x3fffffffu);
+              D2[(sl * GKS + j) % NCH][nt][0] += __uint_as_float((a[0] ^ a[1] ^ a[2] ^ a[3] ^ b0 ^ b1) & 0x3fffffffu);
             else
-              mma_acc(D2[(sl * GKS + j) & 1][nt], a, b0, b1);
+              mma_acc(D2[(sl * GKS + j) % NCH][nt], a, b0, b1);
           }
         }
       }
+    }
     }
 #pragma unroll
     for (int nt = 0; nt < NTC; ++nt) {
       float D[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) D[e] = __fadd_rn(D2[0][nt][e], D2[1][nt][e]);
+      for (int e = 0; e < 4; ++e) {
+        // fixed pairwise order over the chains
+        float t[NCH];
+#pragma unroll
+        for (int c2 = 0; c2 < NCH; ++c2) t[c2] = D2[c2][nt][e];
+#pragma unroll
+        for (int h = NCH / 2; h > 0; h >>= 1)
+#pragma unroll
+          for (int c2 = 0; c2 < h; ++c2) t[c2] = __fadd_rn(t[c2], t[c2 + h]);
+        D[e] = t[0];
+      }
       float vg[2], v8[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
