@@ -30,7 +30,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 LLAMA2_7B = dict(num_layers=32, num_heads=32, num_kv_heads=32, head_dim=128, hidden=4096, mlp_hidden=11008, vocab=32000)
+LLAMA31_8B = dict(num_layers=32, num_heads=32, num_kv_heads=8, head_dim=128, hidden=4096, mlp_hidden=14336, vocab=128256)
 METRIC = "decode tokens/sec @128K ctx + speedup vs FP16 AR; attn HBM GB/s vs peak"
+# BASELINE.json configs; config 3 is the headline (the default), the others are extra profile lines
+WORKLOADS = {
+    "config3": dict(model=LLAMA2_7B, shape="llama2_7b", context=131072, batch=1,
+                    name="config3: LWM-Text-Chat-128k shape (Llama-2-7B arch) random init, 128K ctx, batch 1 per GPU, "
+                         "gamma 4, greedy, mode=both (INT4 KV + INT4 draft weights)"),
+    "config2": dict(model=LLAMA2_7B, shape="llama2_7b", context=32768, batch=1,
+                    name="config2: Llama-2-7B shape random init, 32K ctx, batch 1 per GPU, gamma 4, greedy, mode=both"),
+    "config4": dict(model=LLAMA31_8B, shape="llama31_8b", context=131072, batch=8,
+                    name="config4: Llama-3.1-8B shape (GQA, 8 KV heads) random init, 128K ctx, batch 8 partitioned "
+                         "batch-wise over the GPUs, gamma 4, greedy, mode=both"),
+}
 
 
 def parse():
@@ -39,7 +51,12 @@ def parse():
     p.add_argument("--steps", type=int, default=48)
     p.add_argument("--warmup", type=int, default=4)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--context", type=int, default=131072)
+    p.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
+    p.add_argument("--context", type=int, default=0, help="override the workload's context")
+    p.add_argument("--batch", type=int, default=0, help="override the workload's total batch (all ranks)")
+    p.add_argument("--weights", default="reference", choices=["reference", "device"],
+                   help="reference: the reference init_weights stream replayed bit-exactly (initstream); "
+                        "device: torch.randn on the GPU (same recipe, not the reference's draws)")
     p.add_argument("--gamma", type=int, default=4)
     p.add_argument("--layers", type=int, default=32)
     p.add_argument("--seed", type=int, default=0)
@@ -115,75 +132,186 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def build_workload(args, dev_index: int):
-    import numpy as np
+def resolve(args):
+    """Workload dict with the command-line overrides applied (context, total batch, depth)."""
+    wl = dict(WORKLOADS[args.workload])
+    wl["model"] = dict(wl["model"], num_layers=args.layers)
+    if args.context:
+        wl["context"] = args.context
+    if args.batch:
+        wl["batch"] = args.batch
+    return wl
+
+
+def weight_source(args, wl, geo):
+    """Yields ("layers.i.<mat>" | "embedding" | "lm_head", f32 CUDA tensor) in the reference's
+    init_weights draw order (Q/model.py:89-117).  ``reference``: the numpy PCG64 stream replayed
+    bit-exactly on host threads from recorded per-matrix states (paper_2502_10424_b200/initstream);
+    ``device``: the same recipe (N(0,1)/sqrt(fan_in), unscaled embedding) drawn by torch on the GPU."""
+    import torch
+
+    from paper_2502_10424_b200 import initstream
+
+    m = wl["model"]
+    plan = initstream.draw_plan(m["num_layers"], m["hidden"], m["num_kv_heads"] * m["head_dim"], m["mlp_hidden"],
+                                m["vocab"])
+    if args.weights == "reference":
+        full = initstream.draw_plan(32, m["hidden"], m["num_kv_heads"] * m["head_dim"], m["mlp_hidden"], m["vocab"])
+        states = initstream.load_states(32, m["hidden"], m["num_kv_heads"] * m["head_dim"], m["mlp_hidden"],
+                                        m["vocab"], args.seed)
+        if states is None:
+            raise SystemExit(f"no recorded init stream for {wl['shape']} seed {args.seed}: "
+                             f"run tools/make_init_states.py {wl['shape']} {args.seed} (or --weights device)")
+        # a shallower bench (--layers) keeps the first layers' draws and the embedding / lm_head of the full model
+        idx = {name: i for i, (name, *_) in enumerate(full)}
+        sel = [full[idx[name]] for name, *_ in plan]
+        st = [states[idx[name]] for name, *_ in plan]
+        for name, arr in initstream.stream_matrices(sel, st):
+            yield name, torch.from_numpy(arr).cuda(non_blocking=False)
+    else:
+        gen = torch.Generator(device="cuda").manual_seed(args.seed)
+        for name, rows, cols, scaled in plan:
+            t = torch.randn(rows, cols, device="cuda", generator=gen)
+            yield name, (t / math.sqrt(rows) if scaled else t)
+
+
+def build_weights(args, wl, geo):
+    """Packed fp16 (target) and INT4 g32 (draft) DeviceWeights + f32 embedding / lm_head, streamed one
+    layer at a time so only packed copies stay resident.  Returns (fw, qw, emb, head)."""
     import torch
 
     from paper_2502_10424_b200 import _lib
-    from paper_2502_10424_b200._prefill import run_prefill
-    from paper_2502_10424_b200.cache import CacheLayout, FpKVCache, HierarchicalKVCache
-    from paper_2502_10424_b200.runtime import DeviceWeights, Geometry, PackedLinear, rope_table
+    from paper_2502_10424_b200.runtime import DeviceWeights, PackedLinear, rope_table
 
-    cfg = dict(LLAMA2_7B)
-    cfg["num_layers"] = args.layers
-    S = args.context
-    margin = 4096
-    geo = Geometry(cfg["num_layers"], cfg["hidden"], cfg["num_heads"], cfg["num_kv_heads"], cfg["head_dim"],
-                   cfg["mlp_hidden"], cfg["vocab"], S + margin)
-    d, m, V = geo.hidden, geo.mlp_hidden, geo.vocab
-    gen = torch.Generator(device="cuda").manual_seed(args.seed + 1000 * dev_index)
-
-    def mat(r, c):
-        # N(0,1)/sqrt(fan_in), the reference's init recipe (Q/model.py:94-95), drawn on device
-        return torch.randn(r, c, device="cuda", generator=gen) / math.sqrt(r)
-
-    t0 = time.time()
-    emb = torch.randn(V, d, device="cuda", generator=gen)
-    head = mat(d, V)
-    ones = torch.ones(d, device="cuda")
-    rope = rope_table(geo.head_dim, geo.rope_base, geo.max_positions)
-    G = 128
-    lay = CacheLayout(geo.num_layers, geo.num_heads, geo.head_dim, G)
-    hcache = HierarchicalKVCache(lay, max_tokens=S + margin)
-    fcache = FpKVCache(geo.num_layers, geo.nk, capacity=S + margin, head_dim=geo.head_dim)
     f_layers, q_layers = [], []
-
-    def layers():
-        for _ in range(geo.num_layers):
-            mats = {"wq": mat(d, d), "wk": mat(d, d), "wv": mat(d, d), "wo": mat(d, d), "w_gate": mat(d, m),
-                    "w_up": mat(d, m), "w_down": mat(m, d)}
-            qkv = torch.cat([mats["wq"], mats["wk"], mats["wv"]], dim=1)
-            f_layers.append(dict(qkv=PackedLinear.f16(qkv), o=PackedLinear.f16(mats["wo"]),
-                                 gu=PackedLinear.f16_pair(mats["w_gate"], mats["w_up"]), down=PackedLinear.f16(mats["w_down"])))
-            q_layers.append(dict(qkv=PackedLinear.int4(qkv, 32), o=PackedLinear.int4(mats["wo"], 32),
-                                 gu=PackedLinear.int4_pair(mats["w_gate"], mats["w_up"], 32),
-                                 down=PackedLinear.int4(mats["w_down"], 32)))
+    cur = {}
+    emb = head = None
+    for name, t in weight_source(args, wl, geo):
+        if name == "embedding":
+            emb = t
+            continue
+        if name == "lm_head":
+            head = t
+            continue
+        cur[name.split(".")[-1]] = t
+        if len(cur) == 7:
+            qkv = torch.cat([cur["wq"], cur["wk"], cur["wv"]], dim=1)
+            f_layers.append(dict(qkv=PackedLinear.f16(qkv), o=PackedLinear.f16(cur["wo"]),
+                                 gu=PackedLinear.f16_pair(cur["w_gate"], cur["w_up"]),
+                                 down=PackedLinear.f16(cur["w_down"])))
+            q_layers.append(dict(qkv=PackedLinear.int4(qkv, 32), o=PackedLinear.int4(cur["wo"], 32),
+                                 gu=PackedLinear.int4_pair(cur["w_gate"], cur["w_up"], 32),
+                                 down=PackedLinear.int4(cur["w_down"], 32)))
             del qkv
-            mats["attn_norm"] = ones
-            mats["mlp_norm"] = ones
-            yield mats
-
-    prompt = torch.from_numpy(np.random.default_rng(args.seed + 1).integers(0, V, size=S).astype(np.int32)).cuda()
-
-    def sink(l, k, v):
-        hcache.load_prefill_layer(l, k, v)
-        fcache.load_prefill_layer(l, k, v)
-
-    from torch.nn.attention import SDPBackend, sdpa_kernel
-
-    with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.CUDNN_ATTENTION]):
-        logits = run_prefill(geo, prompt, emb, layers(), ones, head, rope, sink, dtype=torch.float16)
-    hcache.finish_prefill(S)
-    fcache.finish_prefill(S)
+            cur = {}
+    ones = torch.ones(geo.hidden, device="cuda")
+    rope = rope_table(geo.head_dim, geo.rope_base, geo.max_positions)
     common = dict(embedding=emb, attn_norms=[ones] * geo.num_layers, mlp_norms=[ones] * geo.num_layers,
                   final_norm=ones, rope=rope)
     fw = DeviceWeights(geo, f_layers, PackedLinear.f16(head), wmode=_lib.W_F16, **common)
     qw = DeviceWeights(geo, q_layers, PackedLinear.int4(head, 32), wmode=_lib.W_INT4, **common)
-    del head
     torch.cuda.synchronize()
-    first = int(torch.argmax(logits).item())
-    setup_s = time.time() - t0
-    return geo, fw, qw, hcache, fcache, first, setup_s
+    return fw, qw, emb, head
+
+
+def prompts_for(args, wl, seqs):
+    """Uniform random prompt tokens; sequence b of the job uses seed + 1 + b (b = 0: the reference
+    CLI's seed + 1, Q/cli.py:137), so a sequence's prompt does not depend on the GPU count."""
+    import numpy as np
+
+    V = wl["model"]["vocab"]
+    return [np.random.default_rng(args.seed + 1 + b).integers(0, V, size=wl["context"]).astype(np.int32) for b in seqs]
+
+
+def prefill_into(args, wl, geo, fw, head, prompts, sinks):
+    """Prompt prefill (setup, untimed) with torch/cuBLAS/SDPA; ``sinks[b](layer, k, v)`` receive
+    sequence b's K/V.  The f32 weight matrices are re-streamed per pass (they are not kept)."""
+    import torch
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+
+    from paper_2502_10424_b200._prefill import run_prefill
+
+    firsts = []
+    for b, p in enumerate(prompts):
+        def layers():
+            cur = {}
+            for name, t in weight_source(args, wl, geo):
+                if not name.startswith("layers."):
+                    continue
+                cur[name.split(".")[-1]] = t
+                if len(cur) == 7:
+                    cur["attn_norm"] = cur["mlp_norm"] = fw.final_norm
+                    yield cur
+                    cur = {}
+
+        ids = torch.from_numpy(p).cuda()
+        with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.CUDNN_ATTENTION]):
+            logits = run_prefill(geo, ids, fw.embedding, layers(), fw.final_norm, head, fw.rope, sinks[b],
+                                 dtype=torch.float16)
+        firsts.append(int(torch.argmax(logits).item()))
+    torch.cuda.synchronize()
+    return firsts
+
+
+def build_workload(args, wl, seqs):
+    """Weights, the hierarchical store of this rank's sequences (prefilled), the fp16 baseline cache
+    when both fit (else None: built later by ``fp16_cache``) and the first decode tokens."""
+    import torch
+
+    from paper_2502_10424_b200.cache import CacheLayout, FpKVCache, HierarchicalKVCache
+    from paper_2502_10424_b200.runtime import Geometry
+
+    m = wl["model"]
+    S = wl["context"]
+    margin = 4096
+    geo = Geometry(m["num_layers"], m["hidden"], m["num_heads"], m["num_kv_heads"], m["head_dim"], m["mlp_hidden"],
+                   m["vocab"], S + margin)
+    t0 = time.time()
+    fw, qw, emb, head = build_weights(args, wl, geo)
+    t_w = time.time() - t0
+    B = len(seqs)
+    lay = CacheLayout(geo.num_layers, geo.num_heads, geo.head_dim, 128, num_kv_heads=geo.num_kv_heads)
+    hcache = HierarchicalKVCache(lay, max_tokens=S + margin, batch=B)
+    # fp16 baseline cache alongside when it fits (config 3: 64 GiB + 34 GiB store), else after the spec modes
+    fp_bytes = 2 * 2 * B * geo.num_layers * geo.nk * (S + margin)
+    free, _ = torch.cuda.mem_get_info()
+    fcache = None
+    if fp_bytes < free - (24 << 30):
+        fcache = FpKVCache(geo.num_layers, geo.nk, capacity=S + margin, head_dim=geo.head_dim, batch=B)
+    prompts = prompts_for(args, wl, seqs)
+
+    def sink(b):
+        def f(l, k, v):
+            hcache.load_prefill_layer(l, k, v, seq=b)
+            if fcache is not None:
+                fcache.load_prefill_layer(l, k, v, seq=b)
+        return f
+
+    firsts = prefill_into(args, wl, geo, fw, head, prompts, [sink(b) for b in range(B)])
+    for b in range(B):
+        hcache.finish_prefill(S, seq=b)
+        if fcache is not None:
+            fcache.finish_prefill(S, seq=b)
+    setup = {"weights_s": t_w, "prefill_s": time.time() - t0 - t_w, "weights": args.weights}
+    return geo, fw, qw, head, hcache, fcache, firsts, prompts, setup
+
+
+def fp16_cache(args, wl, geo, fw, head, prompts):
+    """The FP16-AR baseline cache of this rank's sequences, prefilled in its own pass (config 4:
+    the quantised store and the fp16 cache of 8 x 128K sequences do not fit one GPU together)."""
+    import torch
+
+    from paper_2502_10424_b200.cache import FpKVCache
+
+    S = wl["context"]
+    B = len(prompts)
+    fcache = FpKVCache(geo.num_layers, geo.nk, capacity=S + 4096, head_dim=geo.head_dim, batch=B)
+    firsts = prefill_into(args, wl, geo, fw, head, prompts,
+                          [lambda l, k, v, b=b: fcache.load_prefill_layer(l, k, v, seq=b) for b in range(B)])
+    for b in range(B):
+        fcache.finish_prefill(S, seq=b)
+    torch.cuda.synchronize()
+    return fcache, firsts
 
 
 def time_kernel(fn, iters: int = 21):
@@ -207,44 +335,98 @@ def time_kernel(fn, iters: int = 21):
     return statistics.median(s.elapsed_time(e) for s, e in ev) / 1e3
 
 
-def kernel_roofline(geo, fw, qw, hcache, fcache, peak):
-    """Isolated timings of the hot kernels at the bench context (inputs >> L2)."""
+def time_graph(fns, reps: int = 5):
+    """Mean device time per call of the launches ``fns`` captured back to back in one CUDA graph
+    (the decode loop's own launch mode, PDL included): the steady-state duration of a kernel inside
+    a forward, where its prologue overlaps the previous launch."""
+    import torch
+
+    for f in fns:
+        f()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for f in fns:
+            f()
+    g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / 1e3 / (reps * len(fns))
+
+
+def kernel_roofline(geo, fw, qw, hcache, peak):
+    """Per-launch timings of the hot kernels at the bench context over this rank's sequences.
+    Attention: isolated launches (each streams 0.1-9 GB >> the 126 MB L2).  Linear layers: the 32
+    layers' matrices launched back to back from a graph (distinct weights, > L2), i.e. the in-forward
+    steady state; the isolated single-launch time is reported next to it."""
     import torch
 
     from paper_2502_10424_b200 import _lib
     from paper_2502_10424_b200.runtime import Runner
 
     out = {}
+    B = hcache.batch
     G = hcache.layout.group_size
     kv = geo.nk
     nq_tok = hcache.quantized_token_count
     nfp = hcache.fp1_len + hcache.fp2_len + 1
-    run = Runner(geo, hcache, max_cols=5)
+    run = Runner(geo, hcache, max_cols=5 * B)
     run.q.normal_()
     s = _lib.stream_ptr()
     per_tok = {"draft": kv * 1.0 + 8.0 * kv / G + 8.0 * math.ceil(kv / G),
                "target": kv * 2.0 + 8.0 * kv / G + 8.0 * math.ceil(kv / G)}
     for name, view, T in (("attn_draft", _lib.VIEW_DRAFT, 1), ("attn_verify", _lib.VIEW_TARGET, 5)):
         dt = time_kernel(lambda: run._attention(0, view, T, 0, s))
-        algo = nq_tok * per_tok["draft" if view == _lib.VIEW_DRAFT else "target"] + (nfp + T) * kv * 4.0 + T * geo.nq * 8.0
-        out[name] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak}
-    frun = Runner(geo, fcache, max_cols=1)
-    frun.q.normal_()
-    n = fcache.seq_len + 1
-    dt = time_kernel(lambda: frun._attention(0, _lib.VIEW_FP16, 1, 0, s))
-    algo = n * kv * 4.0 + geo.nq * 8.0
-    out["attn_fp16"] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak}
-    for name, w in (("gemv_f16_down", fw.layers[0]["down"]), ("gemv_int4_down", qw.layers[0]["down"]),
-                    ("gemv_f16_lm_head", fw.lm_head)):
+        algo = B * (nq_tok * per_tok["draft" if view == _lib.VIEW_DRAFT else "target"] + (nfp + T) * kv * 4.0
+                    + T * geo.nq * 8.0)
+        out[name] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak,
+                     "sequences": B}
+    L = len(fw.layers)
+    for name, ws in (("gemv_f16_down", [lw["down"] for lw in fw.layers]),
+                     ("gemv_int4_down", [lw["down"] for lw in qw.layers]),
+                     ("gemv_int4_qkv", [lw["qkv"] for lw in qw.layers]),
+                     ("gemv_int4_gate_up", [lw["gu"] for lw in qw.layers]),
+                     ("gemv_f16_lm_head", [fw.lm_head])):
+        w = ws[0]
         src = (run.hh, run.hs) if w.K == geo.mlp_hidden else (run.xh, run.xs)
         src[0].normal_()
         src[1].normal_()
-        y = run.x if w.N == geo.hidden else run.logits
-        dt = time_kernel(lambda: run._linear(w, src, y, 1, _lib.EPI_STORE, stream=s))
+        y = run.x if w.N == geo.hidden else (run.logits if w.N == geo.vocab else None)
+        epi = _lib.EPI_STORE if y is not None else _lib.EPI_SILU_MUL if "gate" in name else _lib.EPI_QKV
+        kw = dict(yh=(run.hh, run.hs)) if epi == _lib.EPI_SILU_MUL else {}
+        if epi == _lib.EPI_SILU_MUL:
+            src = (run.xh, run.xs)
+        fns = [(lambda w_=w_, li=li: run._linear(w_, src, y, 1, epi, layer=li, stream=s, **kw)) for li, w_ in enumerate(ws)]
+        dt_iso = time_kernel(fns[0])
+        dt = time_graph(fns) if len(fns) > 1 else dt_iso
         algo = w.algorithmic_bytes() + 2.0 * w.K + 4.0 * w.N
-        out[name] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak}
+        out[name] = {"us": dt * 1e6, "us_isolated": dt_iso * 1e6, "bytes": algo, "gbs": algo / dt / 1e9,
+                     "frac": algo / dt / 1e9 / peak, "frac_isolated": algo / dt_iso / 1e9 / peak,
+                     "timing": f"graph of {len(fns)} launches (layers' own matrices)" if len(fns) > 1 else "isolated"}
     torch.cuda.synchronize()
     return out
+
+
+def kernel_fp16(geo, fcache, peak):
+    import torch
+
+    from paper_2502_10424_b200 import _lib
+    from paper_2502_10424_b200.runtime import Runner
+
+    B = fcache.batch
+    frun = Runner(geo, fcache, max_cols=B)
+    frun.q.normal_()
+    s = _lib.stream_ptr()
+    n = fcache.seq_len + 1
+    dt = time_kernel(lambda: frun._attention(0, _lib.VIEW_FP16, 1, 0, s))
+    algo = B * (n * geo.nk * 4.0 + geo.nq * 8.0)
+    torch.cuda.synchronize()
+    return {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak, "sequences": B}
 
 
 def _binom_ci(acc: int, n: int) -> list:
@@ -345,35 +527,37 @@ def measure_ar(fw, cache, first, steps, warmup, use_graphs):
 # ---------------------------------------------------------------------------
 
 
-def cpu_baseline(context: int, layers: int, sample_layers: int = 8, seg_tokens: int = 16384):
-    """Per-token target-view AR decode time of the reference algorithm at Llama-2-7B shape,
-    timed on a bounded sample (~10 s on 16 host cores): ``sample_layers`` full decoder layers
-    at the full context -- oracle merged_attention (the reference's running f64 merge) over a
-    dequantised f32 view of ``context`` tokens, fed as ``seg_tokens``-token segments, plus the
-    layer's f32 projections -- scaled to ``layers`` layers, plus the lm_head GEMV."""
+def cpu_sample(geo: dict, context: int, nlayers: int, seg_tokens: int = 16384):
+    """Wall time of ``nlayers`` full decoder layers of ONE target-view decode token of the
+    reference algorithm (the oracle port, oracle/qs_oracle.py) at ``context`` tokens:
+    merged_attention (the reference's running f64 merge, Q/model.py:176-195) over the dequantised
+    f32 target view, fed as ``seg_tokens``-token segments (GQA: each KV head repeated r times, as
+    the oracle restates it), plus the layer's f32 projections.  Returns (seconds, lm_head seconds)."""
     import numpy as np
 
     from oracle import qs_oracle as O
 
-    cores = os.cpu_count() or 1
-    H, hd, d, m, V, G = 32, 128, 4096, 11008, 32000, 128
+    H, Hk, hd, d, m, V, G = (geo["num_heads"], geo["num_kv_heads"], geo["head_dim"], geo["hidden"], geo["mlp_hidden"],
+                             geo["vocab"], 128)
+    kv = Hk * hd
     rng = np.random.default_rng(0)
-    blk = O.quantize_kv_block(O.Layout(1, H, hd, G), rng.standard_normal((G, d)).astype(np.float32),
-                              rng.standard_normal((G, d)).astype(np.float32))
-    kb, vb = O.dequant_kv_block(O.Layout(1, H, hd, G), blk, "target")
+    blk = O.quantize_kv_block(O.Layout(1, Hk, hd, G), rng.standard_normal((G, kv)).astype(np.float32),
+                              rng.standard_normal((G, kv)).astype(np.float32))
+    kb, vb = O.dequant_kv_block(O.Layout(1, Hk, hd, G), blk, "target")
     seg_tokens = min(seg_tokens, context)
-    ks = np.tile(kb, (seg_tokens // G, 1)).reshape(-1, H, hd)
-    vs = np.tile(vb, (seg_tokens // G, 1)).reshape(-1, H, hd)
-    nseg = max(1, context // seg_tokens)
-    segs = [(ks, vs)] * nseg  # the context as segments (bounded memory; same work per token)
+    ks = np.tile(kb, (seg_tokens // G, 1)).reshape(-1, Hk, hd)
+    vs = np.tile(vb, (seg_tokens // G, 1)).reshape(-1, Hk, hd)
+    if Hk != H:
+        ks, vs = np.repeat(ks, H // Hk, axis=1), np.repeat(vs, H // Hk, axis=1)
+    segs = [(ks, vs)] * max(1, context // seg_tokens)  # the context as segments (bounded memory)
     q = rng.standard_normal((H, hd)).astype(np.float32)
-    mats = [rng.standard_normal((d, n), dtype=np.float32) for n in (3 * d, d)] + [
-        rng.standard_normal((d, 2 * m), dtype=np.float32), rng.standard_normal((m, d), dtype=np.float32)]
+    mats = [rng.standard_normal((d, H * hd + 2 * kv), dtype=np.float32), rng.standard_normal((d, d), dtype=np.float32),
+            rng.standard_normal((d, 2 * m), dtype=np.float32), rng.standard_normal((m, d), dtype=np.float32)]
     head = rng.standard_normal((d, V), dtype=np.float32)
     x = rng.standard_normal(d).astype(np.float32)
     xm = rng.standard_normal(m).astype(np.float32)
     t0 = time.perf_counter()
-    for _ in range(sample_layers):
+    for _ in range(nlayers):
         O.merged_attention(q, segs, 1.0 / np.sqrt(hd))
         _ = x @ mats[0]
         _ = x @ mats[1]
@@ -382,41 +566,83 @@ def cpu_baseline(context: int, layers: int, sample_layers: int = 8, seg_tokens: 
     t_layers = time.perf_counter() - t0
     t0 = time.perf_counter()
     _ = x @ head
-    t_head = time.perf_counter() - t0
-    per_tok = t_layers * layers / sample_layers + t_head
+    return t_layers, time.perf_counter() - t0
+
+
+def cpu_baseline(context: int, layers: int, geo: dict, sample_layers: int = 2):
+    """The reference algorithm's target-view decode rate on this host: ``sample_layers`` of the
+    ``layers`` decoder layers timed at the full context, extrapolated to one whole token."""
+    cores = os.cpu_count() or 1
+    t_l, t_h = cpu_sample(geo, context, sample_layers)
+    per_tok = t_l * layers / sample_layers + t_h
     return {"value": 1.0 / per_tok, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": (f"oracle target-view decode at {nseg * seg_tokens} tokens: {sample_layers} of {layers} decoder layers "
-                       f"(merged_attention over the dequantised view + f32 projections) timed and scaled x"
-                       f"{layers / sample_layers:.0f}, + lm_head; per-token time {per_tok:.2f} s; sample wall "
-                       f"{t_layers + t_head:.1f} s"),
-            "per_token_s": per_tok}
+            "sample": (f"oracle (NumPy restatement of the reference) target-view decode of one token at {context} "
+                       f"tokens: {sample_layers} of {layers} decoder layers timed ({t_l:.1f} s) and scaled "
+                       f"x{layers / sample_layers:g}, + lm_head; extrapolated per-token time {per_tok:.1f} s"),
+            "per_token_s": per_tok, "extrapolated": True}
 
 
 def reference_arm(args):
+    """--impl reference: the reference's CPU algorithm (the oracle port; the pure-Python reference
+    package does not travel to the GPU box) on this box's host cores, on the b200 arm's config.
+    Each step times ONE full decoder layer of one decode token at the full context (a bounded
+    sample: ms_per_step is that measured time, so ms_per_step x steps is the run's wall time);
+    value = the per-token rate those layer times extrapolate to (x layers, + lm_head)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    wl = resolve(args)
     t0 = time.time()
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        pass
-    vals = []
-    cb = None
-    for _ in range(max(1, min(args.steps, 3))):
-        cb = cpu_baseline(args.context, args.layers)
-        vals.append(cb["value"])
-    v = statistics.median(vals)
-    cb["value"] = v
-    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": len(vals),
-            "warmup": 0, "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64/f32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "config3: Llama-2-7B shape, 128K ctx, batch 1, gamma 4 (CPU oracle sample)",
-                       "context": args.context, "layers": args.layers},
+    for _ in range(min(args.warmup, 1)):
+        cpu_sample(wl["model"], wl["context"], 1)
+    per_layer, heads = [], []
+    for _ in range(args.steps):
+        t_l, t_h = cpu_sample(wl["model"], wl["context"], 1)
+        per_layer.append(t_l)
+        heads.append(t_h)
+    t_layer = statistics.median(per_layer)
+    per_tok = t_layer * args.layers + statistics.median(heads)
+    v = 1.0 / per_tok
+    cores = os.cpu_count() or 1
+    cb = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
+          "sample": (f"per step: one decoder layer of one target-view decode token at {wl['context']} tokens "
+                     f"(median {t_layer:.2f} s over {args.steps} steps), extrapolated x{args.layers} layers + lm_head "
+                     f"= {per_tok:.1f} s per token"),
+          "extrapolated": True}
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * statistics.mean(per_layer), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 attention / f32 projections", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": wl["name"], "context": wl["context"], "layers": args.layers, "gamma": args.gamma,
+                       "batch_total": wl["batch"]},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.time() - t0}
     print(json.dumps(line))
 
 
 # ---------------------------------------------------------------------------
+
+
+def lib_digest() -> str:
+    import hashlib
+
+    from paper_2502_10424_b200 import _lib
+
+    with open(_lib.lib_path(), "rb") as f:
+        return hashlib.md5(f.read()).hexdigest()
+
+
+def measured_traffic():
+    """ncu DRAM bytes (read + write) per draft-attention launch, recorded by profiles/collect_traffic.sh
+    for a specific build of libqsb200.so; null when it was measured on a different build."""
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        t = json.load(open(tpath))
+    except Exception:
+        return None, "no ncu capture (profiles/traffic.json)"
+    if t.get("lib_md5") != lib_digest():
+        return None, f"ncu capture is of build {t.get('lib_md5')}, not this build"
+    return t.get("attn_draft_bytes_per_launch"), f"ncu --set full capture of this build ({t.get('when', '')})"
 
 
 def main():
@@ -426,6 +652,8 @@ def main():
         return
     import torch
     import torch.distributed as dist
+
+    from paper_2502_10424_b200.parallel import partition
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -437,10 +665,16 @@ def main():
 
     __graft_entry__.build()
     peak, peak_kind = load_peaks()
-    geo, fw, qw, hcache, fcache, first, setup_s = build_workload(args, rank)
+    wl = resolve(args)
+    # config 4: the job's sequences partitioned batch-wise over the ranks (no data-path collective);
+    # configs 2/3: one sequence per GPU (replicas)
+    seqs = list(partition(wl["batch"], world, rank)) if wl["batch"] > 1 else [rank]
+    geo, fw, qw, head_w, hcache, fcache, firsts, prompts, setup = build_workload(args, wl, seqs)
     use_graphs = not args.no_graphs
     modes = args.modes.split(",")
-    kr = kernel_roofline(geo, fw, qw, hcache, fcache, peak)
+    kr = kernel_roofline(geo, fw, qw, hcache, peak)
+    if fcache is not None:
+        kr["attn_fp16"] = kernel_fp16(geo, fcache, peak)
     if args.profile_kernels:
         print(json.dumps({"kernels": kr}))
         return
@@ -452,47 +686,58 @@ def main():
 
     res = {}
     clocks = ClockSampler(local)
+    t_timed = 0.0
     with clocks:
         barrier()
-        t_all = time.time()
+        t0 = time.time()
         if "both" in modes:
-            res["both"] = measure_spec(geo, fw, qw, hcache, first, args.gamma, args.steps, args.warmup, use_graphs,
+            res["both"] = measure_spec(geo, fw, qw, hcache, firsts, args.gamma, args.steps, args.warmup, use_graphs,
                                        weight_mode="int4", int4_bytes=qw.algorithmic_bytes())
         if "kv_only" in modes:
-            res["kv_only"] = measure_spec(geo, fw, fw, hcache, first, args.gamma, args.steps, args.warmup, use_graphs,
+            res["kv_only"] = measure_spec(geo, fw, fw, hcache, firsts, args.gamma, args.steps, args.warmup, use_graphs,
                                           weight_mode="fp")
-        if "fp16_ar" in modes:
-            res["fp16_ar"] = measure_ar(fw, fcache, first, args.steps, args.warmup, use_graphs)
         barrier()
-        wall = time.time() - t_all
+        t_timed += time.time() - t0
+    if "fp16_ar" in modes:
+        ffirst = firsts
+        if fcache is None:
+            del hcache
+            torch.cuda.empty_cache()
+            fcache, ffirst = fp16_cache(args, wl, geo, fw, head_w, prompts)
+            kr["attn_fp16"] = kernel_fp16(geo, fcache, peak)
+        with clocks:
+            barrier()
+            t0 = time.time()
+            res["fp16_ar"] = measure_ar(fw, fcache, ffirst, args.steps, args.warmup, use_graphs)
+            barrier()
+            t_timed += time.time() - t0
     head = res.get("both") or res.get("kv_only")
     # whole-job throughput: tokens emitted on all ranks / the slowest rank's device time
     emitted = head["tok_s"] * head["ms_per_step"] * args.steps / 1e3
     e2e_s = emitted / head["e2e_tok_s"]
-    vals = torch.tensor([head["ms_per_step"], e2e_s, emitted], dtype=torch.float64, device="cuda")
+    ar = res.get("fp16_ar")
+    ar_tok = ar["tok_s"] * ar["ms_per_step"] * args.steps / 1e3 if ar else 0.0
+    vals = torch.tensor([head["ms_per_step"], e2e_s, ar["ms_per_step"] if ar else 0.0, emitted, ar_tok],
+                        dtype=torch.float64, device="cuda")
     if world > 1:
         t = vals.clone()
-        dist.all_reduce(t[:2], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         s2 = vals.clone()
         dist.all_reduce(s2, op=dist.ReduceOp.SUM)
         ms = float(t[0])
-        value = float(s2[2]) / (ms * args.steps / 1e3)
-        e2e = float(s2[2]) / float(t[1])
+        value = float(s2[3]) / (ms * args.steps / 1e3)
+        e2e = float(s2[3]) / float(t[1])
+        ar_job = float(s2[4]) / (float(t[2]) * args.steps / 1e3) if ar else None
     else:
         ms, value, e2e = head["ms_per_step"], head["tok_s"], head["e2e_tok_s"]
+        ar_job = ar["tok_s"] if ar else None
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return
-    ar = res.get("fp16_ar")
     dom = kr["attn_draft"]
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("attn_draft_bytes_per_launch")
-        except Exception:
-            traffic = None
-    cb = cpu_baseline(args.context, args.layers) if world == 1 or rank == 0 else None
+    traffic, traffic_src = measured_traffic()
+    cb = cpu_baseline(wl["context"], args.layers, geo=wl["model"])
+    B = wl["batch"]
     line = {
         "metric": METRIC,
         "value": value,
@@ -505,25 +750,31 @@ def main():
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f16 (KV int4/int8 planes, INT4 draft weights), f32 accumulate",
-        "data": "synthetic (random-init weights, uniform random prompt tokens)",
-        "config": {"workload": "config3: Llama-2-7B shape random init, 128K ctx, batch 1 per GPU, gamma 4, greedy, "
-                               "mode=both (INT4 KV + INT4 draft weights)",
-                   "context": args.context, "layers": args.layers, "gamma": args.gamma,
+        "data": (f"synthetic: random-init weights ({'the reference init_weights stream, seed %d, replayed bit-exactly' % args.seed if args.weights == 'reference' else 'torch.randn on device, the reference recipe'}), "
+                 f"uniform random prompt tokens (seed {args.seed}+1+b)"),
+        "config": {"workload": wl["name"], "context": wl["context"], "layers": args.layers, "gamma": args.gamma,
+                   "batch_total": B, "batch_per_gpu": len(seqs),
                    "l2": "working set per forward (GBs) >> 126 MB L2; no flush needed",
-                   "parallelism": f"replicas x{world} (one sequence per GPU)", "cuda_graphs": use_graphs},
-        "speedup_vs_fp16_ar": (value / world) / ar["tok_s"] if ar else None,
+                   "parallelism": (f"batch partition x{world} (no data-path collective)" if B > 1
+                                   else f"replicas x{world} (one sequence per GPU)"),
+                   "cuda_graphs": use_graphs},
+        "speedup_vs_fp16_ar": value / ar_job if ar_job else None,
+        "fp16_ar_tok_s_job": ar_job,
         "modes": res,
         "kernels": kr,
         "roofline": {"bound": "hbm", "kernel": "attn_draft (K2, upper INT4 plane, split-K)", "achieved": dom["gbs"],
                      "peak": peak, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, burst copy)", "unit": "GB/s",
-                     "frac": dom["gbs"] / peak, "traffic": traffic, "algorithmic_bytes_per_launch": dom["bytes"]},
+                     "frac": dom["gbs"] / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": dom["bytes"]},
         "cpu_baseline": cb,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": head["h2d_bytes_per_step"],
-                "d2h_bytes_per_step": head["d2h_bytes_per_step"]},
+                "d2h_bytes_per_step": head["d2h_bytes_per_step"],
+                "path": "SpeculativeDecoder.decode (public API) over the same cycles as value"},
         "gpu_launches": head["launches"],
         "clocks": clocks.summary(),
-        "setup_s": setup_s,
-        "timed_wall_s": wall,
+        "setup": setup,
+        "timed_wall_s": t_timed,
+        "lib_md5": lib_digest(),
     }
     print(json.dumps(line))
     if world > 1:

@@ -97,6 +97,10 @@ EXPORTED = tuple(_SIGS)
 _lib = None
 
 
+def lib_path() -> str:
+    return LIB_PATH
+
+
 def load() -> C.CDLL:
     """Load libqsb200.so (raises if it was not built)."""
     global _lib
