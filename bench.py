@@ -224,33 +224,31 @@ def prompts_for(args, wl, seqs):
 
 
 def prefill_into(args, wl, geo, fw, head, prompts, sinks):
-    """Prompt prefill (setup, untimed) with torch/cuBLAS/SDPA; ``sinks[b](layer, k, v)`` receive
-    sequence b's K/V.  The f32 weight matrices are re-streamed per pass (they are not kept)."""
+    """Prompt prefill (setup, untimed) with torch/cuBLAS/SDPA, layer-outer over all of this rank's
+    prompts; ``sinks[b](layer, k, v)`` receive sequence b's K/V.  The f32 weight matrices are
+    re-streamed for the pass (they are not kept)."""
     import torch
     from torch.nn.attention import SDPBackend, sdpa_kernel
 
-    from paper_2502_10424_b200._prefill import run_prefill
+    from paper_2502_10424_b200._prefill import run_prefill_batch
 
-    firsts = []
-    for b, p in enumerate(prompts):
-        def layers():
-            cur = {}
-            for name, t in weight_source(args, wl, geo):
-                if not name.startswith("layers."):
-                    continue
-                cur[name.split(".")[-1]] = t
-                if len(cur) == 7:
-                    cur["attn_norm"] = cur["mlp_norm"] = fw.final_norm
-                    yield cur
-                    cur = {}
+    def layers():
+        cur = {}
+        for name, t in weight_source(args, wl, geo):
+            if not name.startswith("layers."):
+                continue
+            cur[name.split(".")[-1]] = t
+            if len(cur) == 7:
+                cur["attn_norm"] = cur["mlp_norm"] = fw.final_norm
+                yield cur
+                cur = {}
 
-        ids = torch.from_numpy(p).cuda()
-        with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.CUDNN_ATTENTION]):
-            logits = run_prefill(geo, ids, fw.embedding, layers(), fw.final_norm, head, fw.rope, sinks[b],
-                                 dtype=torch.float16)
-        firsts.append(int(torch.argmax(logits).item()))
+    ids = [torch.from_numpy(p).cuda() for p in prompts]
+    with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.CUDNN_ATTENTION]):
+        logits = run_prefill_batch(geo, ids, fw.embedding, layers(), fw.final_norm, head, fw.rope, sinks,
+                                   dtype=torch.float16)
     torch.cuda.synchronize()
-    return firsts
+    return [int(torch.argmax(lg).item()) for lg in logits]
 
 
 def build_workload(args, wl, seqs):
@@ -376,6 +374,7 @@ def kernel_roofline(geo, fw, qw, hcache, peak):
     nq_tok = hcache.quantized_token_count
     nfp = hcache.fp1_len + hcache.fp2_len + 1
     run = Runner(geo, hcache, max_cols=5 * B)
+    run._rope = fw.rope  # the QKV epilogue's RoPE table (set by forward() in the decode loop)
     run.q.normal_()
     s = _lib.stream_ptr()
     per_tok = {"draft": kv * 1.0 + 8.0 * kv / G + 8.0 * math.ceil(kv / G),
@@ -401,7 +400,9 @@ def kernel_roofline(geo, fw, qw, hcache, peak):
         kw = dict(yh=(run.hh, run.hs)) if epi == _lib.EPI_SILU_MUL else {}
         if epi == _lib.EPI_SILU_MUL:
             src = (run.xh, run.xs)
-        fns = [(lambda w_=w_, li=li: run._linear(w_, src, y, 1, epi, layer=li, stream=s, **kw)) for li, w_ in enumerate(ws)]
+        # the stream is resolved per call: inside graph capture it is the capture stream
+        fns = [(lambda w_=w_, li=li: run._linear(w_, src, y, 1, epi, layer=li, stream=_lib.stream_ptr(), **kw))
+               for li, w_ in enumerate(ws)]
         dt_iso = time_kernel(fns[0])
         dt = time_graph(fns) if len(fns) > 1 else dt_iso
         algo = w.algorithmic_bytes() + 2.0 * w.K + 4.0 * w.N

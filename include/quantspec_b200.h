@@ -45,6 +45,30 @@ enum {
 };
 enum { QS_W_F16 = 0, QS_W_INT4 = 1 };
 
+/* KV-head sharding (the paper's 2-GPU long-context runs): one
+ * sequence's KV heads are split over `world` ranks and every rank needs every head's attention
+ * row for the replicated output projection.  Instead of an all-gather after the attention kernel,
+ * the merge epilogue of each (head, query group) stores its f16 row + 16-sums straight into every
+ * rank's gather buffer (NVLink P2P through CUDA IPC mappings, or plain pointers in one process)
+ * and bumps every rank's arrival counter (release, system scope); the CTA finishing a rank's last
+ * local merge waits (acquire) until all `arrivals` of the layer are in, copies the full row set to
+ * the output projection's input (out_h / out_s) and advances the epoch.  The gather buffers
+ * alternate by layer parity (epoch / arrivals), so a rank one layer ahead never overwrites rows a
+ * slower rank has not consumed.  world = 0: off. */
+#define QS_MAX_RANKS 8
+typedef struct {
+  int world, rank;
+  int q_col_offset;                 /* this rank's first column (query head * hd) of the full row */
+  int arrivals;                     /* head merges per layer over all ranks                         */
+  int64_t par_stride_h;             /* halves between the two parity buffers of gh[i]               */
+  int64_t par_stride_s;             /* floats between the two parity buffers of gs[i]               */
+  void* gh[QS_MAX_RANKS];           /* rank i's gather rows: half [2][rows][ld_out_h]               */
+  float* gs[QS_MAX_RANKS];          /* rank i's 16-sums: f32 [2][rows][ld_out_s]                    */
+  unsigned* flag[QS_MAX_RANKS];     /* rank i's arrival counter (monotonic, wraps)                  */
+  unsigned* epoch;                  /* this rank: arrivals consumed so far (advanced by the waiter) */
+  int* done;                        /* this rank: merges finished in the current launch (zeroed)    */
+} qs_gather_args;
+
 /* Split-K flash-decode over the hierarchical store for one layer.
  * Replaces draft_view/target_view (Q/cache.py:309-378) + _merged_attention
  * (Q/model.py:176-195) for T query rows at once (Q/specdec.py:270-273). */
@@ -85,6 +109,8 @@ typedef struct {
   int64_t ld_out_h;
   float* out_s;
   int64_t ld_out_s;
+  /* KV-head sharding: fused all-gather of the rows into out_h / out_s (needs out_h, out_s) */
+  qs_gather_args gather;
 } qs_attn_args;
 
 /* x @ W with fused epilogue.  Replaces the fp32 `h @ W` products of
@@ -212,6 +238,14 @@ qs_status qs_greedy_accept(int* tok, int tok_stride, const int* target, int T, c
                            int* res, int* fp2_len, int* pos, void* stream);
 /* device-side length bump (append bookkeeping of Q/cache.py:234) */
 qs_status qs_add_int(int* p, int n, int delta, void* stream);
+
+/* ---- KV-head sharding buffers (qs_gather_args): whole cudaMalloc allocations, so they can be
+ * exported to the other ranks' processes as CUDA IPC handles (64 bytes) ---- */
+qs_status qs_dev_alloc(size_t bytes, void** ptr); /* zero-filled */
+qs_status qs_dev_free(void* ptr);
+qs_status qs_ipc_handle(void* ptr, char* handle64);
+qs_status qs_ipc_open(const char* handle64, void** ptr);
+qs_status qs_ipc_close(void* ptr);
 
 #ifdef __cplusplus
 }

@@ -28,6 +28,20 @@ i64 = C.c_int64
 f32 = C.c_float
 
 
+MAX_RANKS = 8  # QS_MAX_RANKS
+
+
+class GatherArgs(C.Structure):
+    """qs_gather_args: fused all-gather of KV-head-sharded attention rows (world = 0: off)."""
+
+    _fields_ = [
+        ("world", i32), ("rank", i32), ("q_col_offset", i32), ("arrivals", i32),
+        ("par_stride_h", i64), ("par_stride_s", i64),
+        ("gh", vp * MAX_RANKS), ("gs", vp * MAX_RANKS), ("flag", vp * MAX_RANKS),
+        ("epoch", vp), ("done", vp),
+    ]
+
+
 class AttnArgs(C.Structure):
     _fields_ = [
         ("B", i32), ("Hkv", i32), ("hd", i32), ("G", i32), ("T", i32), ("r", i32),
@@ -43,6 +57,7 @@ class AttnArgs(C.Structure):
         ("fp1_k", vp), ("fp1_v", vp), ("fp2_k", vp), ("fp2_v", vp), ("fp_seq_stride", i64), ("fp_rows", i32),
         ("partials", vp), ("counters", vp), ("dbg", i32),
         ("out_h", vp), ("ld_out_h", i64), ("out_s", vp), ("ld_out_s", i64),
+        ("gather", GatherArgs),
     ]
 
 
@@ -90,6 +105,11 @@ _SIGS = {
     "qs_argmax": (i32, [vp, i32, i32, vp, i32, vp]),
     "qs_greedy_accept": (i32, [vp, i32, vp, i32, vp, i32, vp, vp, vp, vp]),
     "qs_add_int": (i32, [vp, i32, i32, vp]),
+    "qs_dev_alloc": (i32, [C.c_size_t, C.POINTER(vp)]),
+    "qs_dev_free": (i32, [vp]),
+    "qs_ipc_handle": (i32, [vp, C.c_char_p]),
+    "qs_ipc_open": (i32, [C.c_char_p, C.POINTER(vp)]),
+    "qs_ipc_close": (i32, [vp]),
 }
 
 EXPORTED = tuple(_SIGS)

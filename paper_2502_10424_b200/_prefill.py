@@ -46,44 +46,58 @@ def run_prefill(geo, ids_dev, embedding, layer_iter, final_norm, lm_head, rope, 
     """Generic prefill.  ``layer_iter`` yields dicts of CUDA tensors
     (wq, wk, wv, wo, w_gate, w_up, w_down as [d_in, d_out], attn_norm, mlp_norm);
     ``sink(layer, k, v)`` receives K/V [S, kv_dim].  Returns f32 logits of the last row."""
+    return run_prefill_batch(geo, [ids_dev], embedding, layer_iter, final_norm, lm_head, rope,
+                             [sink], dtype=dtype, chunk=chunk)[0]
+
+
+def run_prefill_batch(geo, ids_list, embedding, layer_iter, final_norm, lm_head, rope, sinks, *, dtype=None,
+                      chunk: int = 8192):
+    """Prefill of several independent prompts, layer-outer: each layer's weights are produced once
+    (``layer_iter``) and applied to every prompt; ``sinks[b](layer, k, v)`` receives prompt b's
+    K/V [S_b, kv_dim].  Returns the f32 last-row logits of every prompt."""
     torch = _torch()
     import torch.nn.functional as F
 
-    S = int(ids_dev.numel())
-    if dtype is None:
-        dtype = torch.float32 if S * geo.hidden <= (1 << 23) else torch.float16
     H, Hk, hd = geo.num_heads, geo.num_kv_heads, geo.head_dim
-    x = embedding[ids_dev.long()].float()  # residual stream stays f32
-    cs = rope[:S]
+    if dtype is None:
+        dtype = torch.float32 if max(int(i.numel()) for i in ids_list) * geo.hidden <= (1 << 23) else torch.float16
+    xs = [embedding[ids.long()].float() for ids in ids_list]  # residual streams stay f32
     for li, lw in enumerate(layer_iter):
         W = {k: (v.to(dtype) if v.dim() == 2 else v.float()) for k, v in lw.items()}
-        q = torch.empty((S, H, hd), dtype=dtype, device=x.device)
-        k = torch.empty((S, Hk, hd), dtype=dtype, device=x.device)
-        v = torch.empty((S, Hk, hd), dtype=dtype, device=x.device)
-        for c0 in range(0, S, chunk):
-            c1 = min(S, c0 + chunk)
-            h = _rmsnorm(x[c0:c1], W["attn_norm"], geo.norm_eps).to(dtype)
-            q[c0:c1] = _rope((h @ W["wq"]).float().view(c1 - c0, H, hd), cs[c0:c1]).to(dtype)
-            k[c0:c1] = _rope((h @ W["wk"]).float().view(c1 - c0, Hk, hd), cs[c0:c1]).to(dtype)
-            v[c0:c1] = (h @ W["wv"]).view(c1 - c0, Hk, hd)
-        sink(li, k.reshape(S, Hk * hd), v.reshape(S, Hk * hd))
-        kq = k if Hk == H else k.repeat_interleave(H // Hk, dim=1)
-        vq = v if Hk == H else v.repeat_interleave(H // Hk, dim=1)
-        ctx = F.scaled_dot_product_attention(q.transpose(0, 1)[None], kq.transpose(0, 1)[None],
-                                             vq.transpose(0, 1)[None], is_causal=True)[0].transpose(0, 1)
-        del kq, vq, q, k, v
-        ctx = ctx.reshape(S, H * hd)
-        for c0 in range(0, S, chunk):
-            c1 = min(S, c0 + chunk)
-            x[c0:c1] += (ctx[c0:c1].to(dtype) @ W["wo"]).float()
-            hm = _rmsnorm(x[c0:c1], W["mlp_norm"], geo.norm_eps).to(dtype)
-            g = (hm @ W["w_gate"]).float()
-            u = (hm @ W["w_up"]).float()
-            act = (g / (1.0 + torch.exp(-g)) * u).to(dtype)
-            x[c0:c1] += (act @ W["w_down"]).float()
-        del ctx, W
-    last = _rmsnorm(x[-1:], final_norm, geo.norm_eps)
-    return (last.to(dtype) @ lm_head.to(dtype)).float()[0]
+        for b, x in enumerate(xs):
+            S = int(x.shape[0])
+            cs = rope[:S]
+            q = torch.empty((S, H, hd), dtype=dtype, device=x.device)
+            k = torch.empty((S, Hk, hd), dtype=dtype, device=x.device)
+            v = torch.empty((S, Hk, hd), dtype=dtype, device=x.device)
+            for c0 in range(0, S, chunk):
+                c1 = min(S, c0 + chunk)
+                h = _rmsnorm(x[c0:c1], W["attn_norm"], geo.norm_eps).to(dtype)
+                q[c0:c1] = _rope((h @ W["wq"]).float().view(c1 - c0, H, hd), cs[c0:c1]).to(dtype)
+                k[c0:c1] = _rope((h @ W["wk"]).float().view(c1 - c0, Hk, hd), cs[c0:c1]).to(dtype)
+                v[c0:c1] = (h @ W["wv"]).view(c1 - c0, Hk, hd)
+            sinks[b](li, k.reshape(S, Hk * hd), v.reshape(S, Hk * hd))
+            kq = k if Hk == H else k.repeat_interleave(H // Hk, dim=1)
+            vq = v if Hk == H else v.repeat_interleave(H // Hk, dim=1)
+            ctx = F.scaled_dot_product_attention(q.transpose(0, 1)[None], kq.transpose(0, 1)[None],
+                                                 vq.transpose(0, 1)[None], is_causal=True)[0].transpose(0, 1)
+            del kq, vq, q, k, v
+            ctx = ctx.reshape(S, H * hd)
+            for c0 in range(0, S, chunk):
+                c1 = min(S, c0 + chunk)
+                x[c0:c1] += (ctx[c0:c1].to(dtype) @ W["wo"]).float()
+                hm = _rmsnorm(x[c0:c1], W["mlp_norm"], geo.norm_eps).to(dtype)
+                g = (hm @ W["w_gate"]).float()
+                u = (hm @ W["w_up"]).float()
+                act = (g / (1.0 + torch.exp(-g)) * u).to(dtype)
+                x[c0:c1] += (act @ W["w_down"]).float()
+            del ctx
+        del W
+    out = []
+    for x in xs:
+        last = _rmsnorm(x[-1:], final_norm, geo.norm_eps)
+        out.append((last.to(dtype) @ lm_head.to(dtype)).float()[0])
+    return out
 
 
 def prefill_device(weights, ids: np.ndarray, cache_mode: str, *, group_size=None, sensitive_layers=frozenset(),

@@ -1203,6 +1203,10 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
   if (*ticket_s != n_split_tot - 1) return;
   // ===================== last CTA of the head: merge splits in fixed order =====================
   const float* allp = P.partials + hidx * n_split_tot * (size_t)NQ * (HD + 2);
+  // KV-head sharding: this layer's gather buffers (parity of the layers consumed so far)
+  const qs_gather_args& GA = P.gather;
+  const unsigned epoch0 = GA.world ? __ldcg(GA.epoch) : 0u;
+  const int gpar = GA.world ? (int)((epoch0 / (unsigned)GA.arrivals) & 1u) : 0;
   // all lanes run every round (whole 16-channel groups are valid or not together) so the
   // optional f16 copy + 16-sums for the output projection can reduce with shuffles
   for (int base = 0; base < nq * HD; base += NTH) {
@@ -1257,12 +1261,50 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
 #pragma unroll
       for (int off = 1; off < 16; off <<= 1) sm16 += __shfl_xor_sync(0xffffffffu, sm16, off);
       if (valid) {
-        reinterpret_cast<__half*>(P.out_h)[row * P.ld_out_h + col] = h;
-        if ((c & 15) == 0) P.out_s[row * P.ld_out_s + col / 16] = sm16;
+        if (GA.world) {
+          // fused all-gather: this head's row goes to every rank's gather buffer (P2P stores)
+          const size_t gcol = (size_t)GA.q_col_offset + col;
+          for (int rk = 0; rk < GA.world; ++rk) {
+            reinterpret_cast<__half*>(GA.gh[rk])[gpar * GA.par_stride_h + row * P.ld_out_h + gcol] = h;
+            if ((c & 15) == 0) GA.gs[rk][gpar * GA.par_stride_s + row * P.ld_out_s + gcol / 16] = sm16;
+          }
+        } else {
+          reinterpret_cast<__half*>(P.out_h)[row * P.ld_out_h + col] = h;
+          if ((c & 15) == 0) P.out_s[row * P.ld_out_s + col / 16] = sm16;
+        }
       }
     }
   }
   if (tid == 0) P.counters[hidx] = 0;
+  if (GA.world) {
+    // signal every rank (release, system scope: the rows above are visible before the count),
+    // then the CTA finishing this rank's last local merge waits for the whole layer
+    __syncthreads();
+    const int nloc = (int)(gridDim.x * gridDim.z);
+    if (tid == 0) {
+      __threadfence_system();
+      for (int rk = 0; rk < GA.world; ++rk) red_release_sys_add(GA.flag[rk], 1u);
+      *ticket_s = atomicAdd(GA.done, 1);
+      if (*ticket_s == nloc - 1) {
+        const unsigned target = epoch0 + (unsigned)GA.arrivals;
+        while ((int)(ld_acquire_sys(GA.flag[GA.rank]) - target) < 0) __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    if (*ticket_s != nloc - 1) return;
+    // every rank's rows of this layer are in: hand the full row set to the output projection
+    const int rows = P.B * P.T;
+    const int nh = (int)(P.ld_out_h / 8), ns = (int)(P.ld_out_s / 4);  // uint4 / float4 per row
+    const uint4* gh = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(GA.gh[GA.rank]) + gpar * GA.par_stride_h);
+    const float4* gs = reinterpret_cast<const float4*>(GA.gs[GA.rank] + gpar * GA.par_stride_s);
+    for (int i = tid; i < rows * nh; i += NTH) reinterpret_cast<uint4*>(P.out_h)[i] = __ldcg(gh + i);
+    for (int i = tid; i < rows * ns; i += NTH) reinterpret_cast<float4*>(P.out_s)[i] = __ldcg(gs + i);
+    __syncthreads();
+    if (tid == 0) {
+      *GA.epoch = epoch0 + (unsigned)GA.arrivals;
+      *GA.done = 0;
+    }
+  }
 }
 
 template <int HD, int NT, int MODE, int QR>

@@ -194,6 +194,16 @@ qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream) {
     QS_FAIL(QS_ERR_CONFIG, "fp buffers of %d rows cannot hold a group of %d", a->fp_rows, a->G);
   if (mode != QS_VIEW_FP16 && !(a->G % a->hd == 0 || a->Hkv * a->hd <= a->G))
     QS_FAIL(QS_ERR_CONFIG, "value groups of %d channels would split a %d-channel head", a->G, a->hd);
+  if (a->gather.world) {
+    const qs_gather_args& g = a->gather;
+    if (g.world < 1 || g.world > QS_MAX_RANKS || g.rank < 0 || g.rank >= g.world)
+      QS_FAIL(QS_ERR_CONFIG, "gather: rank %d of world %d", g.rank, g.world);
+    if (!a->out_h || !a->out_s || !g.epoch || !g.done) QS_FAIL(QS_ERR_CONFIG, "gather needs out_h, out_s, epoch, done");
+    for (int i = 0; i < g.world; ++i)
+      if (!g.gh[i] || !g.gs[i] || !g.flag[i]) QS_FAIL(QS_ERR_CONFIG, "gather: rank %d buffers missing", i);
+    if (g.arrivals != g.world * a->B * a->Hkv * a->n_qgroups)
+      QS_FAIL(QS_ERR_CONFIG, "gather: %d arrivals per layer, expected world*B*Hkv*n_qgroups", g.arrivals);
+  }
   return cuda_status(launch_attention(*a, mode, S(stream)), "attn_decode");
 }
 
@@ -248,5 +258,33 @@ qs_status qs_greedy_accept(int* tok, int tok_stride, const int* target, int T, c
 qs_status qs_add_int(int* p, int n, int delta, void* stream) {
   return cuda_status(launch_add_int(p, n, delta, S(stream)), "add_int");
 }
+
+qs_status qs_dev_alloc(size_t bytes, void** ptr) {
+  if (!ptr) QS_FAIL(QS_ERR_CONFIG, "null out pointer");
+  *ptr = nullptr;
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e == cudaSuccess) e = cudaMemset(*ptr, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return cuda_status(e, "dev_alloc");
+}
+
+qs_status qs_dev_free(void* ptr) { return cuda_status(cudaFree(ptr), "dev_free"); }
+
+qs_status qs_ipc_handle(void* ptr, char* handle64) {
+  if (!ptr || !handle64) QS_FAIL(QS_ERR_CONFIG, "null pointer");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e == cudaSuccess) memcpy(handle64, &h, sizeof(h) < 64 ? sizeof(h) : 64);
+  return cuda_status(e, "ipc_handle");
+}
+
+qs_status qs_ipc_open(const char* handle64, void** ptr) {
+  if (!ptr || !handle64) QS_FAIL(QS_ERR_CONFIG, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h) < 64 ? sizeof(h) : 64);
+  return cuda_status(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "ipc_open");
+}
+
+qs_status qs_ipc_close(void* ptr) { return cuda_status(cudaIpcCloseMemHandle(ptr), "ipc_close"); }
 
 }  // extern "C"

@@ -226,12 +226,16 @@ class Runner:
     """
 
     def __init__(self, geo: Geometry, cache, *, max_cols: int = 16, attn_splits: int | None = None,
-                 shard: tuple | None = None):
+                 shard: tuple | None = None, gather=None):
         """``shard=(rank, world, process_group)``: KV-head sharding for a single sequence
         whose context does not fit one GPU.  This rank's cache and QKV
         weights hold heads [rank*H/world, (rank+1)*H/world); attention runs on those
-        heads only and its outputs are all-gathered (NCCL over NVLink on a real box)
-        before the replicated output projection / MLP."""
+        heads only and every rank needs all heads' rows before the replicated output
+        projection / MLP.  ``gather``: None = torch.distributed.all_gather + prep (the
+        collective baseline); "ipc" = the fused all-gather (the attention merge stores each
+        head's f16 row into every rank's buffer over NVLink P2P, qs_gather_args), buffers
+        exchanged as CUDA IPC handles over ``process_group``; or a parallel.HeadGather the
+        caller links (ranks sharing one process, one stream each)."""
         torch = _torch()
         self.geo = geo
         self.cache = cache
@@ -276,9 +280,24 @@ class Runner:
         self.r = r
         self._attn_splits_override = attn_splits
         ncols_q = self.max_T * r
-        self.n_qgroups_max = max(1, -(-ncols_q // 12))
+        # query-column groups per KV head: <= 8 queries per CTA in the quantised target view (one
+        # 8-query MMA tile: GQA verify splits its r*T queries into several NT = 1 CTAs, which read the
+        # same chunks at the same time -> L2 serves the repeats), <= 12 elsewhere
+        self.n_qgroups_max = max(1, -(-ncols_q // 8))
         self._lin_cache: dict = {}
         self._gen = None
+        self.gather = None
+        if gather is not None:
+            if shard is None:
+                raise ConfigError("a fused gather needs shard=(rank, world, group)")
+            from .parallel import HeadGather
+
+            rank, world, group = shard
+            if isinstance(gather, str):
+                gather = HeadGather.exchange(world, rank, max_cols, self.xh.shape[1], self.xs.shape[1], group)
+            if (gather.rows, gather.ld_h, gather.ld_s) != (max_cols, self.xh.shape[1], self.xs.shape[1]):
+                raise ConfigError("gather buffers do not match the runner's activation rows")
+            self.gather = gather
         self._plan()
 
     def _plan(self) -> None:
@@ -292,10 +311,9 @@ class Runner:
         else:
             self.max_chunks = -(-cache.max_blocks * cache.layout.group_size // 128)
         self._splits: dict = {}
-        ncols_q = self.max_T * self.r
-        per = -(-ncols_q // self.n_qgroups_max)
-        # queries per CTA: 8 per tile in the quantised views, 4 in the fp16 view (qs_attn_partials_floats)
-        nq_cta = max(8 * max(1, -(-per // 8)), 4 * max(1, -(-per // 4)))
+        # queries per CTA (qs_attn_partials_floats): <= 8 in the target view, <= 12 in the draft / fp16
+        # views (whose groups of 12 are never more numerous than the target's groups of 8)
+        nq_cta = 12
         max_splits = self._attn_splits_override or max(1, min(self.max_chunks, 4 * SM_COUNT))
         nparts = self.B * self.lgeo.num_kv_heads * self.n_qgroups_max * (max_splits + 2) * nq_cta * (self.geo.head_dim + 2)
         self.partials = torch.zeros(nparts, dtype=torch.float32, device="cuda")
@@ -318,12 +336,14 @@ class Runner:
             if self._attn_splits_override:
                 n = self._attn_splits_override
             else:
-                cols = self.r if view == _lib.VIEW_DRAFT else min(12, self.max_T * self.r)
+                cols = self.r if view == _lib.VIEW_DRAFT else min(8 if view == _lib.VIEW_TARGET else 12,
+                                                                  self.max_T * self.r)
                 occ = _lib.load().qs_attn_occupancy(self.geo.head_dim, cols, view)
                 occ = occ if occ > 0 else 1
-                # per-sequence plan (never scaled by the batch): a sequence's rows are bit-identical whatever
-                # batch it decodes in (batch-3 == three batch-1 runs)
-                n = plan_attention_splits(self.lgeo.num_kv_heads * self.n_qgroups_max, self.max_chunks, occ)
+                # per-sequence, per-head plan -- never scaled by the batch, the rows per sequence or the
+                # query groups -- so a sequence's rows are bit-identical whatever batch it decodes in
+                # (batch-3 == three batch-1 runs) and a T-row verify equals T one-row target steps
+                n = plan_attention_splits(self.lgeo.num_kv_heads, self.max_chunks, occ)
             self._splits[view] = n
         return n
 
@@ -404,7 +424,9 @@ class Runner:
             a = _lib.AttnArgs()
             a.B, a.Hkv, a.hd, a.T, a.r = self.B, self.lgeo.num_kv_heads, geo.head_dim, T, self.r
             a.n_queries = T * self.r
-            a.n_qgroups = max(1, -(-a.n_queries // 12))
+            quant_target = view == _lib.VIEW_TARGET and not self.is_fp and layer not in getattr(
+                self.cache.layout, "sensitive_layers", ())
+            a.n_qgroups = max(1, -(-a.n_queries // (8 if quant_target else 12)))
             a.n_main = self.splits_for(view if not self.is_fp else _lib.VIEW_FP16)
             a.row_offset = row_offset
             a.sm_scale_log2 = float(1.4426950408889634 / math.sqrt(geo.head_dim))
@@ -412,9 +434,12 @@ class Runner:
             a.partials, a.counters = self.partials.data_ptr(), self.attn_counters.data_ptr()
             # fused hand-off: the merge writes the O projection's f16 input + 16-sums (no prep launch);
             # a head shard gathers first, so its merge writes only the f32 rows
-            if self.shard is None:
+            if self.shard is None or self.gather is not None:
                 a.out_h, a.ld_out_h = self.xh.data_ptr(), self.xh.shape[1]
                 a.out_s, a.ld_out_s = self.xs.data_ptr(), self.xs.shape[1]
+            if self.gather is not None:
+                rank, world, _ = self.shard
+                self.gather.fill(a, arrivals=world * self.B * a.Hkv * a.n_qgroups, q_col_offset=rank * self.lgeo.nq)
             if self.is_fp:
                 a.G = 64
                 a.fp_len = c.d_len.data_ptr()
@@ -480,7 +505,7 @@ class Runner:
                 self._prep(self.x, w.attn_norms[li], X, ncols, s)
                 self._linear(lw["qkv"], X, None, ncols, _lib.EPI_QKV, layer=li, T=T, row_offset=row_offset, stream=s)
             self._attention(li, view, T, row_offset, s)  # also writes X = (f16, 16-sums) of its output
-            if self.shard is not None:
+            if self.shard is not None and self.gather is None:
                 self._gather_heads(ncols)
                 self._prep(self.attn_full, None, X, ncols, s)
             self._linear(lw["o"], X, self.x, ncols, _lib.EPI_ADD, stream=s)

@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--dbg", default="0")
     ap.add_argument("--T", default="1,5")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--r", type=int, default=1, help="query heads per KV head (GQA: 4)")
+    ap.add_argument("--batch", type=int, default=1, help="sequences per launch")
     a = ap.parse_args()
     import torch
 
@@ -37,8 +39,8 @@ def main():
     from paper_2502_10424_b200.runtime import Geometry, Runner
 
     G, H, hd = 128, a.heads, a.hd
-    lay = CacheLayout(1, H, hd, G)
-    c = HierarchicalKVCache(lay, max_tokens=a.context + 2 * G)
+    lay = CacheLayout(1, H * a.r, hd, G, num_kv_heads=H)
+    c = HierarchicalKVCache(lay, max_tokens=a.context + 2 * G, batch=a.batch)
     nb = a.context // G - 1
     for t in (c.ku, c.kl, c.vu, c.vl):
         t.random_(0, 256)
@@ -52,14 +54,14 @@ def main():
     c.d_fp1_len.fill_(G)
     c.d_fp2_len.fill_(3)
     kv = H * hd
-    geo = Geometry(1, kv, H, H, hd, 16, 16, 1 << 20)
+    geo = Geometry(1, kv * a.r, H * a.r, H, hd, 16, 16, 1 << 20)
     s = _lib.stream_ptr()
     for T in [int(x) for x in a.T.split(",")]:
         view = _lib.VIEW_DRAFT if T == 1 else _lib.VIEW_TARGET
         per_tok = (kv * (1.0 if T == 1 else 2.0)) + 8.0 * kv / G + 8.0 * math.ceil(kv / G)
-        nbytes = nb * G * per_tok + (G + 3 + T) * kv * 4.0
+        nbytes = a.batch * (nb * G * per_tok + (G + 3 + T) * kv * 4.0)
         for sp in [int(x) for x in a.splits.split(",")]:
-            run = Runner(geo, c, max_cols=max(T, 5), attn_splits=sp or None)
+            run = Runner(geo, c, max_cols=max(T, 5) * a.batch, attn_splits=sp or None)
             run.q.normal_()
             for dbg in [int(x) for x in a.dbg.split(",")]:
                 run._attention(0, view, T, 0, s)  # build args

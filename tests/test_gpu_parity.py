@@ -750,3 +750,39 @@ def test_trace_matches_reference_structure(toy):
         for line in res.trace.to_ndjson().strip().splitlines() if res.trace.steps else []:
             rec = json.loads(line)
             assert set(rec) == {"step", "drafted", "accepted", "corrected", "bonus", "flushed", "draft_bytes", "target_bytes"}
+
+
+def test_reference_written_qskv_round_trips_through_the_device_store(tmp_path):
+    """A QSKV file written by the REFERENCE (tests/golden/make_qskv_golden.py: prefill, decode appends,
+    a full-fp1 flush, a sensitive layer) loads into the device store with the reference's views, and
+    the device writes it back byte for byte (Q/cache.py:405-553)."""
+    src = os.path.join(GOLDEN, "ref_cache.qskv")
+    z = np.load(os.path.join(GOLDEN, "ref_cache_views.npz"))
+    c = qs.HierarchicalKVCache.load_snapshot(src)
+    assert c.seq_len == int(z["seq_len"]) and c.quantized_token_count == int(z["quantized"])
+    for layer in range(2):
+        for kind in ("draft", "target"):
+            view = c.draft_view(layer) if kind == "draft" else c.target_view(layer)
+            k, v = view.concat()
+            assert np.array_equal(k, z[f"{kind}_k{layer}"]) and np.array_equal(v, z[f"{kind}_v{layer}"]), (layer, kind)
+    out = tmp_path / "dev.qskv"
+    c.save_snapshot(out)
+    with open(src, "rb") as f:
+        assert out.read_bytes() == f.read()
+
+
+def test_stochastic_decode_on_device_logits(toy):
+    """Stochastic verification end to end (host decisions, Q/specdec.py:148-170, over device logits):
+    the lossless configuration (fp cache, fp draft: p == q bit for bit) accepts every draft, and the
+    hierarchical one keeps the emission budget with a valid trace; a fixed seed reproduces the run."""
+    w, _ = toy
+    prompt = np.random.default_rng(6).integers(0, 64, size=150)
+    spec = qs.SpecConfig(gamma=4, decode_len=40, sampling="stochastic", temperature=0.8, seed=3)
+    res = qs.SpeculativeDecoder(w, spec, kv_quant=False).run(prompt)
+    assert res.metrics.acceptance_rate == 1.0 and len(res.tokens) == 40
+    sd = qs.SpeculativeDecoder(w, spec, group_size=16)
+    a, b = sd.run(prompt), qs.SpeculativeDecoder(w, spec, group_size=16).run(prompt)
+    assert len(a.tokens) == 40 and all(0 <= t < 64 for t in a.tokens)
+    assert 0.0 < a.metrics.acceptance_rate <= 1.0
+    assert a.tokens == b.tokens
+    assert len(a.trace.to_ndjson().splitlines()) == len(a.trace.steps)
