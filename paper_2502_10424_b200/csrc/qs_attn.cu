@@ -47,6 +47,9 @@ __device__ __forceinline__ void mma_nv(float (&d)[4], const uint32_t (&a)[4], ui
 }
 
 constexpr int PSTRIDE = 24;
+#ifndef QS_TGT_PLO
+#define QS_TGT_PLO 0  // target view P.V: p' as f16 hi only (1: hi + lo); |error| <= 2^-12 |p'|, as the draft view
+#endif
 #ifndef QS_DRAFT_NPC
 #define QS_DRAFT_NPC 1
 #endif  // halves per P row (16 tokens + pad: conflict-free transposes)
@@ -100,22 +103,34 @@ struct AttnCfg {
   static constexpr int S2 = (233472 / 2 - 1024 - FIXED) / QSTAGE;
   static constexpr int S1 = (232448 - FIXED) / QSTAGE;
   static constexpr int MIN_BLOCKS = QUANT ? ((NT == 1 && S2 >= 4) ? 2 : 1) : 3;  // wide launches: registers
-  // TMAW (one CTA per SM, the target's wide fold): a dedicated TMA warp refills each stage as
-  // soon as the consumers release it, and NPW = NSTAGE fold warps each own one stage -- every
-  // mbarrier's phases are then waited in order by a single warp, so a parity wait can never
-  // run a phase ahead.  Otherwise (two CTAs per SM, or the draft's cheap fold) two fold warps
-  // alternate chunks and refill the ring themselves behind the consumers.
+  // TMAW (one CTA per SM, the target's wide fold): NPW = NSTAGE fold warps each own one ring stage
+  // -- fold its chunk, hand it to the consumers, and refill it with the chunk NSTAGE ahead as soon
+  // as they release it -- so every mbarrier's phases are waited in order by a single warp (a parity
+  // wait can never run a phase ahead) and no separate TMA warp is needed: 8 + 4 = 12 warps, three
+  // per SM sub-partition, 168 registers each.  Otherwise (two CTAs per SM, or the draft's cheap
+  // fold) two fold warps alternate chunks and refill the ring themselves behind the consumers.
   static constexpr bool TMAW = ROWQ && MIN_BLOCKS == 1;
   static constexpr int NSTAGE =
       QUANT ? (MIN_BLOCKS == 2 ? (S2 < 6 ? S2 : 6) : TMAW ? (S1 < 4 ? S1 : 4) : (S1 < 6 ? S1 : 6)) : 1;
   static constexpr int NPW = QUANT ? (TMAW ? NSTAGE : (NSTAGE > 2 ? 2 : 1)) : 0;
-  static constexpr int NWARPS = NCW + (TMAW ? 1 : 0) + NPW;
+  static constexpr int NWARPS = NCW + NPW;
   static constexpr int THREADS = NWARPS * 32;
   static constexpr int REGION_Q = QUANT ? NSTAGE * QSTAGE : 0;
   static constexpr int R0 = REGION_Q > REGION_F ? REGION_Q : REGION_F;
   static constexpr int REGION = R0 > MERGE_BYTES ? R0 : MERGE_BYTES;
-  static constexpr int VPAD = 2 * NQ <= 8 ? 8 : 2 * NQ <= 16 ? 16 : 32;      // reduce-scatter width
+  static constexpr int VPAD = 2 * NQ <= 8 ? 8 : 2 * NQ <= 16 ? 16 : 2 * NQ <= 32 ? 32 : 64;  // reduce-scatter width
   static constexpr int SMEM = REGION + FIXED;
+  // wide-query verify (NT >= 2 query tiles: GQA r*T queries, or T > 8): the consumers' P.V
+  // accumulators of every query tile live in tensor memory between chunks (32 columns per tile per
+  // warp; warps w, w+4 share a lane quarter) -- one CTA streams a head's chunks once for all its
+  // queries without the register file holding NT x 32 accumulators per thread
+  static constexpr bool PARK = ROWQ && NT >= 2;
+  static constexpr int TMEM_COLS = !PARK ? 0 : (2 * NT * 32 <= 128 ? 128 : 256);
+  // registers per thread: each SM sub-partition holds 16K registers and gets every 4th resident
+  // warp, so the busiest one holds ceil(MIN_BLOCKS * NWARPS / 4) warps (8-register granules)
+  static constexpr int WPS = (MIN_BLOCKS * NWARPS + 3) / 4;
+  static constexpr int MAXREG_ = (16384 / (WPS * 32)) / 8 * 8;
+  static constexpr int MAXREG = MAXREG_ > 255 ? 255 : MAXREG_;
 };
 
 __device__ __forceinline__ int swz16(int chunk, int row, int nchunk) {
@@ -366,7 +381,7 @@ template <typename C, int HD, int NT>
 __device__ __forceinline__ void fp16_region_q(uint8_t* region, uint32_t* aqf, const float* q_s, int nq,
                                               const __half* fk, const __half* fv, int n_tok, int c_begin, int c_end,
                                               int causal, int qg, const AttnParams& P, Softmax (&st)[NT],
-                                              float (&acc)[C::KS][NT][4]) {
+                                              float (&acc)[C::KS][NT][4], uint32_t tacc = 0) {
   constexpr int KS = C::KS, NQ = C::NQ, NTH = C::THREADS, CF = C::CF;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
@@ -449,6 +464,8 @@ __device__ __forceinline__ void fp16_region_q(uint8_t* region, uint32_t* aqf, co
         }
       }
       uint32_t bph[NT][2], bpl[NT][2];
+      bool resc[NT];
+      float al0[NT], al1[NT];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         int lim = n_tok;
@@ -474,7 +491,11 @@ __device__ __forceinline__ void fp16_region_q(uint8_t* region, uint32_t* aqf, co
           st[nt].l *= alpha;
           st[nt].m = mx;
         }
-        if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+        if constexpr (C::PARK) {
+          resc[nt] = __any_sync(0xffffffffu, alpha != 1.0f);
+          al0[nt] = __shfl_sync(0xffffffffu, alpha, 8 * t4);
+          al1[nt] = __shfl_sync(0xffffffffu, alpha, 8 * t4 + 4);
+        } else if (__any_sync(0xffffffffu, alpha != 1.0f)) {
           const float a0 = __shfl_sync(0xffffffffu, alpha, 8 * t4);
           const float a1 = __shfl_sync(0xffffffffu, alpha, 8 * t4 + 4);
 #pragma unroll
@@ -499,16 +520,47 @@ __device__ __forceinline__ void fp16_region_q(uint8_t* region, uint32_t* aqf, co
         bpl[nt][0] = h2_as_u32(__floats2half2_rn(p[0][0] - f0.x, p[0][1] - f0.y));
         bpl[nt][1] = h2_as_u32(__floats2half2_rn(p[1][0] - f1.x, p[1][1] - f1.y));
       }
+      if constexpr (C::PARK) {
+        uint32_t va[KS][4];
 #pragma unroll
-      for (int cm = 0; cm < KS; ++cm) {
-        const int row = mt * 16 + (ii >> 1) * 8 + rr;
-        const int ch = cm * 2 + (ii & 1);
-        uint32_t a[4];
-        ldmatrix_x4_trans(a, smem_u32(vs_ + row * HD + swz16(ch, row, NCH16) * 8));
+        for (int cm = 0; cm < KS; ++cm) {
+          const int row = mt * 16 + (ii >> 1) * 8 + rr;
+          const int ch = cm * 2 + (ii & 1);
+          ldmatrix_x4_trans(va[cm], smem_u32(vs_ + row * HD + swz16(ch, row, NCH16) * 8));
+        }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          mma_nv(acc[cm][nt], a, bph[nt][0], bph[nt][1]);
-          mma_nv(acc[cm][nt], a, bpl[nt][0], bpl[nt][1]);
+          float aw[32];
+          tmem_ld32(tacc + nt * 32, aw);
+          if (resc[nt]) {
+#pragma unroll
+            for (int cm = 0; cm < KS; ++cm) {
+              aw[cm * 4 + 0] *= al0[nt];
+              aw[cm * 4 + 1] *= al1[nt];
+              aw[cm * 4 + 2] *= al0[nt];
+              aw[cm * 4 + 3] *= al1[nt];
+            }
+          }
+#pragma unroll
+          for (int cm = 0; cm < KS; ++cm) {
+            float (&a4)[4] = *reinterpret_cast<float(*)[4]>(aw + cm * 4);
+            mma_nv(a4, va[cm], bph[nt][0], bph[nt][1]);
+            if constexpr (QS_TGT_PLO) mma_nv(a4, va[cm], bpl[nt][0], bpl[nt][1]);
+          }
+          tmem_st32(tacc + nt * 32, aw);
+        }
+      } else {
+#pragma unroll
+        for (int cm = 0; cm < KS; ++cm) {
+          const int row = mt * 16 + (ii >> 1) * 8 + rr;
+          const int ch = cm * 2 + (ii & 1);
+          uint32_t a[4];
+          ldmatrix_x4_trans(a, smem_u32(vs_ + row * HD + swz16(ch, row, NCH16) * 8));
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mma_nv(acc[cm][nt], a, bph[nt][0], bph[nt][1]);
+            if constexpr (QS_TGT_PLO) mma_nv(acc[cm][nt], a, bpl[nt][0], bpl[nt][1]);
+          }
         }
       }
     }
@@ -522,7 +574,8 @@ __device__ __forceinline__ void fp16_region_q(uint8_t* region, uint32_t* aqf, co
 template <typename C, int HD, int NT, int MODE>
 __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, const float* q_s, __half* pw, int nq,
                                              int seq, int head, int n_tok, int c_begin, int c_end,
-                                             const AttnParams& P, Softmax (&st)[NT], float (&acc)[C::KS][NT][4]) {
+                                             const AttnParams& P, Softmax (&st)[NT], float (&acc)[C::KS][NT][4],
+                                             uint32_t tacc = 0) {
   constexpr int KS = C::KS, NQ = C::NQ, S = C::NSTAGE;
   constexpr bool TGT = MODE == MODE_QTARGET;
   constexpr float kvs = TGT ? 0.0625f : 1.0f;  // target code = 16 c_u + c_l -> scale S/16
@@ -540,23 +593,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   if (warp >= C::NCW) {
     // ======================= producer warps (NPW) =======================
     auto issue = [&](int i) { quant_issue<C, HD, MODE>(P, region, tma_b, seq, head, n_blocks, c_begin, i); };
-    if constexpr (C::TMAW) {
-      if (warp == C::NCW) {
-        // dedicated TMA warp: chunk c >= S goes into the stage chunk c - S vacated (whole warp
-        // loops, lane 0 issues, so it reaches the kernel's CTA barriers converged)
-        for (int c = S, st_ = 0, ph_ = 0; c < nchunk; ++c) {
-          mbar_wait(&empty_b[st_], ph_);
-          if (++st_ == S) {
-            st_ = 0;
-            ph_ ^= 1;
-          }
-          if (lane == 0) issue(c);
-          __syncwarp();
-        }
-        return;
-      }
-    }
-    const int pwid = warp - C::NCW - (C::TMAW ? 1 : 0);
+    const int pwid = warp - C::NCW;
     // Producer warp p folds whole chunks j = p (mod NPW) on its own (no inter-warp
     // synchronisation: the per-chunk fold is a latency chain, so independent warps
     // overlap it), then refills the stage of its previous chunk once the consumers
@@ -629,7 +666,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         // warp reduce-scatter of the 2*NQ partial sums (zs then bs): each level halves
         // the values a lane holds, so 2*NQ-1 shuffles replace 5*2*NQ dependent ones
         constexpr int V = C::VPAD;  // 2*NQ padded to a power of two
-        constexpr int LV = V == 8 ? 3 : V == 16 ? 4 : 5;
+        constexpr int LV = V == 8 ? 3 : V == 16 ? 4 : 5;  // levels (V = 64: five, two sums per lane)
         float vals[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) vals[i] = 0.f;
@@ -649,13 +686,23 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
             vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
           }
         }
-        float tot = vals[0];
-#pragma unroll
-        for (int o = 16 >> LV; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        // lanes [idx << (5-LV), (idx+1) << (5-LV)) now hold sum idx (idx < NQ: zs, else bs)
         const int qq = lane < nq ? lane : 0;
-        const float z = __shfl_sync(0xffffffffu, tot, qq << (5 - LV));
-        const float b = __shfl_sync(0xffffffffu, tot, (NQ + qq) << (5 - LV));
+        float z, b;
+        if constexpr (V == 64) {
+          // sum idx sits in lane idx >> 1, slot idx & 1
+          const float z0 = __shfl_sync(0xffffffffu, vals[0], qq >> 1), z1 = __shfl_sync(0xffffffffu, vals[1], qq >> 1);
+          const float b0 = __shfl_sync(0xffffffffu, vals[0], (NQ + qq) >> 1);
+          const float b1 = __shfl_sync(0xffffffffu, vals[1], (NQ + qq) >> 1);
+          z = (qq & 1) ? z1 : z0;
+          b = ((NQ + qq) & 1) ? b1 : b0;
+        } else {
+          float tot = vals[0];
+#pragma unroll
+          for (int o = 16 >> LV; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+          // lanes [idx << (5-LV), (idx+1) << (5-LV)) now hold sum idx (idx < NQ: zs, else bs)
+          z = __shfl_sync(0xffffffffu, tot, qq << (5 - LV));
+          b = __shfl_sync(0xffffffffu, tot, (NQ + qq) << (5 - LV));
+        }
         // draft tokens g of a 16-token tile carry 1024 + c, tokens g+8 carry (1024 + 16c) (scaled
         // by 1/16 after the MMA); target tokens carry 1032 + (16 c_u + c_l)
         if (lane < nq) {
@@ -667,7 +714,14 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       if (lane == 0) mbar_arrive(&full_b[s]);
       // refill the stage of this warp's previous chunk (every chunk >= S is issued exactly once)
       const int jp = j - NPW;
-      if (!C::TMAW && jp >= 0 && jp + S < nchunk) {
+      if constexpr (C::TMAW) {
+        // this warp's stage: refill it with chunk j + S once the consumers release chunk j
+        if (j + S < nchunk) {
+          mbar_wait(&empty_b[s], ph);
+          if (lane == 0) issue(j + S);
+          __syncwarp();
+        }
+      } else if (jp >= 0 && jp + S < nchunk) {
         mbar_wait(&empty_b[s_prev], ph_prev);
         if (lane == 0) issue(jp + S);
       }
@@ -727,6 +781,8 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       }
       const float4 vz0 = vps4[mt * 8 + t4], vz1 = vps4[mt * 8 + 4 + t4];
       uint32_t bph[NT][2], bpl[NT][2];
+      bool resc[NT];
+      float al0[NT], al1[NT];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const float2 bb = *reinterpret_cast<const float2*>(bias + (bl * NQ + nt * 8 + g) * 2);
@@ -750,7 +806,11 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
           st[nt].m = mx;
         }
         // the accumulator columns of query q = nt*8 + 2t + e live in this lane; its alpha in lanes g = q
-        if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+        if constexpr (C::PARK) {
+          resc[nt] = __any_sync(0xffffffffu, alpha != 1.0f);
+          al0[nt] = __shfl_sync(0xffffffffu, alpha, 8 * t4);
+          al1[nt] = __shfl_sync(0xffffffffu, alpha, 8 * t4 + 4);
+        } else if (__any_sync(0xffffffffu, alpha != 1.0f)) {
           const float a0 = __shfl_sync(0xffffffffu, alpha, 8 * t4);
           const float a1 = __shfl_sync(0xffffffffu, alpha, 8 * t4 + 4);
 #pragma unroll
@@ -773,7 +833,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         float psum = (f0.x + f0.y) + (f1.x + f1.y);
         bph[nt][0] = h2_as_u32(h0);
         bph[nt][1] = h2_as_u32(h1);
-        if constexpr (TGT) {
+        if constexpr (TGT && QS_TGT_PLO) {
           const __half2 l0 = __floats2half2_rn(v00 - f0.x, v01 - f0.y), l1 = __floats2half2_rn(v10 - f1.x, v11 - f1.y);
           const float2 g0 = __half22float2(l0), g1 = __half22float2(l1);
           psum += (g0.x + g0.y) + (g1.x + g1.y);
@@ -786,15 +846,44 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       uint32_t vw[KS], vwl[KS];
       load_words<KS>(reinterpret_cast<const uint32_t*>(sp + C::PLANE_CHUNK), mt, lane, vw);
       if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp + 3 * C::PLANE_CHUNK), mt, lane, vwl);
+      if constexpr (C::PARK) {
+        // per query tile: accumulators TMEM -> registers, rescale, the tile's MMAs, back to TMEM
+        // (the same operations in the same order as the register-resident NT = 1 path)
+        uint32_t va[KS][4];
 #pragma unroll
-      for (int cm = 0; cm < KS; ++cm) {
-        uint32_t a[4];
-        if constexpr (TGT) unpack_u4l4_raw(vw[cm], vwl[cm], a);
-        else unpack_u4_raw(vw[cm], a);
+        for (int cm = 0; cm < KS; ++cm) unpack_u4l4_raw(vw[cm], vwl[cm], va[cm]);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          mma_nv(acc[cm][nt], a, bph[nt][0], bph[nt][1]);
-          if constexpr (TGT) mma_nv(acc[cm][nt], a, bpl[nt][0], bpl[nt][1]);
+          float aw[32];
+          tmem_ld32(tacc + nt * 32, aw);
+          if (resc[nt]) {
+#pragma unroll
+            for (int cm = 0; cm < KS; ++cm) {
+              aw[cm * 4 + 0] *= al0[nt];
+              aw[cm * 4 + 1] *= al1[nt];
+              aw[cm * 4 + 2] *= al0[nt];
+              aw[cm * 4 + 3] *= al1[nt];
+            }
+          }
+#pragma unroll
+          for (int cm = 0; cm < KS; ++cm) {
+            float (&a4)[4] = *reinterpret_cast<float(*)[4]>(aw + cm * 4);
+            mma_nv(a4, va[cm], bph[nt][0], bph[nt][1]);
+            if constexpr (QS_TGT_PLO) mma_nv(a4, va[cm], bpl[nt][0], bpl[nt][1]);
+          }
+          tmem_st32(tacc + nt * 32, aw);
+        }
+      } else {
+#pragma unroll
+        for (int cm = 0; cm < KS; ++cm) {
+          uint32_t a[4];
+          if constexpr (TGT) unpack_u4l4_raw(vw[cm], vwl[cm], a);
+          else unpack_u4_raw(vw[cm], a);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mma_nv(acc[cm][nt], a, bph[nt][0], bph[nt][1]);
+            if constexpr (TGT && QS_TGT_PLO) mma_nv(acc[cm][nt], a, bpl[nt][0], bpl[nt][1]);
+          }
         }
       }
     }
@@ -941,7 +1030,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
 // (1024 + c) p' and rows g+8 (1024 + 16c) p'; target rows carried (1032 + 16 c_u + c_l) p'.
 template <typename C, int HD, int NT, int MODE>
 __device__ __forceinline__ void merge_rows_quant(float* mrg, const Softmax (&st)[NT], const float (&acc)[C::KS][NT][4],
-                                                 bool offsets) {
+                                                 bool offsets, uint32_t tacc = 0) {
   constexpr int KS = C::KS, NQ = C::NQ, MS = C::MS;
   constexpr bool TGT = MODE == MODE_QTARGET;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -968,17 +1057,27 @@ __device__ __forceinline__ void merge_rows_quant(float* mrg, const Softmax (&st)
   const float og = offsets ? (TGT ? 1032.f : 1024.f) : 0.f, og8 = offsets ? (TGT ? 1032.f : 64.f) : 0.f;
   const float sc8 = (offsets && !TGT) ? 0.0625f : 1.0f;
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
+  for (int nt = 0; nt < NT; ++nt) {
+    float aw[32];
+    if constexpr (C::PARK) {
+      tmem_ld32(tacc + nt * 32, aw);  // parked accumulators (wide-query verify; TMEM address 0 is valid)
+    } else {
+#pragma unroll
+      for (int cm = 0; cm < KS; ++cm)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) aw[cm * 4 + e] = acc[cm][nt][e];
+    }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       float* row = mrg + (warp * NQ + nt * 8 + 2 * t4 + e) * MS;
       const float z = row[2], ps = row[3];
 #pragma unroll
       for (int cm = 0; cm < KS; ++cm) {
-        row[4 + cm * 16 + g] = (acc[cm][nt][e] - og * ps) + z;
-        row[4 + cm * 16 + g + 8] = fmaf(acc[cm][nt][e + 2], sc8, -og8 * ps) + z;
+        row[4 + cm * 16 + g] = (aw[cm * 4 + e] - og * ps) + z;
+        row[4 + cm * 16 + g + 8] = fmaf(aw[cm * 4 + e + 2], sc8, -og8 * ps) + z;
       }
     }
+  }
 }
 
 // per-warp merge rows of the hi/lo column-pair layout (query q = nt*4 + t): the fp16
@@ -1020,7 +1119,8 @@ __device__ __forceinline__ void merge_rows_fp(float* mrg, const Softmax (&st)[NT
 // the kernel
 // ---------------------------------------------------------------------------
 template <int HD, int NT, int MODE, int QR>
-__global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD, NT, MODE, QR>::MIN_BLOCKS) attn_kernel(const __grid_constant__ AttnParams P) {
+__global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS) __maxnreg__((AttnCfg<HD, NT, MODE, QR>::MAXREG))
+    attn_kernel(const __grid_constant__ AttnParams P) {
   using C = AttnCfg<HD, NT, MODE, QR>;
   constexpr int KS = C::KS, NQ = C::NQ, NCW = C::NCW, NTH = C::THREADS;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1030,7 +1130,7 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
   __half* pw_all = reinterpret_cast<__half*>(q_s + NQ * HD);           // [NCW][PW_HALVES]
   // tma[8] full[8] empty[8] (the row-query kernels have no P transpose buffers)
   uint64_t* bars = reinterpret_cast<uint64_t*>(C::ROWQ ? reinterpret_cast<__half*>(q_s + NQ * HD) : pw_all + NCW * C::PW_WARP);
-  int* ticket_s = reinterpret_cast<int*>(bars + 24);
+  int* ticket_s = reinterpret_cast<int*>(bars + 24);  // [0] split ticket, [2] TMEM base (PARK)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int seq = blockIdx.z;
@@ -1105,7 +1205,24 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
     c_end = fk ? (n_tok + C::CF - 1) / C::CF : 0;
   }
 
-  __syncthreads();  // barriers initialised, fragment buffers zeroed
+  uint32_t tacc = 0;  // this consumer warp's parked accumulators (TMEM lane quarter + column block)
+  if constexpr (C::PARK) {
+    if (warp == 0) tmem_alloc(reinterpret_cast<uint32_t*>(ticket_s + 2), C::TMEM_COLS);
+    tmem_fence_before();
+  }
+  __syncthreads();  // barriers initialised, fragment buffers zeroed, TMEM allocated
+  if constexpr (C::PARK) {
+    tmem_fence_after();
+    if (warp < NCW) {
+      tacc = reinterpret_cast<const uint32_t*>(ticket_s)[2] + ((uint32_t)(32 * (warp & 3)) << 16) +
+             (uint32_t)((warp >> 2) * NT * 32);
+      float z[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) z[i] = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) tmem_st32(tacc + nt * 32, z);
+    }
+  }
   if constexpr (C::QUANT) {
     // PDL: the first ring stages of packed planes stream in before the grid dependency resolves
     if (region_kind == 0 && warp == NCW && lane == 0)
@@ -1140,10 +1257,11 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
 #pragma unroll
           for (int e = 0; e < 4; ++e) acc[a][nt][e] = 0.f;
       }
-      if (c_end > c_begin) quant_region<C, HD, NT, MODE>(region, bars, q_s, pw, nq, seq, head, n_tok, c_begin, c_end, P, st, acc);
+      if (c_end > c_begin)
+        quant_region<C, HD, NT, MODE>(region, bars, q_s, pw, nq, seq, head, n_tok, c_begin, c_end, P, st, acc, tacc);
       __syncthreads();
       if (warp < NCW) {
-        if constexpr (C::ROWQ) merge_rows_quant<C, HD, NT, MODE>(mrg, st, acc, true);
+        if constexpr (C::ROWQ) merge_rows_quant<C, HD, NT, MODE>(mrg, st, acc, true, tacc);
         else merge_rows_fp<C, HD, NT, MODE>(mrg, st, acc, true);
       }
     }
@@ -1158,9 +1276,10 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[a][nt][e] = 0.f;
     }
-    if (c_end > c_begin) fp16_region_q<C, HD, NT>(region, bqf, q_s, nq, fk, fv, n_tok, c_begin, c_end, causal, qg, P, st, acc);
+    if (c_end > c_begin)
+      fp16_region_q<C, HD, NT>(region, bqf, q_s, nq, fk, fv, n_tok, c_begin, c_end, causal, qg, P, st, acc, tacc);
     __syncthreads();
-    if (warp < NCW) merge_rows_quant<C, HD, NT, MODE>(mrg, st, acc, false);
+    if (warp < NCW) merge_rows_quant<C, HD, NT, MODE>(mrg, st, acc, false, tacc);
   } else {
     constexpr int NTO = C::NTO;
     Softmax st[NTO];
@@ -1177,7 +1296,14 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS, AttnCfg<HD
     __syncthreads();
     if (warp < NCW) merge_rows_fp<C, HD, NTO, MODE>(mrg, st, acc, false);
   }
+  if constexpr (C::PARK) tmem_fence_before();
   __syncthreads();
+  if constexpr (C::PARK) {
+    if (warp == 0) {
+      tmem_fence_after();
+      tmem_dealloc(reinterpret_cast<const uint32_t*>(ticket_s)[2], C::TMEM_COLS);
+    }
+  }
   const size_t hidx = ((size_t)seq * P.Hkv + head) * P.n_qgroups + qg;
   float* part = P.partials + (hidx * n_split_tot + split) * (size_t)NQ * (HD + 2);
   for (int i = tid; i < nq * (HD + 2); i += NTH) {
@@ -1342,6 +1468,7 @@ static cudaError_t launch_attn_nt(const AttnParams& p, int nt, int per, cudaStre
     }
   } else {
     if (nt == 2) return launch_attn_t<HD, 2, MODE, 8>(p, s);
+    if (nt == 3) return launch_attn_t<HD, 3, MODE, 8>(p, s);
     if (nt != 1) return cudaErrorInvalidValue;
     switch (attn_qr(per)) {
       case 1: return launch_attn_t<HD, 1, MODE, 1>(p, s);
@@ -1391,6 +1518,7 @@ static int occ_h(int per) {
     return nt == 1 ? occ_t<HD, 1, MODE, 8>() : nt == 2 ? occ_t<HD, 2, MODE, 8>() : occ_t<HD, 3, MODE, 8>();
   } else {
     if (nt == 2) return occ_t<HD, 2, MODE, 8>();
+    if (nt == 3) return occ_t<HD, 3, MODE, 8>();
     switch (attn_qr(per)) {
       case 1: return occ_t<HD, 1, MODE, 1>();
       case 2: return occ_t<HD, 1, MODE, 2>();

@@ -187,7 +187,8 @@ qs_status qs_attn_decode(const qs_attn_args* a, int mode, void* stream) {
   if (a->hd != 16 && a->hd != 32 && a->hd != 64 && a->hd != 128) QS_FAIL(QS_ERR_CONFIG, "head_dim %d unsupported", a->hd);
   if (a->T < 1 || a->r < 1 || a->n_queries != a->T * a->r) QS_FAIL(QS_ERR_DIMENSION, "bad query geometry");
   int per = (a->n_queries + a->n_qgroups - 1) / a->n_qgroups;
-  if (per > 12) QS_FAIL(QS_ERR_CONFIG, "at most 12 query columns per CTA (got %d); raise n_qgroups", per);
+  const int per_max = mode == QS_VIEW_TARGET ? 24 : 12;  // target: up to three 8-query MMA tiles (TMEM-parked)
+  if (per > per_max) QS_FAIL(QS_ERR_CONFIG, "at most %d query columns per CTA (got %d); raise n_qgroups", per_max, per);
   if (a->n_main < 1) QS_FAIL(QS_ERR_CONFIG, "need at least one main split");
   if (mode != QS_VIEW_FP16 && (a->G % 16 || a->G > 128 || 128 % a->G)) QS_FAIL(QS_ERR_CONFIG, "group size %d unsupported", a->G);
   if ((a->fp1_k || a->fp2_k) && a->fp_rows < a->G)

@@ -280,10 +280,10 @@ class Runner:
         self.r = r
         self._attn_splits_override = attn_splits
         ncols_q = self.max_T * r
-        # query-column groups per KV head: <= 8 queries per CTA in the quantised target view (one
-        # 8-query MMA tile: GQA verify splits its r*T queries into several NT = 1 CTAs, which read the
-        # same chunks at the same time -> L2 serves the repeats), <= 12 elsewhere
-        self.n_qgroups_max = max(1, -(-ncols_q // 8))
+        # query-column groups per KV head: <= 24 queries per CTA in the quantised target view (three
+        # 8-query MMA tiles with TMEM-parked accumulators: a GQA verify reads each chunk once for all
+        # its r*T queries), <= 12 in the draft / fp16 views
+        self.n_qgroups_max = max(1, -(-ncols_q // 12))
         self._lin_cache: dict = {}
         self._gen = None
         self.gather = None
@@ -311,9 +311,9 @@ class Runner:
         else:
             self.max_chunks = -(-cache.max_blocks * cache.layout.group_size // 128)
         self._splits: dict = {}
-        # queries per CTA (qs_attn_partials_floats): <= 8 in the target view, <= 12 in the draft / fp16
-        # views (whose groups of 12 are never more numerous than the target's groups of 8)
-        nq_cta = 12
+        # queries per CTA (qs_attn_partials_floats): <= 24 in the target view, <= 12 in the draft / fp16
+        # views (the target's groups of 24 are never more numerous than the groups of 12)
+        nq_cta = 24
         max_splits = self._attn_splits_override or max(1, min(self.max_chunks, 4 * SM_COUNT))
         nparts = self.B * self.lgeo.num_kv_heads * self.n_qgroups_max * (max_splits + 2) * nq_cta * (self.geo.head_dim + 2)
         self.partials = torch.zeros(nparts, dtype=torch.float32, device="cuda")
@@ -336,7 +336,7 @@ class Runner:
             if self._attn_splits_override:
                 n = self._attn_splits_override
             else:
-                cols = self.r if view == _lib.VIEW_DRAFT else min(8 if view == _lib.VIEW_TARGET else 12,
+                cols = self.r if view == _lib.VIEW_DRAFT else min(24 if view == _lib.VIEW_TARGET else 12,
                                                                   self.max_T * self.r)
                 occ = _lib.load().qs_attn_occupancy(self.geo.head_dim, cols, view)
                 occ = occ if occ > 0 else 1
@@ -426,7 +426,7 @@ class Runner:
             a.n_queries = T * self.r
             quant_target = view == _lib.VIEW_TARGET and not self.is_fp and layer not in getattr(
                 self.cache.layout, "sensitive_layers", ())
-            a.n_qgroups = max(1, -(-a.n_queries // (8 if quant_target else 12)))
+            a.n_qgroups = max(1, -(-a.n_queries // (24 if quant_target else 12)))
             a.n_main = self.splits_for(view if not self.is_fp else _lib.VIEW_FP16)
             a.row_offset = row_offset
             a.sm_scale_log2 = float(1.4426950408889634 / math.sqrt(geo.head_dim))
