@@ -14,19 +14,15 @@ Q/specdec.py:270-273).
 from __future__ import annotations
 
 import math
-import struct
-import zlib
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib, quant
+from . import _lib, qspw, quant
 from .cache import CacheLayout, CacheView, FpKVCache, HierarchicalKVCache
 from .errors import BufferOverflowError, ConfigError, DataError, DimensionError, EmptyPromptError, FormatError
 from .runtime import DeviceWeights, Geometry, Runner, build_device_weights, rope_table
 
-WEIGHT_MAGIC = b"QSPW"
-WEIGHT_VERSION = 1
 F32_BYTES = 4.0
 INT4_BYTES = 0.5
 DTYPE = np.float32
@@ -448,72 +444,24 @@ def chunked_attention(q: np.ndarray, chunks, scale: float | None = None) -> np.n
 
 
 def save_weights(path, weights: ModelWeights) -> None:
+    """Write the reference's QSPW weight file (Q/model.py:415-458; codec in qspw.py)."""
     cfg = weights.config
-    body = bytearray()
-    for name, arr in weights.named_tensors():
-        enc = name.encode("utf-8")
-        body += struct.pack("<H", len(enc)) + enc
-        a32 = np.asarray(arr, dtype="<f4")
-        body += struct.pack("<B", a32.ndim)
-        for dim in a32.shape:
-            body += struct.pack("<I", dim)
-        body += a32.tobytes()
+    dims = (cfg.num_layers, cfg.num_heads, cfg.head_dim, cfg.hidden, cfg.mlp_hidden, cfg.vocab, cfg.max_positions)
     with open(path, "wb") as f:
-        f.write(WEIGHT_MAGIC)
-        f.write(struct.pack("<B", WEIGHT_VERSION))
-        f.write(struct.pack("<7I", cfg.num_layers, cfg.num_heads, cfg.head_dim, cfg.hidden, cfg.mlp_hidden, cfg.vocab,
-                            cfg.max_positions))
-        f.write(struct.pack("<2d", cfg.rope_base, cfg.norm_eps))
-        f.write(struct.pack("<Q", len(body)))
-        f.write(bytes(body))
-        f.write(struct.pack("<I", zlib.crc32(bytes(body))))
+        f.write(qspw.encode(dims, cfg.rope_base, cfg.norm_eps, weights.named_tensors()))
 
 
 def load_weights(path) -> ModelWeights:
+    """Read a QSPW weight file (Q/model.py:461-524): FormatError on a bad magic / version, truncation,
+    checksum mismatch, a missing tensor or a wrong shape.  GQA files (this package's extension: the
+    reference is MHA) carry their KV width in the wk / wv shapes."""
     with open(path, "rb") as f:
-        raw = f.read()
-    off = 0
-
-    def take(n):
-        nonlocal off
-        if off + n > len(raw):
-            raise FormatError("weight file truncated")
-        b = raw[off : off + n]
-        off += n
-        return b
-
-    if take(4) != WEIGHT_MAGIC:
-        raise FormatError("bad weight-file magic")
-    (version,) = struct.unpack("<B", take(1))
-    if version != WEIGHT_VERSION:
-        raise FormatError(f"unsupported weight-file version {version}")
-    dims = struct.unpack("<7I", take(28))
-    rope_base, norm_eps = struct.unpack("<2d", take(16))
-    cfg = ModelConfig(*dims, rope_base=float(rope_base), norm_eps=float(norm_eps))
-    (blen,) = struct.unpack("<Q", take(8))
-    body = take(blen)
-    (crc,) = struct.unpack("<I", take(4))
-    if zlib.crc32(body) != crc:
-        raise FormatError("weight-file checksum mismatch")
-    tensors = {}
-    b = 0
-    while b < len(body):
-        if b + 2 > len(body):
-            raise FormatError("weight file truncated inside tensor table")
-        (nl,) = struct.unpack_from("<H", body, b)
-        b += 2
-        name = body[b : b + nl].decode("utf-8")
-        b += nl
-        (rank,) = struct.unpack_from("<B", body, b)
-        b += 1
-        shape = struct.unpack_from(f"<{rank}I", body, b)
-        b += 4 * rank
-        cnt = int(np.prod(shape)) if rank else 1
-        e = b + 4 * cnt
-        if e > len(body):
-            raise FormatError("weight file truncated inside tensor data")
-        tensors[name] = np.frombuffer(body, dtype="<f4", count=cnt, offset=b).reshape(shape).astype(DTYPE)
-        b = e
+        dims, rope_base, norm_eps, tensors = qspw.decode(f.read())
+    L, H, hd, d, mh, v, max_pos = dims
+    wk = tensors.get("layers.0.wk")
+    kvd = int(wk.shape[1]) if wk is not None and wk.ndim == 2 and wk.shape[1] % max(hd, 1) == 0 else d
+    cfg = ModelConfig(L, H, hd, d, mh, v, max_pos, rope_base=rope_base, norm_eps=norm_eps,
+                      num_kv_heads=None if kvd == d else kvd // hd)
 
     def grab(name, shape):
         a = tensors.get(name)
@@ -523,8 +471,7 @@ def load_weights(path) -> ModelWeights:
             raise FormatError(f"tensor {name!r} has shape {a.shape}, expected {shape}")
         return a
 
-    d, mh, v = cfg.hidden, cfg.mlp_hidden, cfg.vocab
-    layers = [LayerWeights(**{n: grab(f"layers.{i}.{n}", s) for n, s in (
-        ("wq", (d, d)), ("wk", (d, d)), ("wv", (d, d)), ("wo", (d, d)), ("w_gate", (d, mh)), ("w_up", (d, mh)),
-        ("w_down", (mh, d)), ("attn_norm", (d,)), ("mlp_norm", (d,)))}) for i in range(cfg.num_layers)]
+    shapes = {"wq": (d, d), "wk": (d, kvd), "wv": (d, kvd), "wo": (d, d), "w_gate": (d, mh), "w_up": (d, mh),
+              "w_down": (mh, d), "attn_norm": (d,), "mlp_norm": (d,)}
+    layers = [LayerWeights(**{n: grab(f"layers.{i}.{n}", sh) for n, sh in shapes.items()}) for i in range(L)]
     return ModelWeights(cfg, grab("embedding", (v, d)), layers, grab("final_norm", (d,)), grab("lm_head", (d, v)))

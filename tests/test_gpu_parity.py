@@ -786,3 +786,22 @@ def test_stochastic_decode_on_device_logits(toy):
     assert 0.0 < a.metrics.acceptance_rate <= 1.0
     assert a.tokens == b.tokens
     assert len(a.trace.to_ndjson().splitlines()) == len(a.trace.steps)
+
+
+def test_cli_run_and_ablate_measure_on_device(tmp_path):
+    """The harness (cli.py, Q/cli.py:233-284) runs on the device and reports measured tok/s; greedy
+    kv_quant tokens equal target-view AR tokens (losslessness through the CLI path too)."""
+    from paper_2502_10424_b200 import cli
+
+    assert cli.main(["run", "--out", str(tmp_path / "r"), "--decode-len", "40", "--gamma", "4"]) == 0
+    hdr, row = (tmp_path / "r" / "metrics.csv").read_text().strip().split("\n")
+    m = dict(zip(hdr.split(","), row.split(",")))
+    assert float(m["measured_tok_s"]) > 0 and float(m["measured_ar_tok_s"]) > 0
+    assert int(m["emitted_tokens"]) == 40
+    toks = [int(t) for t in (tmp_path / "r" / "tokens.txt").read_text().split()]
+    cfg = cli.resolve_config(cli.build_parser().parse_args(["run"]))
+    w = cli._weights(cfg)
+    assert toks == qs.autoregressive_decode(w, cli._prompt(cfg, w.config.vocab), 40, group_size=128)
+    assert cli.main(["ablate", "--out", str(tmp_path / "a"), "--decode-len", "20"]) == 0
+    lines = (tmp_path / "a" / "ablate.csv").read_text().strip().split("\n")
+    assert [l.split(",")[0] for l in lines[1:]] == ["neither", "kv_only", "weight_only", "both"]

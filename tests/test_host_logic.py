@@ -123,3 +123,24 @@ def test_partition_rejects_bad_rank():
 def test_job_throughput_single_process():
     jt = job_throughput(100, 2.0)
     assert jt.world == 1 and jt.rate == 50.0
+
+
+def test_cli_config_resolution_and_gen_model(tmp_path):
+    """The harness resolves defaults <- JSON file <- flags like the reference CLI (Q/cli.py:81-111) and
+    gen-model writes the reference-format weights of the seed + 2 init stream (Q/cli.py:118-133)."""
+    import json
+
+    from paper_2502_10424_b200 import cli, model
+
+    cfgf = tmp_path / "c.json"
+    cfgf.write_text(json.dumps({"spec": {"gamma": 6}, "model": {"num_layers": 1}}))
+    args = cli.build_parser().parse_args(["gen-model", "--config", str(cfgf), "--seed", "5", "--out", str(tmp_path),
+                                          "--kv-quant", "false"])
+    cfg = cli.resolve_config(args)
+    assert cfg["spec"]["gamma"] == 6 and cfg["seed"] == 5 and cfg["quant"]["kv_quant"] is False
+    assert cfg["model"]["num_heads"] == 4 and cfg["spec"]["decode_len"] == 90
+    assert cli.main(["gen-model", "--config", str(cfgf), "--seed", "5", "--out", str(tmp_path)]) == 0
+    w = model.load_weights(tmp_path / "weights.qspw")
+    ref = model.init_weights(w.config, seed=7)
+    assert all(np.array_equal(a, b) for (_, a), (_, b) in zip(w.named_tensors(), ref.named_tensors()))
+    assert json.loads((tmp_path / "manifest.json").read_text())["seed"] == 5
