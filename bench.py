@@ -243,12 +243,21 @@ def prefill_into(args, wl, geo, fw, head, prompts, sinks):
                 yield cur
                 cur = {}
 
-    ids = [torch.from_numpy(p).cuda() for p in prompts]
-    with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.CUDNN_ATTENTION]):
-        logits = run_prefill_batch(geo, ids, fw.embedding, layers(), fw.final_norm, head, fw.rope, sinks,
-                                   dtype=torch.float16)
-    torch.cuda.synchronize()
-    return [int(torch.argmax(lg).item()) for lg in logits]
+    # prompts per pass: the f32 residual streams of a group must fit next to the caches
+    S = max(int(p.size) for p in prompts)
+    free, _ = torch.cuda.mem_get_info()
+    per_seq = S * geo.hidden * 4 * 2 + S * (geo.nq + 2 * geo.nk) * 2 * 3
+    group = max(1, min(len(prompts), int(0.6 * free) // per_seq))
+    firsts = []
+    for g0 in range(0, len(prompts), group):
+        ids = [torch.from_numpy(p).cuda() for p in prompts[g0:g0 + group]]
+        with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.CUDNN_ATTENTION]):
+            logits = run_prefill_batch(geo, ids, fw.embedding, layers(), fw.final_norm, head, fw.rope,
+                                       sinks[g0:g0 + group], dtype=torch.float16)
+        torch.cuda.synchronize()
+        firsts += [int(torch.argmax(lg).item()) for lg in logits]
+        del ids, logits
+    return firsts
 
 
 def build_workload(args, wl, seqs):
@@ -673,8 +682,9 @@ def main():
     geo, fw, qw, head_w, hcache, fcache, firsts, prompts, setup = build_workload(args, wl, seqs)
     use_graphs = not args.no_graphs
     modes = args.modes.split(",")
-    kr = kernel_roofline(geo, fw, qw, hcache, peak)
-    if fcache is not None:
+    # QS_BENCH_NO_KERNELS=1: skip the per-kernel timings (ncu launch-list runs count only the decode loop)
+    kr = {} if os.environ.get("QS_BENCH_NO_KERNELS") else kernel_roofline(geo, fw, qw, hcache, peak)
+    if fcache is not None and kr:
         kr["attn_fp16"] = kernel_fp16(geo, fcache, peak)
     if args.profile_kernels:
         print(json.dumps({"kernels": kr}))
@@ -702,10 +712,14 @@ def main():
     if "fp16_ar" in modes:
         ffirst = firsts
         if fcache is None:
-            del hcache
+            import gc
+
+            del hcache, qw  # the spec engines' graphs / runners die with them
+            gc.collect()
             torch.cuda.empty_cache()
             fcache, ffirst = fp16_cache(args, wl, geo, fw, head_w, prompts)
-            kr["attn_fp16"] = kernel_fp16(geo, fcache, peak)
+            if kr:
+                kr["attn_fp16"] = kernel_fp16(geo, fcache, peak)
         with clocks:
             barrier()
             t0 = time.time()
@@ -735,7 +749,7 @@ def main():
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return
-    dom = kr["attn_draft"]
+    dom = kr.get("attn_draft", {"gbs": 0.0, "bytes": 0.0})
     traffic, traffic_src = measured_traffic()
     cb = cpu_baseline(wl["context"], args.layers, geo=wl["model"])
     B = wl["batch"]
