@@ -453,6 +453,17 @@ class Config:
     max_positions: int
     rope_base: float = 10000.0
     norm_eps: float = 1e-5
+    # GQA (configs 4/5) has no reference model: SURVEY 8(c) restates it by repeating each KV head
+    # num_heads / num_kv_heads times into the reference's _merged_attention (None = MHA)
+    num_kv_heads: int | None = None
+
+    @property
+    def kv_heads(self) -> int:
+        return self.num_kv_heads or self.num_heads
+
+    @property
+    def kv_dim(self) -> int:
+        return self.kv_heads * self.head_dim
 
 
 MATS = ("wq", "wk", "wv", "wo", "w_gate", "w_up", "w_down")
@@ -466,7 +477,8 @@ def init_weights(cfg: Config, seed: int = 0) -> dict:
     """
     rng = np.random.default_rng(seed)
     d, m, vocab = cfg.hidden, cfg.mlp_hidden, cfg.vocab
-    shapes = {"wq": (d, d), "wk": (d, d), "wv": (d, d), "wo": (d, d),
+    kvd = cfg.kv_dim
+    shapes = {"wq": (d, d), "wk": (d, kvd), "wv": (d, kvd), "wo": (d, d),
               "w_gate": (d, m), "w_up": (d, m), "w_down": (m, d)}
 
     def draw(r, c):
@@ -548,8 +560,12 @@ def merged_attention(q: np.ndarray, segments, scale: float) -> np.ndarray:
     return (acc / den[:, None]).astype(F32)
 
 
-def attend_view(q: np.ndarray, view: View, nh: int, hd: int) -> np.ndarray:
-    segs = [(k.reshape(-1, nh, hd), v.reshape(-1, nh, hd)) for k, v in view.segments]
+def attend_view(q: np.ndarray, view: View, nh: int, hd: int, nkv: int | None = None) -> np.ndarray:
+    nkv = nkv or nh
+    r = nh // nkv
+    segs = [(k.reshape(-1, nkv, hd), v.reshape(-1, nkv, hd)) for k, v in view.segments]
+    if r > 1:  # GQA: each KV head serves r consecutive query heads
+        segs = [(np.repeat(k, r, axis=1), np.repeat(v, r, axis=1)) for k, v in segs]
     return merged_attention(q, segs, 1.0 / np.sqrt(hd))
 
 
@@ -588,16 +604,17 @@ def decode_step(weights: dict, token: int, cache, view: str = "fp", weight_mode:
     x = weights["embedding"][token].copy()
     for li, lw in enumerate(layers):
         h = rmsnorm(x, lw["attn_norm"], cfg.norm_eps)
+        nkv = cfg.kv_heads
         q = rope((h @ lw["wq"]).reshape(nh, hd), pos, cfg.rope_base)
-        k = rope((h @ lw["wk"]).reshape(nh, hd), pos, cfg.rope_base)
-        v = (h @ lw["wv"]).reshape(nh, hd)
-        cache.append_decode_token(li, k.reshape(d), v.reshape(d))
+        k = rope((h @ lw["wk"]).reshape(nkv, hd), pos, cfg.rope_base)
+        v = (h @ lw["wv"]).reshape(nkv, hd)
+        cache.append_decode_token(li, k.reshape(nkv * hd), v.reshape(nkv * hd))
         vw = cache.view(li, view)
         cost.kv_quantized_bytes += vw.quantized_bytes
         cost.kv_param_bytes += vw.param_bytes
         cost.kv_fp_bytes += vw.fp_bytes
         cost.kv_quantized_elements += vw.quantized_elements
-        ctx = attend_view(q, vw, nh, hd)
+        ctx = attend_view(q, vw, nh, hd, nkv)
         x = x + ctx.reshape(d) @ lw["wo"]
         hm = rmsnorm(x, lw["mlp_norm"], cfg.norm_eps)
         x = x + (silu(hm @ lw["w_gate"]) * (hm @ lw["w_up"])) @ lw["w_down"]
@@ -619,19 +636,21 @@ def prefill_kv(weights: dict, tokens) -> tuple[np.ndarray, list, list]:
     keys, vals = [], []
     for lw in weights["layers"]:
         h = rmsnorm(x, lw["attn_norm"], cfg.norm_eps)
+        nkv = cfg.kv_heads
         q = np.stack([rope(r, p, cfg.rope_base) for p, r in enumerate((h @ lw["wq"]).reshape(s, nh, hd))])
-        k = np.stack([rope(r, p, cfg.rope_base) for p, r in enumerate((h @ lw["wk"]).reshape(s, nh, hd))])
-        v = (h @ lw["wv"]).reshape(s, nh, hd)
-        sc = np.einsum("shd,thd->hst", q, k, dtype=F64) * (1.0 / np.sqrt(hd)) + mask
+        k = np.stack([rope(r, p, cfg.rope_base) for p, r in enumerate((h @ lw["wk"]).reshape(s, nkv, hd))])
+        v = (h @ lw["wv"]).reshape(s, nkv, hd)
+        kr, vr = (k, v) if nkv == nh else (np.repeat(k, nh // nkv, axis=1), np.repeat(v, nh // nkv, axis=1))
+        sc = np.einsum("shd,thd->hst", q, kr, dtype=F64) * (1.0 / np.sqrt(hd)) + mask
         sc -= sc.max(axis=2, keepdims=True)
         p = np.exp(sc)
         p /= p.sum(axis=2, keepdims=True)
-        ctx = np.einsum("hst,thd->shd", p, v, dtype=F64).astype(F32)
+        ctx = np.einsum("hst,thd->shd", p, vr, dtype=F64).astype(F32)
         x = x + ctx.reshape(s, cfg.hidden) @ lw["wo"]
         hm = rmsnorm(x, lw["mlp_norm"], cfg.norm_eps)
         x = x + (silu(hm @ lw["w_gate"]) * (hm @ lw["w_up"])) @ lw["w_down"]
-        keys.append(np.ascontiguousarray(k.reshape(s, cfg.hidden)))
-        vals.append(np.ascontiguousarray(v.reshape(s, cfg.hidden)))
+        keys.append(np.ascontiguousarray(k.reshape(s, cfg.kv_dim)))
+        vals.append(np.ascontiguousarray(v.reshape(s, cfg.kv_dim)))
     logits = rmsnorm(x[-1], weights["final_norm"], cfg.norm_eps) @ weights["lm_head"]
     return logits.astype(F32), keys, vals
 
@@ -641,7 +660,7 @@ def prefill(weights: dict, tokens, mode: str = "fp", group_size: int = 128, sens
     logits, keys, vals = prefill_kv(weights, tokens)
     cfg = weights["config"]
     if mode == "hierarchical":
-        lay = Layout(cfg.num_layers, cfg.num_heads, cfg.head_dim, group_size, frozenset(sensitive))
+        lay = Layout(cfg.num_layers, cfg.kv_heads, cfg.head_dim, group_size, frozenset(sensitive))
         return logits, OracleKVCache.from_prefill(lay, keys, vals)
     return logits, OracleFpCache(keys, vals)
 

@@ -805,3 +805,32 @@ def test_cli_run_and_ablate_measure_on_device(tmp_path):
     assert cli.main(["ablate", "--out", str(tmp_path / "a"), "--decode-len", "20"]) == 0
     lines = (tmp_path / "a" / "ablate.csv").read_text().strip().split("\n")
     assert [l.split(",")[0] for l in lines[1:]] == ["neither", "kv_only", "weight_only", "both"]
+
+
+@pytest.mark.parametrize("mode", ["draft", "target", "int4"])
+def test_gqa_forward_vs_oracle(mode):
+    """GQA model path (configs 4/5: the oracle repeats each KV head r times into the
+    reference's merged attention): bit-exact weights, prefill logits, and the draft / target /
+    INT4-weight decode logits on the same cache contents, at the fp16-weight tolerance."""
+    cfg = qs.ModelConfig(num_layers=2, num_heads=8, head_dim=16, hidden=128, mlp_hidden=176, vocab=96,
+                         max_positions=1024, num_kv_heads=2)
+    ocfg = O.Config(2, 8, 16, 128, 176, 96, 1024, num_kv_heads=2)
+    w, ow = qs.init_weights(cfg, seed=13), O.init_weights(ocfg, seed=13)
+    assert np.array_equal(w.layers[1].wk, ow["layers"][1]["wk"]) and w.layers[1].wk.shape == (128, 32)
+    prompt = np.random.default_rng(5).integers(0, 96, size=230)
+    lg0, cache = qs.prefill(w, prompt, "hierarchical", group_size=16)
+    olg0, _ = O.prefill(ow, prompt, "hierarchical", 16)
+    assert np.abs(lg0 - olg0).max() <= 2e-3 * max(1.0, float(np.abs(olg0).max()))
+    oc = _oracle_cache_like(cache)
+    ow16 = _f16_weights(ow)
+    if mode == "int4":
+        q = qs.quantize_model_weights(w, 32)
+        lg, _ = qs.decode_step(w, 17, cache, view="draft", weight_mode="int4", draft_weights=q)
+        olg, _ = O.decode_step(ow, 17, oc, "draft", "int4", O.quantize_model(ow, 32))
+        tol = 2e-3
+    else:
+        lg, _ = qs.decode_step(w, 17, cache, view=mode)
+        olg, _ = O.decode_step(ow16, 17, oc, mode)
+        tol = 2e-2
+    scale = max(1.0, float(np.abs(olg).max()))
+    assert np.abs(lg - olg).max() <= tol * scale, (mode, float(np.abs(lg - olg).max()))
