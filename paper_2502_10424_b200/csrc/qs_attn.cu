@@ -47,6 +47,13 @@ __device__ __forceinline__ void mma_nv(float (&d)[4], const uint32_t (&a)[4], ui
 }
 
 constexpr int PSTRIDE = 24;
+#ifndef QS_WAIT_SLEEP
+#define QS_WAIT_SLEEP 0  // A/B builds: ring waits suspend in hardware (try_wait with a time hint) instead of spinning
+#endif
+__device__ __forceinline__ void attn_wait(uint64_t* bar, uint32_t parity) {
+  if constexpr (QS_WAIT_SLEEP) mbar_wait_sleep(bar, parity);
+  else mbar_wait(bar, parity);
+}
 #ifndef QS_TGT_PLO
 #define QS_TGT_PLO 0  // target view P.V: p' as f16 hi only (1: hi + lo); |error| <= 2^-12 |p'|, as the draft view
 #endif
@@ -616,7 +623,11 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
     int s = pwid % S, ph = (pwid / S) & 1, s_prev = 0, ph_prev = 0;
     for (int j = pwid; j < nchunk; j += NPW) {
       uint8_t* sp = stage_ptr(s);
-      mbar_wait(&tma_b[s], ph);
+      attn_wait(&tma_b[s], ph);
+      // the consumers' release of this stage's previous chunk (j - S) -- already complete, since the
+      // refill that brought chunk j was issued after it, but that edge runs through another fold warp
+      // and the TMA engine; waiting here makes the fragment rewrite's ordering explicit (racecheck)
+      if (!C::TMAW && j >= S) attn_wait(&empty_b[s], ph ^ 1);
       const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + j) * QS_CHUNK_Q);
       const int nbl = (ntok_chunk + G - 1) >> lgG;
       const float2* kps = reinterpret_cast<const float2*>(sp + C::KP_OFF);
@@ -717,12 +728,12 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       if constexpr (C::TMAW) {
         // this warp's stage: refill it with chunk j + S once the consumers release chunk j
         if (j + S < nchunk) {
-          mbar_wait(&empty_b[s], ph);
+          attn_wait(&empty_b[s], ph);
           if (lane == 0) issue(j + S);
           __syncwarp();
         }
       } else if (jp >= 0 && jp + S < nchunk) {
-        mbar_wait(&empty_b[s_prev], ph_prev);
+        attn_wait(&empty_b[s_prev], ph_prev);
         if (lane == 0) issue(jp + S);
       }
       s_prev = s;
@@ -748,7 +759,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   const int mt = warp;
   for (int i = 0, s = 0, ph = 0; i < nchunk; ++i) {
     const uint8_t* sp = stage_ptr(s);
-    mbar_wait(&full_b[s], ph);
+    attn_wait(&full_b[s], ph);
     const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
     const bool live = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
     if (live) {
@@ -916,7 +927,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       sp[k] = stage_ptr(s);
       live[k] = false;
       if (i < nchunk) {
-        mbar_wait(&full_b[s], ph);
+        attn_wait(&full_b[s], ph);
         const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
         live[k] = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
       }

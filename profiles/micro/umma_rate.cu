@@ -37,7 +37,7 @@ __host__ __device__ inline uint32_t make_idesc(int M, int N) {
   return d;
 }
 
-template <int N, int K>
+template <int N, int K, int NACC, bool ATMEM>
 __global__ void umma_kernel(const __half* A, const __half* B, float* D, long long* cycles, int iters) {
   constexpr int M = 128;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -58,7 +58,9 @@ __global__ void umma_kernel(const __half* A, const __half* B, float* D, long lon
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
     asm volatile("fence.mbarrier_init.release.cluster;\n");
   }
-  constexpr uint32_t NCOL = N < 32 ? 32 : N;
+  constexpr uint32_t ACOL = ATMEM ? K / 2 : 0;  // A in tensor memory: K f16 = K/2 columns per row
+  constexpr uint32_t NC0 = N * NACC + ACOL < 32 ? 32 : N * NACC + ACOL;
+  constexpr uint32_t NCOL = NC0 <= 32 ? 32 : NC0 <= 64 ? 64 : NC0 <= 128 ? 128 : NC0 <= 256 ? 256 : 512;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)), "r"(NCOL));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -68,6 +70,27 @@ __global__ void umma_kernel(const __half* A, const __half* B, float* D, long lon
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = *tslot;
+  const uint32_t ta = tmem + (uint32_t)(N * NACC);  // A operand columns (ATMEM)
+  if constexpr (ATMEM) {
+    // row 32w + lane of A -> TMEM lane 32w + lane, k pairs -> consecutive columns
+    if (warp < 4) {
+      const int row = 32 * warp + (tid & 31);
+      uint32_t r[K / 2];
+#pragma unroll
+      for (int c = 0; c < K / 2; ++c) {
+        __half2 h = __halves2half2(A[row * K + 2 * c], A[row * K + 2 * c + 1]);
+        r[c] = *reinterpret_cast<uint32_t*>(&h);
+      }
+#pragma unroll
+      for (int c = 0; c < K / 2; c += 8)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta + ((uint32_t)(32 * warp) << 16) + c),
+                     "r"(r[c]), "r"(r[c + 1]), "r"(r[c + 2]), "r"(r[c + 3]), "r"(r[c + 4]), "r"(r[c + 5]), "r"(r[c + 6]), "r"(r[c + 7]));
+      asm volatile("tcgen05.wait::st.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+  }
   const uint64_t da = make_desc(smem_u32(sa), K), db = make_desc(smem_u32(sb), K);
   const uint32_t id = make_idesc(M, N);
   long long t0 = 0, t1 = 0;
@@ -78,11 +101,17 @@ __global__ void umma_kernel(const __half* A, const __half* B, float* D, long lon
       for (int ks = 0; ks < K / 16; ++ks) {
         // advance both descriptors by one 16-wide k step = two core matrices (2 * LBO bytes)
         const uint64_t step = (uint64_t)(ks * 2 * 128) >> 4;
-        const uint32_t acc = (it > 0 || ks > 0) ? 1u : 0u;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-            "l"(da + step), "l"(db + step), "r"(id), "r"(acc));
+        const uint32_t acc = (it >= NACC || ks > 0) ? 1u : 0u;
+        if constexpr (ATMEM)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem + (uint32_t)((it % NACC) * N)),
+              "r"(ta + (uint32_t)(ks * 8)), "l"(db + step), "r"(id), "r"(acc));
+        else
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (uint32_t)((it % NACC) * N)),
+              "l"(da + step), "l"(db + step), "r"(id), "r"(acc));
       }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar)));
@@ -110,7 +139,7 @@ __global__ void umma_kernel(const __half* A, const __half* B, float* D, long lon
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(NCOL));
 }
 
-template <int N, int K>
+template <int N, int K, int NACC = 1, bool ATMEM = false>
 void run(int nblocks, int iters) {
   constexpr int M = 128;
   std::vector<__half> a(M * K), b(N * K);
@@ -123,7 +152,7 @@ void run(int nblocks, int iters) {
   cudaMemcpy(dA, a.data(), M * K * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, b.data(), N * K * 2, cudaMemcpyHostToDevice);
   const int smem = M * K * 2 + N * K * 2 + 64;
-  auto kern = umma_kernel<N, K>;
+  auto kern = umma_kernel<N, K, NACC, ATMEM>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   // correctness: one pass (iters = 1) -> D = A . B^T
   kern<<<1, 128, smem>>>(dA, dB, dD, dc, 1);
@@ -145,8 +174,8 @@ void run(int nblocks, int iters) {
   double mean = 0;
   for (long long x : c) mean += (double)x / nblocks;
   const double per = mean / (iters * (K / 16));
-  printf("UMMA m128n%dk16 (K=%d per pass) blocks=%d: max|err| %.3g, %.2f cycles per UMMA, %.0f MAC/cycle/SM (HMMA.16816: ~2048)\n",
-         N, K, nblocks, maxerr, per, 128.0 * N * 16 / per);
+  printf("UMMA m128n%dk16 A in %s (K=%d per pass, %d independent accumulators) blocks=%d: max|err| %.3g, %.2f cycles per UMMA, %.0f MAC/cycle/SM (HMMA.16816: ~2048)\n",
+         N, ATMEM ? "TMEM" : "SMEM", K, NACC, nblocks, maxerr, per, 128.0 * N * 16 / per);
   cudaFree(dA); cudaFree(dB); cudaFree(dD); cudaFree(dc);
 }
 
@@ -159,5 +188,16 @@ int main() {
   run<128, 64>(1, 1024);
   run<256, 64>(1, 512);
   run<48, 64>(148, 1024);
+  run<16, 64, 4>(1, 1024);
+  run<32, 64, 4>(1, 1024);
+  run<48, 64, 4>(1, 1024);
+  run<48, 64, 8>(1, 1024);
+  run<64, 64, 4>(1, 1024);
+  run<128, 64, 2>(1, 1024);
+  run<16, 64, 4, true>(1, 1024);
+  run<48, 64, 1, true>(1, 1024);
+  run<48, 64, 4, true>(1, 1024);
+  run<64, 64, 4, true>(1, 1024);
+  run<128, 64, 2, true>(1, 1024);
   return 0;
 }

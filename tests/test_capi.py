@@ -50,8 +50,13 @@ def test_cubin_is_sm100a_and_uses_tensor_cores(lib_path):
     out = subprocess.run(["cuobjdump", "--list-elf", lib_path], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True).stdout
-    assert "HMMA" in sass  # tensor-core MMA in the attention / linear kernels
-    assert "UBLKCP" in sass  # TMA bulk copies staging the packed KV planes
+    # the decode contractions run as mma.sync (HMMA): at their N <= 48 columns a tcgen05 UMMA issues
+    # no faster (profiles/r02/umma_rate.txt: ~45 cycles per m128 k16 UMMA, <= 2160 MAC/cycle/SM vs
+    # 2048 for HMMA.16816); tensor memory holds the wide-query verify's parked accumulators
+    assert "HMMA" in sass
+    assert "LDTM" in sass and "STTM" in sass  # tcgen05.ld / tcgen05.st (TMEM accumulator parking)
+    assert "UTCATOMSWS" in sass  # tcgen05.alloc / dealloc
+    assert "UBLKCP" in sass  # TMA bulk copies staging the packed KV planes and weights
 
 
 def test_status_codes_map_to_reference_errors(lib_path):

@@ -103,3 +103,49 @@ def test_batch_state_machine_matches_oracle(toy):
             n_emitted += len(s.emitted)
         # tokens past the budget were still decoded for the batch, so compare up to the last record
         assert oc.quantized_token_count <= int(cache._nq[b])
+
+
+def _rank_worker(rank, world, port, out):
+    """One process per rank (both on cuda:0 here, one GPU each under torchrun): its partition of the
+    job's sequences in one ragged-batch engine, job accounting over the process group (bench.py)."""
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_10424_b200.parallel import job_throughput, partition
+
+        w = qs.init_weights(TOY, seed=7)
+        mine = list(partition(len(JOB), world, rank))
+        res, _ = _decode(w, [JOB[i] for i in mine], "int4", 30)
+        jt = job_throughput(sum(len(r.tokens) for r in res), 1.0 + rank)
+        out[rank] = (mine, [r.tokens for r in res], jt.total_units, jt.max_seconds)
+    finally:
+        dist.destroy_process_group()
+
+
+JOB = [np.random.default_rng(s).integers(0, 64, size=n) for s, n in ((41, 200), (42, 251), (43, 90), (44, 333), (45, 140))]
+
+
+def test_batch_partition_over_two_ranks_equals_one_batch(toy):
+    """Config 4's batch partition: 5 sequences over 2 ranks (3 + 2, each rank its own engine) emit
+    exactly the tokens of one 5-sequence batch, and the job accounting sums tokens / maxes time."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    ref, _ = _decode(toy, JOB, "int4", 30)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = mp.Manager().dict()
+    mp.spawn(_rank_worker, args=(2, port, out), nprocs=2, join=True)
+    got = {}
+    for r in range(2):
+        mine, toks, total, mx = out[r]
+        assert total == sum(len(x.tokens) for x in ref) and mx == 2.0
+        got.update(dict(zip(mine, toks)))
+    assert [got[i] for i in range(len(JOB))] == [r.tokens for r in ref]
