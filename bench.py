@@ -39,6 +39,9 @@ WORKLOADS = {
                          "gamma 4, greedy, mode=both (INT4 KV + INT4 draft weights)"),
     "config2": dict(model=LLAMA2_7B, shape="llama2_7b", context=32768, batch=1,
                     name="config2: Llama-2-7B shape random init, 32K ctx, batch 1 per GPU, gamma 4, greedy, mode=both"),
+    "config5": dict(model=LLAMA2_7B, shape="llama2_7b", context=131072, batch=1, shard_heads=True,
+                    name="config5: Llama-2-7B shape random init, ONE 128K sequence with its KV heads sharded over the "
+                         "GPUs (fused all-gather of the attention rows), gamma 4, greedy, mode=both"),
     "config4": dict(model=LLAMA31_8B, shape="llama31_8b", context=131072, batch=8,
                     name="config4: Llama-3.1-8B shape (GQA, 8 KV heads) random init, 128K ctx, batch 8 partitioned "
                          "batch-wise over the GPUs, gamma 4, greedy, mode=both"),
@@ -175,7 +178,7 @@ def weight_source(args, wl, geo):
             yield name, (t / math.sqrt(rows) if scaled else t)
 
 
-def build_weights(args, wl, geo):
+def build_weights(args, wl, geo, head_shard=None):
     """Packed fp16 (target) and INT4 g32 (draft) DeviceWeights + f32 embedding / lm_head, streamed one
     layer at a time so only packed copies stay resident.  Returns (fw, qw, emb, head)."""
     import torch
@@ -195,7 +198,12 @@ def build_weights(args, wl, geo):
             continue
         cur[name.split(".")[-1]] = t
         if len(cur) == 7:
-            qkv = torch.cat([cur["wq"], cur["wk"], cur["wv"]], dim=1)
+            wq, wk, wv = cur["wq"], cur["wk"], cur["wv"]
+            if head_shard is not None:  # this rank's query / KV head columns (KV-head sharding)
+                r, n = head_shard
+                qn, kn = geo.nq // n, geo.nk // n
+                wq, wk, wv = wq[:, r * qn:(r + 1) * qn], wk[:, r * kn:(r + 1) * kn], wv[:, r * kn:(r + 1) * kn]
+            qkv = torch.cat([wq, wk, wv], dim=1)
             f_layers.append(dict(qkv=PackedLinear.f16(qkv), o=PackedLinear.f16(cur["wo"]),
                                  gu=PackedLinear.f16_pair(cur["w_gate"], cur["w_up"]),
                                  down=PackedLinear.f16(cur["w_down"])))
@@ -274,21 +282,28 @@ def build_workload(args, wl, seqs):
     geo = Geometry(m["num_layers"], m["hidden"], m["num_heads"], m["num_kv_heads"], m["head_dim"], m["mlp_hidden"],
                    m["vocab"], S + margin)
     t0 = time.time()
-    fw, qw, emb, head = build_weights(args, wl, geo)
+    shard = wl.get("shard")  # (rank, world) of a KV-head-sharded single sequence
+    fw, qw, emb, head = build_weights(args, wl, geo, head_shard=shard)
     t_w = time.time() - t0
     B = len(seqs)
-    lay = CacheLayout(geo.num_layers, geo.num_heads, geo.head_dim, 128, num_kv_heads=geo.num_kv_heads)
+    nh, nkv = geo.num_heads, geo.num_kv_heads
+    if shard is not None:
+        nh, nkv = nh // shard[1], nkv // shard[1]
+    lay = CacheLayout(geo.num_layers, nh, geo.head_dim, 128, num_kv_heads=nkv)
     hcache = HierarchicalKVCache(lay, max_tokens=S + margin, batch=B)
     # fp16 baseline cache alongside when it fits (config 3: 64 GiB + 34 GiB store), else after the spec modes
-    fp_bytes = 2 * 2 * B * geo.num_layers * geo.nk * (S + margin)
+    kvd = nkv * geo.head_dim
+    fp_bytes = 2 * 2 * B * geo.num_layers * kvd * (S + margin)
     free, _ = torch.cuda.mem_get_info()
     fcache = None
     if fp_bytes < free - (24 << 30):
-        fcache = FpKVCache(geo.num_layers, geo.nk, capacity=S + margin, head_dim=geo.head_dim, batch=B)
+        fcache = FpKVCache(geo.num_layers, kvd, capacity=S + margin, head_dim=geo.head_dim, batch=B)
     prompts = prompts_for(args, wl, seqs)
+    loc = slice(shard[0] * kvd, (shard[0] + 1) * kvd) if shard is not None else slice(None)
 
     def sink(b):
         def f(l, k, v):
+            k, v = k[:, loc], v[:, loc]
             hcache.load_prefill_layer(l, k, v, seq=b)
             if fcache is not None:
                 fcache.load_prefill_layer(l, k, v, seq=b)
@@ -366,7 +381,7 @@ def time_graph(fns, reps: int = 5):
     return s.elapsed_time(e) / 1e3 / (reps * len(fns))
 
 
-def kernel_roofline(geo, fw, qw, hcache, peak):
+def kernel_roofline(geo, fw, qw, hcache, peak, shard=None):
     """Per-launch timings of the hot kernels at the bench context over this rank's sequences.
     Attention: isolated launches (each streams 0.1-9 GB >> the 126 MB L2).  Linear layers: the 32
     layers' matrices launched back to back from a graph (distinct weights, > L2), i.e. the in-forward
@@ -379,10 +394,10 @@ def kernel_roofline(geo, fw, qw, hcache, peak):
     out = {}
     B = hcache.batch
     G = hcache.layout.group_size
-    kv = geo.nk
+    kv = hcache.layout.kv_dim  # this rank's KV heads (all of them unless KV-head sharded)
     nq_tok = hcache.quantized_token_count
     nfp = hcache.fp1_len + hcache.fp2_len + 1
-    run = Runner(geo, hcache, max_cols=5 * B)
+    run = Runner(geo, hcache, max_cols=5 * B, shard=(shard[0], shard[1], None) if shard else None)
     run._rope = fw.rope  # the QKV epilogue's RoPE table (set by forward() in the decode loop)
     run.q.normal_()
     s = _lib.stream_ptr()
@@ -391,7 +406,7 @@ def kernel_roofline(geo, fw, qw, hcache, peak):
     for name, view, T in (("attn_draft", _lib.VIEW_DRAFT, 1), ("attn_verify", _lib.VIEW_TARGET, 5)):
         dt = time_kernel(lambda: run._attention(0, view, T, 0, s))
         algo = B * (nq_tok * per_tok["draft" if view == _lib.VIEW_DRAFT else "target"] + (nfp + T) * kv * 4.0
-                    + T * geo.nq * 8.0)
+                    + T * run.lgeo.nq * 8.0)
         out[name] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak,
                      "sequences": B}
     L = len(fw.layers)
@@ -451,7 +466,7 @@ def _binom_ci(acc: int, n: int) -> list:
 
 
 def measure_spec(geo, fw, dw, cache, first, gamma, steps, warmup, use_graphs, *, weight_mode, int4_bytes=0.0,
-                 long_drafted=1000):
+                 long_drafted=1000, runner=None):
     """Device time (CUDA events) and wall time of the SAME ``steps`` cycles of the public decode loop
     (SpeculativeDecoder.decode over a SpecEngine): per cycle the loop uploads the gamma_steps
     (pinned H2D), replays the captured cycle, and reads back (v, next, drafts, status); so the
@@ -466,7 +481,7 @@ def measure_spec(geo, fw, dw, cache, first, gamma, steps, warmup, use_graphs, *,
                       geo.max_positions, num_kv_heads=geo.num_kv_heads)
     dec = SpeculativeDecoder.for_device(cfg, SpecConfig(gamma=gamma, decode_len=1 << 30, weight_mode=weight_mode),
                                         fw, dw, int4_weight_bytes=int4_bytes, use_graphs=use_graphs)
-    eng = SpecEngine(fw, dw, cache, gamma, use_graphs=use_graphs)
+    eng = SpecEngine(fw, dw, cache, gamma, use_graphs=use_graphs, runner=runner)
     B = cache.batch
     pending = list(first) if isinstance(first, (list, tuple)) else [first] * B
     res = dec.decode(eng, pending, max_cycles=warmup, costs=False)
@@ -507,12 +522,12 @@ def measure_spec(geo, fw, dw, cache, first, gamma, steps, warmup, use_graphs, *,
     return out
 
 
-def measure_ar(fw, cache, first, steps, warmup, use_graphs):
+def measure_ar(fw, cache, first, steps, warmup, use_graphs, runner=None):
     import torch
 
     from paper_2502_10424_b200.engine import ARAutoEngine
 
-    eng = ARAutoEngine(fw, cache, use_graphs=use_graphs)
+    eng = ARAutoEngine(fw, cache, use_graphs=use_graphs, runner=runner)
     B = cache.batch
     eng.set_pending(list(first) if isinstance(first, (list, tuple)) else [first] * B)
     for _ in range(warmup):
@@ -677,13 +692,29 @@ def main():
     peak, peak_kind = load_peaks()
     wl = resolve(args)
     # config 4: the job's sequences partitioned batch-wise over the ranks (no data-path collective);
-    # configs 2/3: one sequence per GPU (replicas)
-    seqs = list(partition(wl["batch"], world, rank)) if wl["batch"] > 1 else [rank]
+    # configs 2/3: one sequence per GPU (replicas); config 5: ONE sequence, its KV heads over the ranks
+    sharded = bool(wl.get("shard_heads"))
+    if sharded:
+        wl["shard"] = (rank, world)
+        seqs = [0]
+    else:
+        seqs = list(partition(wl["batch"], world, rank)) if wl["batch"] > 1 else [rank]
     geo, fw, qw, head_w, hcache, fcache, firsts, prompts, setup = build_workload(args, wl, seqs)
     use_graphs = not args.no_graphs
     modes = args.modes.split(",")
+    shard = wl.get("shard")
+    kv_heads_local = hcache.layout.kv_heads
+
+    def spec_runner():
+        # KV-head sharding: the fused all-gather, buffers exchanged as CUDA IPC handles (collective)
+        from paper_2502_10424_b200.runtime import Runner
+
+        if not sharded:
+            return None
+        return Runner(geo, hcache, max_cols=args.gamma + 1, shard=(rank, world, None), gather="ipc")
+
     # QS_BENCH_NO_KERNELS=1: skip the per-kernel timings (ncu launch-list runs count only the decode loop)
-    kr = {} if os.environ.get("QS_BENCH_NO_KERNELS") else kernel_roofline(geo, fw, qw, hcache, peak)
+    kr = {} if os.environ.get("QS_BENCH_NO_KERNELS") else kernel_roofline(geo, fw, qw, hcache, peak, shard)
     if fcache is not None and kr:
         kr["attn_fp16"] = kernel_fp16(geo, fcache, peak)
     if args.profile_kernels:
@@ -703,10 +734,10 @@ def main():
         t0 = time.time()
         if "both" in modes:
             res["both"] = measure_spec(geo, fw, qw, hcache, firsts, args.gamma, args.steps, args.warmup, use_graphs,
-                                       weight_mode="int4", int4_bytes=qw.algorithmic_bytes())
+                                       weight_mode="int4", int4_bytes=qw.algorithmic_bytes(), runner=spec_runner())
         if "kv_only" in modes:
             res["kv_only"] = measure_spec(geo, fw, fw, hcache, firsts, args.gamma, args.steps, args.warmup, use_graphs,
-                                          weight_mode="fp")
+                                          weight_mode="fp", runner=spec_runner())
         barrier()
         t_timed += time.time() - t0
     if "fp16_ar" in modes:
@@ -723,7 +754,12 @@ def main():
         with clocks:
             barrier()
             t0 = time.time()
-            res["fp16_ar"] = measure_ar(fw, fcache, ffirst, args.steps, args.warmup, use_graphs)
+            ar_runner = None
+            if sharded:
+                from paper_2502_10424_b200.runtime import Runner
+
+                ar_runner = Runner(geo, fcache, max_cols=1, shard=(rank, world, None), gather="ipc")
+            res["fp16_ar"] = measure_ar(fw, fcache, ffirst, args.steps, args.warmup, use_graphs, runner=ar_runner)
             barrier()
             t_timed += time.time() - t0
     head = res.get("both") or res.get("kv_only")
@@ -739,6 +775,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         s2 = vals.clone()
         dist.all_reduce(s2, op=dist.ReduceOp.SUM)
+        if sharded:  # one sequence decoded by all ranks together: its tokens count once
+            s2 = s2 / world
         ms = float(t[0])
         value = float(s2[3]) / (ms * args.steps / 1e3)
         e2e = float(s2[3]) / float(t[1])
@@ -768,9 +806,10 @@ def main():
         "data": (f"synthetic: random-init weights ({'the reference init_weights stream, seed %d, replayed bit-exactly' % args.seed if args.weights == 'reference' else 'torch.randn on device, the reference recipe'}), "
                  f"uniform random prompt tokens (seed {args.seed}+1+b)"),
         "config": {"workload": wl["name"], "context": wl["context"], "layers": args.layers, "gamma": args.gamma,
-                   "batch_total": B, "batch_per_gpu": len(seqs),
+                   "batch_total": B, "batch_per_gpu": len(seqs), "kv_heads_per_gpu": kv_heads_local,
                    "l2": "working set per forward (GBs) >> 126 MB L2; no flush needed",
-                   "parallelism": (f"batch partition x{world} (no data-path collective)" if B > 1
+                   "parallelism": (f"KV-head sharding x{world} (fused all-gather in the attention merge)" if sharded
+                                   else f"batch partition x{world} (no data-path collective)" if B > 1
                                    else f"replicas x{world} (one sequence per GPU)"),
                    "cuda_graphs": use_graphs},
         "speedup_vs_fp16_ar": value / ar_job if ar_job else None,

@@ -294,7 +294,12 @@ class Runner:
 
             rank, world, group = shard
             if isinstance(gather, str):
-                gather = HeadGather.exchange(world, rank, max_cols, self.xh.shape[1], self.xs.shape[1], group)
+                import torch.distributed as dist
+
+                if world == 1 and not (dist.is_available() and dist.is_initialized()):
+                    gather = HeadGather(1, 0, max_cols, self.xh.shape[1], self.xs.shape[1])
+                else:
+                    gather = HeadGather.exchange(world, rank, max_cols, self.xh.shape[1], self.xs.shape[1], group)
             if (gather.rows, gather.ld_h, gather.ld_s) != (max_cols, self.xh.shape[1], self.xs.shape[1]):
                 raise ConfigError("gather buffers do not match the runner's activation rows")
             self.gather = gather

@@ -9,8 +9,9 @@ ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum 
     -k regex:attn_kernel -s 3 -c 1 --csv python bench.py --profile-kernels "$@" > gpurun_out/traffic_ncu.csv 2> gpurun_out/traffic_ncu.err
 python - <<'PY'
 import csv, hashlib, json, time
-rows = [r for r in csv.reader(open("gpurun_out/traffic_ncu.csv")) if len(r) > 5]
-hdr = rows[0]
+rows = list(csv.reader(open("gpurun_out/traffic_ncu.csv")))
+hdr = next(r for r in rows if r and r[0] == "ID")
+rows = [hdr] + [r for r in rows if len(r) == len(hdr) and r[0].isdigit()]
 iN, iV = hdr.index("Metric Name"), hdr.index("Metric Value")
 m = {r[iN]: float(r[iV].replace(",", "")) for r in rows[1:]}
 unit = {r[iN]: r[hdr.index("Metric Unit")] for r in rows[1:]}

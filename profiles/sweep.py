@@ -51,7 +51,12 @@ def main():
     from paper_2502_10424_b200.cache import CacheLayout, HierarchicalKVCache
     from paper_2502_10424_b200.runtime import Geometry, Runner
 
-    peak = 6557.4
+    import json
+
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, 'MEASURED_PEAKS.json')))['hbm_gbs'])
+    except Exception:
+        peak = 6459.6
     G, H, hd = 128, 32, 128
     kv = H * hd
     gammas = [int(g) for g in a.gammas.split(",")]
@@ -89,7 +94,7 @@ def main():
     # ---- K1 flush-quantise: one flush of all 32 layers (fp1 -> one quantised block per layer) ----
     L = 32
     lay = CacheLayout(L, H, hd, G)
-    c = HierarchicalKVCache(lay, max_tokens=8 * G)
+    c = HierarchicalKVCache(lay, max_tokens=(L + 8) * G)
     c.fp_k.normal_()
     c.fp_v.normal_()
     st = c.store_struct()
