@@ -360,7 +360,7 @@ __device__ __forceinline__ void quant_issue(const AttnParams& P, uint8_t* region
                                             int n_blocks, int c_begin, int i) {
   constexpr bool TGT = MODE == MODE_QTARGET;
   const int G = P.G;
-  const int bpc = QS_CHUNK_Q / G;
+  const int bpc = QS_CHUNK_Q >> (31 - __clz(G));  // G is a power of two: no integer division per issue
   const size_t plane_blk = (size_t)G * HD / 2;
   const size_t ph = ((size_t)seq * P.plane_seq_stride) + (size_t)head * P.plane_head_stride;
   const float2* kp = reinterpret_cast<const float2*>(P.kp) + (size_t)seq * P.kp_seq_stride + (size_t)head * P.kp_head_stride;
@@ -595,6 +595,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   const int lgG = 31 - __clz(G);
   const int n_blocks = P.n_blocks[seq];
   const int nchunk = c_end - c_begin;
+  const int tok_left = n_tok - c_begin * QS_CHUNK_Q;  // tokens from this CTA's first chunk on
   auto stage_ptr = [&](int s) { return region + s * C::QSTAGE; };
 
   if (warp >= C::NCW) {
@@ -760,8 +761,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   for (int i = 0, s = 0, ph = 0; i < nchunk; ++i) {
     const uint8_t* sp = stage_ptr(s);
     attn_wait(&full_b[s], ph);
-    const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
-    const bool live = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
+    const bool live = mt * 16 + i * QS_CHUNK_Q < tok_left && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
     if (live) {
       const int bl = (mt * 16) >> lgG;
       const uint4* aq = reinterpret_cast<const uint4*>(sp + C::BQ_OFF) + (size_t)bl * KS * NT * (C::AQ / 4) + lane;
@@ -928,8 +928,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       live[k] = false;
       if (i < nchunk) {
         attn_wait(&full_b[s], ph);
-        const int ntok_chunk = min(QS_CHUNK_Q, n_tok - (c_begin + i) * QS_CHUNK_Q);
-        live[k] = mt * 16 < ntok_chunk && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
+        live[k] = mt * 16 + i * QS_CHUNK_Q < tok_left && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
       }
       if (++s == S) {
         s = 0;
