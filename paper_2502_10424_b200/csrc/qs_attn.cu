@@ -57,8 +57,9 @@ __device__ __forceinline__ void attn_wait(uint64_t* bar, uint32_t parity) {
 #ifndef QS_TGT_PLO
 #define QS_TGT_PLO 0  // target view P.V: p' as f16 hi only (1: hi + lo); |error| <= 2^-12 |p'|, as the draft view
 #endif
-#ifndef QS_DRAFT_NPC
-#define QS_DRAFT_NPC 1
+#ifndef QS_DRAFT_TPW
+#define QS_DRAFT_TPW 1  // A/B: draft consumer warps own this many 16-token tiles of a chunk (2: 5% slower, and
+                         // breaks T-row == one-row invariance against the NT > 1 launches)
 #endif  // halves per P row (16 tokens + pad: conflict-free transposes)
 
 // NT: quantised modes -> query tiles of 8 queries (QK runs queries on the MMA M rows:
@@ -71,10 +72,10 @@ __device__ __forceinline__ void attn_wait(uint64_t* bar, uint32_t parity) {
 template <int HD, int NT, int MODE, int QR = 8>
 struct AttnCfg {
   static constexpr bool QUANT = MODE != MODE_FP16;
-  static constexpr int NCW = QUANT ? 8 : 4;            // compute warps
   static constexpr int KS = HD / 16;
   // target view: queries on the QK M rows (ROWQ); draft and fp16 views: hi/lo column pairs
   static constexpr bool ROWQ = MODE == MODE_QTARGET;
+  static constexpr int NCW = QUANT ? 8 / ((!ROWQ && NT == 1) ? QS_DRAFT_TPW : 1) : 4;  // compute warps
   static constexpr int NQ = ROWQ ? NT * 8 : NT * 4;      // queries per CTA
   static constexpr int NTO = NQ / 4;                     // hi/lo column-pair n-tiles of the fp16 path
   static constexpr int AQ = QR * 16;                     // words per (k-tile, query tile) of q' A fragments
@@ -100,10 +101,10 @@ struct AttnCfg {
   static constexpr int MERGE_BYTES = NCW * NQ * MS * 4;
   static constexpr int BQF_WORDS = ROWQ ? KS * NT * AQ : KS * NTO * 64;  // query fragments of fp16 chunks
   static constexpr int PW_HALVES = NTO * 8 * PSTRIDE;
-  // chunks a draft consumer warp carries per loop iteration (its tile of each): one online-softmax
-  // update, one P transpose round trip and one barrier round per NPC chunks, twice the MMA chains
-  static constexpr int NPC = (QUANT && !ROWQ && NT == 1) ? QS_DRAFT_NPC : 1;
-  static constexpr int PW_WARP = PW_HALVES * NPC;  // halves of P transpose buffer per warp
+  // 16-token tiles per consumer warp per chunk in the draft view (and the fp16 tails of a draft
+  // launch): TPW = 2 halves the consumer warps and shares each warp's per-chunk overhead over two tiles
+  static constexpr int TPW = (QUANT && !ROWQ && NT == 1) ? QS_DRAFT_TPW : 1;
+  static constexpr int PW_WARP = PW_HALVES * TPW;  // halves of P transpose buffer per warp
   static constexpr int FIXED = BQF_WORDS * 4 + NQ * HD * 4 + (ROWQ ? 0 : NCW * PW_WARP * 2) + 3 * 8 * 8 + 16;
   // TMA ring: two CTAs per SM when at least 4 stages fit each (of 228 KB, 1 KB reserved per CTA),
   // else one CTA with the deepest ring that fits; at most 6 stages
@@ -273,8 +274,6 @@ __device__ __forceinline__ void fp16_region(uint8_t* region, uint32_t* bqf, cons
     cp_async_commit();
   };
   for (int i = 0; i < C::NSTAGE_F - 1; ++i) issue_f(i);
-  const int mt = warp;
-  const bool has_tile = mt * 16 < CF && warp < C::NCW;
   for (int i = 0; i < nchunk; ++i) {
     if constexpr (C::NSTAGE_F == 1) {
       if (i > 0) __syncthreads();  // every warp is done with the previous chunk
@@ -285,7 +284,10 @@ __device__ __forceinline__ void fp16_region(uint8_t* region, uint32_t* bqf, cons
     }
     __syncthreads();
     if constexpr (C::NSTAGE_F > 1) issue_f(i + C::NSTAGE_F - 1);
-    if (!has_tile) continue;
+    // the warp's TPW 16-token tiles of the chunk, one after another (one softmax state per warp)
+    for (int tt = 0; tt < C::TPW; ++tt) {
+    const int mt = warp * C::TPW + tt;
+    if (!(mt * 16 < CF && warp < C::NCW)) continue;
     const int c = c_begin + i;
     const __half* ks_ = fstage(i % C::NSTAGE_F);
     const __half* vs_ = ks_ + CF * HD;
@@ -347,6 +349,7 @@ __device__ __forceinline__ void fp16_region(uint8_t* region, uint32_t* bqf, cons
       }
     }
     __syncwarp();
+    }
   }
   cp_async_wait<0>();
 }
@@ -907,78 +910,71 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
   }
   } else {
   // ======================= consumer warps =======================
-  // Warp mt owns the 16-token tile mt of every chunk and carries NPC consecutive chunks per
-  // iteration: their Q.K^T chains run interleaved, one online-softmax update covers all of them,
-  // and their P.V k-steps accumulate into the same registers in chunk order (the per-chunk
-  // latency chain -- barrier wait, shuffles, P transpose -- is paid once per NPC chunks).
-  constexpr int NP = C::NPC;
+  // Warp w owns the TPW consecutive 16-token tiles w*TPW .. w*TPW+TPW-1 of every chunk: their
+  // Q.K^T chains interleave and share the query fragments' shared-memory loads, one online-softmax
+  // update covers all of them, and the warp's per-chunk bookkeeping (barrier wait, shuffles,
+  // release) is paid once per TPW tiles.
+  constexpr int TP = C::TPW;
   const float sl2 = P.sm_scale_log2;
-  const int mt = warp;  // this warp's 16-token tile of every chunk
   // P' feeds P.V as f16 hi parts only (the lo columns stay zero): |error| <= 2^-12 |p'|, inside
   // the draft's fp16-level tolerance, and one split fewer per score
-  for (int i0 = 0, s = 0, ph = 0; i0 < nchunk; i0 += NP) {
-    const uint8_t* sp[NP];
-    bool live[NP];
-    int stg[NP];
+  const bool share_blk = TP == 1 || G >= 16 * TP;  // all of the warp's tiles in one (S,Z) block
+  for (int i = 0, s = 0, ph = 0; i < nchunk; ++i) {
+    const uint8_t* sp = stage_ptr(s);
+    attn_wait(&full_b[s], ph);
+    bool live[TP];
+    int bl[TP];
 #pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const int i = i0 + k;
-      stg[k] = s;
-      sp[k] = stage_ptr(s);
-      live[k] = false;
-      if (i < nchunk) {
-        attn_wait(&full_b[s], ph);
-        live[k] = mt * 16 + i * QS_CHUNK_Q < tok_left && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
-      }
-      if (++s == S) {
-        s = 0;
-        ph ^= 1;
-      }
+    for (int k = 0; k < TP; ++k) {
+      const int mt = warp * TP + k;
+      live[k] = mt * 16 + i * QS_CHUNK_Q < tok_left && !(P.dbg & 1);  // tiles are whole: G is a multiple of 16
+      bl[k] = (mt * 16) >> lgG;
     }
     if (live[0]) {  // live[k] implies live[k - 1]
-      const int bl = (mt * 16) >> lgG;
-      // ---- Q.K^T: A = K codes [tokens x channels], two accumulator chains per chunk ----
-      float d[NP][2][NT][4];
+      // ---- Q.K^T: A = K codes [tokens x channels], two accumulator chains per tile ----
+      float d[TP][2][NT][4];
 #pragma unroll
-      for (int k = 0; k < NP; ++k)
+      for (int k = 0; k < TP; ++k)
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int e = 0; e < 4; ++e) d[k][j][nt][e] = 0.f;
-      // both chunks' chains run unconditionally (a dead second chunk -- past the range or a
-      // partial tile -- reads finite codes and is masked to -inf below), so they interleave
-      uint32_t wu[NP][KS], wl[NP][KS];
+      // a dead second tile (partial last chunk) reads finite codes and is masked to -inf below
+      uint32_t wu[TP][KS], wl[TP][KS];
 #pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        load_words<KS>(reinterpret_cast<const uint32_t*>(sp[k]), mt, lane, wu[k]);
-        if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp[k] + 2 * C::PLANE_CHUNK), mt, lane, wl[k]);
+      for (int k = 0; k < TP; ++k) {
+        load_words<KS>(reinterpret_cast<const uint32_t*>(sp), warp * TP + k, lane, wu[k]);
+        if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp + 2 * C::PLANE_CHUNK), warp * TP + k, lane, wl[k]);
       }
+      const uint2* bq = reinterpret_cast<const uint2*>(sp + C::BQ_OFF) + lane;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
 #pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          const uint2* bqt = reinterpret_cast<const uint2*>(sp[k] + C::BQ_OFF) + (size_t)bl * KS * NT * 32 + lane;
-          uint32_t a[4];
-          if constexpr (TGT) unpack_u4l4_raw(wu[k][ks], wl[k][ks], a);
-          else unpack_u4_raw(wu[k][ks], a);
+        for (int nt = 0; nt < NT; ++nt) {
+          const uint2 b0 = bq[((size_t)bl[0] * KS * NT + ks * NT + nt) * 32];
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const uint2 b = bqt[(ks * NT + nt) * 32];
+          for (int k = 0; k < TP; ++k) {
+            uint2 b = b0;
+            if (k > 0 && !share_blk) b = bq[((size_t)bl[k] * KS * NT + ks * NT + nt) * 32];
+            uint32_t a[4];
+            if constexpr (TGT) unpack_u4l4_raw(wu[k][ks], wl[k][ks], a);
+            else unpack_u4_raw(wu[k][ks], a);
             mma_nv(d[k][ks & 1][nt], a, b.x, b.y);
           }
         }
       }
+      const float* bias = reinterpret_cast<const float*>(sp + C::BIAS_OFF);
+      const float2* vps = reinterpret_cast<const float2*>(sp + C::VP_OFF);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        float sv[2 * NP], p[2 * NP];
-        float2 sz[NP][2];
+        float sv[2 * TP], p[2 * TP];
+        float2 sz[TP][2];
 #pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          const float* bias = reinterpret_cast<const float*>(sp[k] + C::BIAS_OFF);
-          const float2* vps = reinterpret_cast<const float2*>(sp[k] + C::VP_OFF);
-          const float2 bb = *reinterpret_cast<const float2*>(bias + (bl * NQ + nt * 4 + t4) * 2);
+        for (int k = 0; k < TP; ++k) {
+          const int mt = warp * TP + k;
+          const float2 bb = *reinterpret_cast<const float2*>(bias + (bl[k] * NQ + nt * 4 + t4) * 2);
           sz[k][0] = vps[mt * 16 + g];
           sz[k][1] = vps[mt * 16 + g + 8];
           const float r0 = (d[k][0][nt][0] + d[k][0][nt][1]) + (d[k][1][nt][0] + d[k][1][nt][1]);
@@ -986,12 +982,12 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
           sv[2 * k] = live[k] ? (r0 + bb.x) * sl2 : kNegInf;
           sv[2 * k + 1] = live[k] ? (TGT ? (r1 + bb.y) : fmaf(r1, 0.0625f, bb.y)) * sl2 : kNegInf;
         }
-        const float alpha = softmax_update<2 * NP>(st[nt], sv, p);
+        const float alpha = softmax_update<2 * TP>(st[nt], sv, p);
         if (alpha != 1.0f) rescale<KS, NT>(acc, nt, alpha);
 #pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          if (k > 0 && !live[k]) {  // dead chunk: p' = 0 feeds its (finite) codes
-            __half* prow = pw + k * C::PW_HALVES + (nt * 8 + 2 * t4) * PSTRIDE;
+        for (int k = 0; k < TP; ++k) {
+          __half* prow = pw + k * C::PW_HALVES + (nt * 8 + 2 * t4) * PSTRIDE;
+          if (k > 0 && !live[k]) {  // dead tile: p' = 0 feeds its (finite) codes
             prow[g] = prow[g + 8] = __float2half_rn(0.f);
             continue;
           }
@@ -1000,21 +996,20 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
           const __half h0 = __float2half_rn(p[2 * k] * (sz[k][0].x * kvs));
           const __half h1 = __float2half_rn(p[2 * k + 1] * (sz[k][1].x * kvs));
           st[nt].ps += __half2float(h0) + __half2float(h1);
-          __half* prow = pw + k * C::PW_HALVES + (nt * 8 + 2 * t4) * PSTRIDE;
           prow[g] = h0;
           prow[g + 8] = h1;
         }
       }
       __syncwarp();
-      // ---- P.V: A = V^T codes [channels x tokens] of this token k-step, chunk by chunk ----
-      uint32_t bpv[NP][NT][2];
+      // ---- P.V: A = V^T codes [channels x tokens] of each tile's token k-step ----
+      uint32_t bpv[TP][NT][2];
 #pragma unroll
-      for (int k = 0; k < NP; ++k) get_pv_b<NT>(pw + k * C::PW_HALVES, g, t4, bpv[k]);
+      for (int k = 0; k < TP; ++k) get_pv_b<NT>(pw + k * C::PW_HALVES, g, t4, bpv[k]);
 #pragma unroll
-      for (int k = 0; k < NP; ++k) {
+      for (int k = 0; k < TP; ++k) {
         uint32_t vw[KS], vwl[KS];
-        load_words<KS>(reinterpret_cast<const uint32_t*>(sp[k] + C::PLANE_CHUNK), mt, lane, vw);
-        if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp[k] + 3 * C::PLANE_CHUNK), mt, lane, vwl);
+        load_words<KS>(reinterpret_cast<const uint32_t*>(sp + C::PLANE_CHUNK), warp * TP + k, lane, vw);
+        if constexpr (TGT) load_words<KS>(reinterpret_cast<const uint32_t*>(sp + 3 * C::PLANE_CHUNK), warp * TP + k, lane, vwl);
 #pragma unroll
         for (int cm = 0; cm < KS; ++cm) {
           uint32_t a[4];
@@ -1026,10 +1021,10 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       }
     }
     __syncwarp();
-    if (lane == 0) {
-#pragma unroll
-      for (int k = 0; k < NP; ++k)
-        if (i0 + k < nchunk) mbar_arrive(&empty_b[stg[k]]);
+    if (lane == 0) mbar_arrive(&empty_b[s]);
+    if (++s == S) {
+      s = 0;
+      ph ^= 1;
     }
   }
   }
