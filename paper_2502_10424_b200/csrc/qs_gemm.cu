@@ -258,7 +258,11 @@ struct I4Cfg {
   static constexpr int THREADS = (NCW + 1) * 32;
   static constexpr bool SINGLE = NTC == 1 && CW == 1;             // one activation row
   static constexpr int KCH = SINGLE ? QS_I4_KCH1 : 128;           // k-steps per stage
+#ifdef QS_I4_MINB1
+  static constexpr int MINB = SINGLE ? QS_I4_MINB1 : 1;             // A/B builds: resident CTAs per SM
+#else
   static constexpr int MINB = (SINGLE && KCH <= 64) ? 2 : 1;      // resident CTAs per SM
+#endif
   static constexpr int SMEM_CAP = MINB == 2 ? 233472 / 2 - 1024 : 232448;
   static constexpr int HKS = KCH / KP;                            // k-steps per consumer warp per stage
   static constexpr int WBYTES = (KCH / 4) * 2 * 512;              // codes of both tiles

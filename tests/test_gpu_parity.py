@@ -834,3 +834,21 @@ def test_gqa_forward_vs_oracle(mode):
         tol = 2e-2
     scale = max(1.0, float(np.abs(olg).max()))
     assert np.abs(lg - olg).max() <= tol * scale, (mode, float(np.abs(lg - olg).max()))
+
+
+def test_decode_time_flush_of_non_finite_kv_raises(toy):
+    """A non-finite K/V row reaching the decode-time flush (K1 inside the captured step) sets the
+    device status word; the per-step readback raises the reference's DataError (Q/quant.py:60-64,
+    reached from Q/cache.py:261-262) -- one step later than the reference, which raises before mutating."""
+    from paper_2502_10424_b200.engine import ARAutoEngine
+
+    w, _ = toy
+    prompt = np.random.default_rng(12).integers(0, 64, size=63)  # 32 quantised + fp1 16 + fp2 15 (G = 16)
+    _, cache = qs.prefill(w, prompt, "hierarchical", group_size=16)
+    assert (cache.fp1_len, cache.fp2_len) == (16, 15)
+    cache.fp_k[0, 1, 0, 0, 3, 5] = float("nan")  # layer 1, fp1, head 0, row 3
+    fw, _ = w.device()
+    eng = ARAutoEngine(fw, cache, use_graphs=False)
+    eng.set_pending([7])
+    with pytest.raises(qs.DataError):
+        eng.step()  # fp2 fills -> the flush quantises fp1 (with the NaN) -> status word -> DataError
