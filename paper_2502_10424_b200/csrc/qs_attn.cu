@@ -126,7 +126,10 @@ struct AttnCfg {
   static constexpr int REGION_Q = QUANT ? NSTAGE * QSTAGE : 0;
   static constexpr int R0 = REGION_Q > REGION_F ? REGION_Q : REGION_F;
   static constexpr int REGION = R0 > MERGE_BYTES ? R0 : MERGE_BYTES;
-  static constexpr int VPAD = 2 * NQ <= 8 ? 8 : 2 * NQ <= 16 ? 16 : 2 * NQ <= 32 ? 32 : 64;  // reduce-scatter width
+  // query slots the fold computes: the draft stores QR live queries per CTA (MHA draft: 1 of NQ = 4)
+  static constexpr int NQF = (!ROWQ && QR < 8 && QR < NQ) ? QR : NQ;  // QR = 8: every slot
+  static constexpr int VPAD = 2 * NQF <= 2 ? 2 : 2 * NQF <= 4 ? 4 : 2 * NQF <= 8 ? 8 : 2 * NQF <= 16 ? 16 :
+                              2 * NQF <= 32 ? 32 : 64;  // fold reduce-scatter width
   static constexpr int SMEM = REGION + FIXED;
   // wide-query verify (NT >= 2 query tiles: GQA r*T queries, or T > 8): the consumers' P.V
   // accumulators of every query tile live in tensor memory between chunks (32 columns per tile per
@@ -639,10 +642,11 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
       float* bias = reinterpret_cast<float*>(sp + C::BIAS_OFF);
       // q'_c = q_c * S_c as f16 hi/lo B fragments; per (block, query): bias = sum q Z - offset * sum(q').
       // All queries are processed together so the warp reductions overlap (ILP), not serialise.
+      constexpr int NQF = C::NQF;
       for (int bl = 0; bl < ((P.dbg & 2) ? 0 : nbl); ++bl) {
-        float zs[NQ], bs[NQ];
+        float zs[NQF], bs[NQF];
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) zs[q] = bs[q] = 0.f;
+        for (int q = 0; q < NQF; ++q) zs[q] = bs[q] = 0.f;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           const int cp = lane + 32 * k;
@@ -655,7 +659,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
             uint32_t* tb = C::ROWQ ? bqb + (size_t)(bl * KS + (cp >> 3)) * NT * C::AQ + (jj & 3) * 4 + 2 * (jj >> 2)
                                    : bqb + (size_t)(bl * KS + (cp >> 3)) * NT * 64 + (jj & 3) * 2 + (jj >> 2);
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
+            for (int q = 0; q < NQF; ++q) {
               if (q < nq) {
                 const float2 qv = QREG ? qr[QREG ? q : 0][k] : *reinterpret_cast<const float2*>(q_s + q * HD + 2 * cp);
                 const float v0 = qv.x * s0, v1 = qv.y * s1;
@@ -680,15 +684,15 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         }
         // warp reduce-scatter of the 2*NQ partial sums (zs then bs): each level halves
         // the values a lane holds, so 2*NQ-1 shuffles replace 5*2*NQ dependent ones
-        constexpr int V = C::VPAD;  // 2*NQ padded to a power of two
-        constexpr int LV = V == 8 ? 3 : V == 16 ? 4 : 5;  // levels (V = 64: five, two sums per lane)
+        constexpr int V = C::VPAD;  // 2*NQF padded to a power of two
+        constexpr int LV = V == 2 ? 1 : V == 4 ? 2 : V == 8 ? 3 : V == 16 ? 4 : 5;  // levels (V = 64: five, two sums per lane)
         float vals[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) vals[i] = 0.f;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
+        for (int q = 0; q < NQF; ++q) {
           vals[q] = zs[q];
-          vals[NQ + q] = bs[q];
+          vals[NQF + q] = bs[q];
         }
 #pragma unroll
         for (int l = 0, h = V / 2; l < LV; ++l, h >>= 1) {
@@ -706,17 +710,17 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
         if constexpr (V == 64) {
           // sum idx sits in lane idx >> 1, slot idx & 1
           const float z0 = __shfl_sync(0xffffffffu, vals[0], qq >> 1), z1 = __shfl_sync(0xffffffffu, vals[1], qq >> 1);
-          const float b0 = __shfl_sync(0xffffffffu, vals[0], (NQ + qq) >> 1);
-          const float b1 = __shfl_sync(0xffffffffu, vals[1], (NQ + qq) >> 1);
+          const float b0 = __shfl_sync(0xffffffffu, vals[0], (NQF + qq) >> 1);
+          const float b1 = __shfl_sync(0xffffffffu, vals[1], (NQF + qq) >> 1);
           z = (qq & 1) ? z1 : z0;
-          b = ((NQ + qq) & 1) ? b1 : b0;
+          b = ((NQF + qq) & 1) ? b1 : b0;
         } else {
           float tot = vals[0];
 #pragma unroll
           for (int o = 16 >> LV; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
           // lanes [idx << (5-LV), (idx+1) << (5-LV)) now hold sum idx (idx < NQ: zs, else bs)
           z = __shfl_sync(0xffffffffu, tot, qq << (5 - LV));
-          b = __shfl_sync(0xffffffffu, tot, (NQ + qq) << (5 - LV));
+          b = __shfl_sync(0xffffffffu, tot, (NQF + qq) << (5 - LV));
         }
         // draft tokens g of a 16-token tile carry 1024 + c, tokens g+8 carry (1024 + 16c) (scaled
         // by 1/16 after the MMA); target tokens carry 1032 + (16 c_u + c_l)
@@ -1466,7 +1470,12 @@ static cudaError_t launch_attn_nt(const AttnParams& p, int nt, int per, cudaStre
     }
   } else if constexpr (MODE == MODE_QDRAFT) {
     switch (nt) {
-      case 1: return launch_attn_t<HD, 1, MODE, 8>(p, s);
+      case 1:  // the fold computes only the live query slots (MHA: one)
+        switch (attn_qr(per)) {
+          case 1: return launch_attn_t<HD, 1, MODE, 1>(p, s);
+          case 2: return launch_attn_t<HD, 1, MODE, 2>(p, s);
+          default: return launch_attn_t<HD, 1, MODE, 8>(p, s);
+        }
       case 2: return launch_attn_t<HD, 2, MODE, 8>(p, s);
       case 3: return launch_attn_t<HD, 3, MODE, 8>(p, s);
       default: return cudaErrorInvalidValue;
@@ -1519,7 +1528,11 @@ static int occ_t() {
 template <int HD, int MODE>
 static int occ_h(int per) {
   const int nt = attention_nt(per, MODE);
-  if constexpr (MODE != MODE_QTARGET) {
+  if constexpr (MODE == MODE_QDRAFT) {
+    if (nt == 1) return attn_qr(per) == 1 ? occ_t<HD, 1, MODE, 1>() : attn_qr(per) == 2 ? occ_t<HD, 1, MODE, 2>()
+                                                                                        : occ_t<HD, 1, MODE, 8>();
+    return nt == 2 ? occ_t<HD, 2, MODE, 8>() : occ_t<HD, 3, MODE, 8>();
+  } else if constexpr (MODE != MODE_QTARGET) {
     return nt == 1 ? occ_t<HD, 1, MODE, 8>() : nt == 2 ? occ_t<HD, 2, MODE, 8>() : occ_t<HD, 3, MODE, 8>();
   } else {
     if (nt == 2) return occ_t<HD, 2, MODE, 8>();
