@@ -127,7 +127,7 @@ struct AttnCfg {
   static constexpr int R0 = REGION_Q > REGION_F ? REGION_Q : REGION_F;
   static constexpr int REGION = R0 > MERGE_BYTES ? R0 : MERGE_BYTES;
   // query slots the fold computes: the draft stores QR live queries per CTA (MHA draft: 1 of NQ = 4)
-  static constexpr int NQF = (!ROWQ && QR < 8 && QR < NQ) ? QR : NQ;  // QR = 8: every slot
+  static constexpr int NQF = (QR < 8 && QR < NQ) ? QR : NQ;  // QR = 8: every slot
   static constexpr int VPAD = 2 * NQF <= 2 ? 2 : 2 * NQF <= 4 ? 4 : 2 * NQF <= 8 ? 8 : 2 * NQF <= 16 ? 16 :
                               2 * NQF <= 32 ? 32 : 64;  // fold reduce-scatter width
   static constexpr int SMEM = REGION + FIXED;
