@@ -54,6 +54,9 @@ __device__ __forceinline__ void attn_wait(uint64_t* bar, uint32_t parity) {
   if constexpr (QS_WAIT_SLEEP) mbar_wait_sleep(bar, parity);
   else mbar_wait(bar, parity);
 }
+#ifndef QS_LAZY_MAX_LOG2
+#define QS_LAZY_MAX_LOG2 8  // draft online softmax: raise the reference max only past 2^8 (0: exact max every chunk)
+#endif
 #ifndef QS_TGT_PLO
 #define QS_TGT_PLO 0  // target view P.V: p' as f16 hi only (1: hi + lo); |error| <= 2^-12 |p'|, as the draft view
 #endif
@@ -171,11 +174,22 @@ struct Softmax {
 };
 
 // per-warp online softmax for the query column owned by this lane (t4)
-template <int NS>
+// LAZY: the running max is only a reference point -- it is raised (warp max, rescale) when some
+// score exceeds it by more than 2^QS_LAZY_MAX_LOG2 (p then stays <= 2^QS_LAZY_MAX_LOG2), which takes
+// the three max shuffles off most chunks' dependency chain; the result is normalised by the same
+// reference, so only the rounding of p changes (deterministic, independent of the other rows)
+template <int NS, bool LAZY = false>
 __device__ __forceinline__ float softmax_update(Softmax& st, const float (&s)[NS], float (&p)[NS]) {
   float mx = kNegInf;
 #pragma unroll
   for (int i = 0; i < NS; ++i) mx = fmaxf(mx, s[i]);
+  if constexpr (LAZY) {
+    if (!__any_sync(0xffffffffu, mx > st.m + (float)QS_LAZY_MAX_LOG2)) {
+#pragma unroll
+      for (int i = 0; i < NS; ++i) p[i] = ex2_approx(s[i] - st.m);
+      return 1.0f;
+    }
+  }
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
@@ -813,22 +827,32 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
             sv[j][e] = (TGT || j == 0) ? (raw + bb.x) * sl2 : fmaf(raw, 0.0625f, bb.y) * sl2;
           }
         float mx = fmaxf(fmaxf(sv[0][0], sv[0][1]), fmaxf(sv[1][0], sv[1][1]));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         float alpha = 1.0f;
-        if (mx > st[nt].m) {
-          alpha = ex2_approx(st[nt].m - mx);  // st.m == -inf -> 0
-          st[nt].l *= alpha;
-          st[nt].z *= alpha;
-          st[nt].ps *= alpha;
-          st[nt].m = mx;
+        // lazy reference max (softmax_update): the quad max / rescale only when a score runs
+        // 2^QS_LAZY_MAX_LOG2 past the current reference (warp-uniform decision)
+        // (not in the parked wide-query path: measured 3% slower there)
+        const bool upd = QS_LAZY_MAX_LOG2 == 0 || C::PARK ||
+                         __any_sync(0xffffffffu, mx > st[nt].m + (float)QS_LAZY_MAX_LOG2);
+        if (upd) {
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+          if (mx > st[nt].m) {
+            alpha = ex2_approx(st[nt].m - mx);  // st.m == -inf -> 0
+            st[nt].l *= alpha;
+            st[nt].z *= alpha;
+            st[nt].ps *= alpha;
+            st[nt].m = mx;
+          }
         }
         // the accumulator columns of query q = nt*8 + 2t + e live in this lane; its alpha in lanes g = q
         if constexpr (C::PARK) {
-          resc[nt] = __any_sync(0xffffffffu, alpha != 1.0f);
-          al0[nt] = __shfl_sync(0xffffffffu, alpha, 8 * t4);
-          al1[nt] = __shfl_sync(0xffffffffu, alpha, 8 * t4 + 4);
-        } else if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+          resc[nt] = upd && __any_sync(0xffffffffu, alpha != 1.0f);
+          al0[nt] = al1[nt] = 1.0f;
+          if (resc[nt]) {
+            al0[nt] = __shfl_sync(0xffffffffu, alpha, 8 * t4);
+            al1[nt] = __shfl_sync(0xffffffffu, alpha, 8 * t4 + 4);
+          }
+        } else if (upd && __any_sync(0xffffffffu, alpha != 1.0f)) {
           const float a0 = __shfl_sync(0xffffffffu, alpha, 8 * t4);
           const float a1 = __shfl_sync(0xffffffffu, alpha, 8 * t4 + 4);
 #pragma unroll
@@ -986,7 +1010,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
           sv[2 * k] = live[k] ? (r0 + bb.x) * sl2 : kNegInf;
           sv[2 * k + 1] = live[k] ? (TGT ? (r1 + bb.y) : fmaf(r1, 0.0625f, bb.y)) * sl2 : kNegInf;
         }
-        const float alpha = softmax_update<2 * TP>(st[nt], sv, p);
+        const float alpha = softmax_update<2 * TP, (QS_LAZY_MAX_LOG2 > 0)>(st[nt], sv, p);
         if (alpha != 1.0f) rescale<KS, NT>(acc, nt, alpha);
 #pragma unroll
         for (int k = 0; k < TP; ++k) {
