@@ -57,6 +57,9 @@ __device__ __forceinline__ void attn_wait(uint64_t* bar, uint32_t parity) {
 #ifndef QS_LAZY_MAX_LOG2
 #define QS_LAZY_MAX_LOG2 8  // draft online softmax: raise the reference max only past 2^8 (0: exact max every chunk)
 #endif
+#ifndef QS_PARK_MIN_NT
+#define QS_PARK_MIN_NT 3  // query tiles from which the verify's P.V accumulators live in TMEM (NT = 2 fits registers)
+#endif
 #ifndef QS_TGT_PLO
 #define QS_TGT_PLO 0  // target view P.V: p' as f16 hi only (1: hi + lo); |error| <= 2^-12 |p'|, as the draft view
 #endif
@@ -138,7 +141,7 @@ struct AttnCfg {
   // accumulators of every query tile live in tensor memory between chunks (32 columns per tile per
   // warp; warps w, w+4 share a lane quarter) -- one CTA streams a head's chunks once for all its
   // queries without the register file holding NT x 32 accumulators per thread
-  static constexpr bool PARK = ROWQ && NT >= 2;
+  static constexpr bool PARK = ROWQ && NT >= QS_PARK_MIN_NT;
   static constexpr int TMEM_COLS = !PARK ? 0 : (2 * NT * 32 <= 128 ? 128 : 256);
   // registers per thread: each SM sub-partition holds 16K registers and gets every 4th resident
   // warp, so the busiest one holds ceil(MIN_BLOCKS * NWARPS / 4) warps (8-register granules)

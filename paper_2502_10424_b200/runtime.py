@@ -28,6 +28,8 @@ from . import _lib
 from .errors import ConfigError
 
 SM_COUNT = 148
+# queries per CTA in the quantised target view (<= 24: three 8-query tiles); QS_TGT_GROUP for A/B runs
+_TGT_GROUP = int(__import__("os").environ.get("QS_TGT_GROUP", "24"))
 
 
 def _torch():
@@ -431,7 +433,7 @@ class Runner:
             a.n_queries = T * self.r
             quant_target = view == _lib.VIEW_TARGET and not self.is_fp and layer not in getattr(
                 self.cache.layout, "sensitive_layers", ())
-            a.n_qgroups = max(1, -(-a.n_queries // (24 if quant_target else 12)))
+            a.n_qgroups = max(1, -(-a.n_queries // (_TGT_GROUP if quant_target else 12)))
             a.n_main = self.splits_for(view if not self.is_fp else _lib.VIEW_FP16)
             a.row_offset = row_offset
             a.sm_scale_log2 = float(1.4426950408889634 / math.sqrt(geo.head_dim))
