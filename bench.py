@@ -357,6 +357,11 @@ def time_kernel(fn, iters: int = 21):
     return statistics.median(s.elapsed_time(e) for s, e in ev) / 1e3
 
 
+# QS_BENCH_ISOLATED=1: isolated launches only (the ncu captures of profiles/profile_kernels.sh count
+# launches; graph replays would shift their -s offsets)
+ISO_ONLY = bool(os.environ.get("QS_BENCH_ISOLATED"))
+
+
 def time_graph(fns, reps: int = 5):
     """Mean device time per call of the launches ``fns`` captured back to back in one CUDA graph
     (the decode loop's own launch mode, PDL included): the steady-state duration of a kernel inside
@@ -403,18 +408,24 @@ def kernel_roofline(geo, fw, qw, hcache, peak, shard=None):
     s = _lib.stream_ptr()
     per_tok = {"draft": kv * 1.0 + 8.0 * kv / G + 8.0 * math.ceil(kv / G),
                "target": kv * 2.0 + 8.0 * kv / G + 8.0 * math.ceil(kv / G)}
+    L = geo.num_layers
     for name, view, T in (("attn_draft", _lib.VIEW_DRAFT, 1), ("attn_verify", _lib.VIEW_TARGET, 5)):
-        dt = time_kernel(lambda: run._attention(0, view, T, 0, s))
+        dt_iso = time_kernel(lambda: run._attention(0, view, T, 0, s))
+        # in-forward steady state: the L layers' launches back to back from one graph (PDL lets each
+        # launch's barrier setup and first plane copies overlap its predecessor, as in the decode loop)
+        dt = dt_iso if ISO_ONLY else time_graph(
+            [(lambda li=li: run._attention(li, view, T, 0, _lib.stream_ptr())) for li in range(L)])
         algo = B * (nq_tok * per_tok["draft" if view == _lib.VIEW_DRAFT else "target"] + (nfp + T) * kv * 4.0
                     + T * run.lgeo.nq * 8.0)
-        out[name] = {"us": dt * 1e6, "bytes": algo, "gbs": algo / dt / 1e9, "frac": algo / dt / 1e9 / peak,
-                     "sequences": B}
+        out[name] = {"us": dt * 1e6, "us_isolated": dt_iso * 1e6, "bytes": algo, "gbs": algo / dt / 1e9,
+                     "frac": algo / dt / 1e9 / peak, "frac_isolated": algo / dt_iso / 1e9 / peak, "sequences": B,
+                     "timing": f"graph of {L} launches (layers' own stores)"}
     L = len(fw.layers)
     for name, ws in (("gemv_f16_down", [lw["down"] for lw in fw.layers]),
                      ("gemv_int4_down", [lw["down"] for lw in qw.layers]),
                      ("gemv_int4_qkv", [lw["qkv"] for lw in qw.layers]),
                      ("gemv_int4_gate_up", [lw["gu"] for lw in qw.layers]),
-                     ("gemv_f16_lm_head", [fw.lm_head])):
+                     ("gemv_f16_lm_head", [fw.lm_head])):  # lm_head: one matrix, isolated
         w = ws[0]
         src = (run.hh, run.hs) if w.K == geo.mlp_hidden else (run.xh, run.xs)
         src[0].normal_()
@@ -428,7 +439,7 @@ def kernel_roofline(geo, fw, qw, hcache, peak, shard=None):
         fns = [(lambda w_=w_, li=li: run._linear(w_, src, y, 1, epi, layer=li, stream=_lib.stream_ptr(), **kw))
                for li, w_ in enumerate(ws)]
         dt_iso = time_kernel(fns[0])
-        dt = time_graph(fns) if len(fns) > 1 else dt_iso
+        dt = time_graph(fns) if len(fns) > 1 and not ISO_ONLY else dt_iso
         algo = w.algorithmic_bytes() + 2.0 * w.K + 4.0 * w.N
         out[name] = {"us": dt * 1e6, "us_isolated": dt_iso * 1e6, "bytes": algo, "gbs": algo / dt / 1e9,
                      "frac": algo / dt / 1e9 / peak, "frac_isolated": algo / dt_iso / 1e9 / peak,

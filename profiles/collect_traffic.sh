@@ -5,7 +5,7 @@
 #   bash profiles/collect_traffic.sh [extra bench args]
 set -e
 mkdir -p gpurun_out
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+QS_BENCH_ISOLATED=1 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
     -k regex:attn_kernel -s 3 -c 1 --csv python bench.py --profile-kernels "$@" > gpurun_out/traffic_ncu.csv 2> gpurun_out/traffic_ncu.err
 python - <<'PY'
 import csv, hashlib, json, time
