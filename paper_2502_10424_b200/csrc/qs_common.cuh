@@ -319,4 +319,13 @@ __device__ __forceinline__ float warp_min_f(float v) {
   return v;
 }
 
+// INT4 weight params: slot of row g of group grp is g ^ i4_param_swz(grp).  One param load of
+// the W4A16 consumer reads, per quarter warp, rows {2q, 2q+1} of four groups 512 B (CW = 1) or
+// 256 B (CW = 2) apart -- the same banks without the swizzle (4-way conflict); the even XOR mask
+// 2 f(grp & 7), f = 0 2 1 3 2 0 3 1, makes those groups' slots distinct for CW = 1, 2 and 4.
+__host__ __device__ __forceinline__ int i4_param_swz(int grp) {
+  const int i = grp & 7;
+  return 2 * (((i >> 1) ^ ((i & 1) << 1)) & 3);
+}
+
 }  // namespace qs

@@ -235,7 +235,7 @@ __device__ __forceinline__ void act_prep_row(const float* __restrict__ xr, const
 // the (gate, up) rows of one output tile) over the FULL K range, so no tile spans CTAs:
 // the stream-K fix-up (partials through L2, a ticket, the last CTA's reduction) was the
 // limiter of these short INT4 launches.  Weights are stored pair-major
-// ([pair][k-quad][2 tiles][32 lanes][16 B], params [pair][group][2 tiles][8][float4]), so
+// ([pair][k-quad][2 tiles][32 lanes][16 B], params [pair][group][2 tiles][8 slots][float4], row g in slot g ^ i4_param_swz(group)), so
 // a 64-k-step stage of a pair is one contiguous bulk copy of codes and one of params.
 // Persistent: one CTA per SM takes pairs b, b + grid, ...; its TMA ring (up to 8 stages of 64
 // k-steps) runs straight across pair boundaries.  Warps 0-7: tile w&1, k-quarter w>>1 of every
@@ -291,11 +291,12 @@ struct I4Cfg {
 
 // HKS k-steps of one 16-row tile for one consumer warp (window / group-slot scheme of
 // int4_unit; pair-major strides).  wa: this lane's first uint4 of the k-range; bbase: B rows
-// at the k-range; pp: float4 params of the first group (this tile, row g); xsm: 16-sums.
+// at the k-range; pp: float4 params of the first group (this tile, slot 0), whose absolute group
+// index is gb (the slot of row g is g ^ i4_param_swz(group)); xsm: 16-sums.
 template <class C, int NTC, int GKS, int CW, bool NOMMA = false>
 __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uint8_t* bbase, const float4* pp,
                                          const float* xsm, const int nks, const int g, const int t4,
-                                         float (&acc)[NTC][4], const int brs, const int XW) {
+                                         float (&acc)[NTC][4], const int brs, const int XW, const int gb) {
   constexpr int G8 = 8 / CW;
   constexpr int WIN = (G8 * GKS < C::HKS) ? G8 * GKS : C::HKS;  // k-steps per window
   constexpr int NSLOT = WIN / GKS;
@@ -395,7 +396,7 @@ __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uin
         const int kk0 = gl * GKS;
         vg[e] = v8[e] = 0.f;
         if (sl < NSLOT && kk0 < nks) {
-          const float4 p = pp[gl * 16];  // {S_g, Z_g - 1024 S_g, S_g8 / 16, Z_g8 - 64 S_g8}
+          const float4 p = pp[gl * 16 + (g ^ i4_param_swz(gb + gl))];  // {S_g, Z_g - 1024 S_g, S_g8 / 16, Z_g8 - 64 S_g8}
           const float* xc = xsm + c * XW + kk0;
           float X;
           if (kk0 + GKS <= nks) {
@@ -552,17 +553,18 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS, I4Cfg<NTC, GKS, 
         const uint8_t* sp = sm + s * C::STAGE;
         const int ko = kp * C::HKS;
         const uint4* wa = reinterpret_cast<const uint4*>(sp) + (ko / 4) * 64 + tile * 32 + lane;
-        const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + (ko * 16 / WG) * 16 + tile * 8 + g;
+        const float4* pp = reinterpret_cast<const float4*>(sp + C::OFF_P) + (ko * 16 / WG) * 16 + tile * 8;
+        const int gb = (u * KCH + ko) * 16 / WG;  // absolute group index of pp
         const int kabs = u * KCH + ko;  // absolute k-step (activations built in-kernel)
         const float* xsm = act_in ? act_s + kabs : reinterpret_cast<const float*>(sp + C::OFF_X) + ko;
         const uint8_t* bb = act_in ? act_h + kabs * 32 : sp + C::OFF_B + ko * 32;
         const int brs = act_in ? C::ACT_ROW : C::BROW, xw = act_in ? C::ACT_SROW : C::XROW / 4;
         if (P.dbg & 2)
-          i4_steps<C, NTC, GKS, CW, true>(wa, bb, pp, xsm, min(nks, C::HKS), g, t4, acc, brs, xw);
+          i4_steps<C, NTC, GKS, CW, true>(wa, bb, pp, xsm, min(nks, C::HKS), g, t4, acc, brs, xw, gb);
         else if (nks >= C::HKS)
-          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, C::HKS, g, t4, acc, brs, xw);
+          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, C::HKS, g, t4, acc, brs, xw, gb);
         else
-          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, nks, g, t4, acc, brs, xw);
+          i4_steps<C, NTC, GKS, CW>(wa, bb, pp, xsm, nks, g, t4, acc, brs, xw, gb);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_b[s]);

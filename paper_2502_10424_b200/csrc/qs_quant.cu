@@ -257,18 +257,20 @@ __global__ void wq_frag_kernel(const float* __restrict__ w, WGeom geo, const flo
   frag[wi] = word;
 }
 
-// params, tile-pair major: float4 per [pair][group][2 tiles][g] (zeros for a padding tile)
+// params, tile-pair major: float4 per [pair][group][2 tiles][8 slots] (zeros for a padding tile);
+// row g of group grp sits in slot g ^ i4_param_swz(grp) (qs_common.cuh: the consumer lanes of one
+// load read four different groups, which the swizzle spreads over distinct banks)
 __global__ void wq_fragparams_kernel(WGeom geo, const float* __restrict__ s, const float* __restrict__ z,
                                      float4* __restrict__ out) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int MT = geo.d_out / 16, MT2 = (MT + 1) / 2 * 2;
   long long total = (long long)MT2 * geo.gpr * 8;
   if (i >= total) return;
-  int g = (int)(i & 7);
   long long rest = i >> 3;
   int wt = (int)(rest & 1);
   rest >>= 1;
   int grp = (int)(rest % geo.gpr);
+  int g = (int)(i & 7) ^ i4_param_swz(grp);
   int mt = (int)(rest / geo.gpr) * 2 + wt;
   if (mt >= MT) {
     out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
