@@ -188,8 +188,9 @@ __device__ __forceinline__ float softmax_update(Softmax& st, const float (&s)[NS
   for (int i = 0; i < NS; ++i) mx = fmaxf(mx, s[i]);
   if constexpr (LAZY) {
     if (!__any_sync(0xffffffffu, mx > st.m + (float)QS_LAZY_MAX_LOG2)) {
+      const float mu = st.m == kNegInf ? 0.f : st.m;  // a dead first tile: p = 0, not NaN
 #pragma unroll
-      for (int i = 0; i < NS; ++i) p[i] = ex2_approx(s[i] - st.m);
+      for (int i = 0; i < NS; ++i) p[i] = ex2_approx(s[i] - mu);
       return 1.0f;
     }
   }
@@ -197,14 +198,15 @@ __device__ __forceinline__ float softmax_update(Softmax& st, const float (&s)[NS
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
   float alpha = 1.0f;
-  if (mx > st.m) {
+  // the raise is decided per query on its own (column-reduced) max, so a query's reference --
+  // and every rounding after it -- does not depend on which other queries share the warp
+  if (mx > st.m + (LAZY ? (float)QS_LAZY_MAX_LOG2 : 0.f)) {
     alpha = ex2_approx(st.m - mx);  // st.m == -inf -> 0
     st.l *= alpha;
     st.z *= alpha;
     st.ps *= alpha;
     st.m = mx;
   }
-#pragma unroll
   const float mu = st.m == kNegInf ? 0.f : st.m;  // every score -inf: p = ex2(-inf) = 0, not NaN
 #pragma unroll
   for (int i = 0; i < NS; ++i) p[i] = ex2_approx(s[i] - mu);
@@ -841,15 +843,17 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
           }
         float mx = fmaxf(fmaxf(sv[0][0], sv[0][1]), fmaxf(sv[1][0], sv[1][1]));
         float alpha = 1.0f;
-        // lazy reference max (softmax_update): the quad max / rescale only when a score runs
-        // 2^QS_LAZY_MAX_LOG2 past the current reference (warp-uniform decision)
-        // (not in the parked wide-query path: measured 3% slower there)
+        // lazy reference max (softmax_update): a query's reference rises only when its max runs
+        // 2^QS_LAZY_MAX_LOG2 past it -- decided per query (quad max), the same rule in every
+        // instantiation, so a row's result does not depend on the rows sharing the launch; the
+        // quad max is skipped when no lane of the warp gets there (not in the parked wide-query
+        // path, where that test measured 3% slower)
         const bool upd = QS_LAZY_MAX_LOG2 == 0 || C::PARK ||
                          __any_sync(0xffffffffu, mx > st[nt].m + (float)QS_LAZY_MAX_LOG2);
         if (upd) {
           mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
           mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-          if (mx > st[nt].m) {
+          if (mx > st[nt].m + (float)QS_LAZY_MAX_LOG2) {
             alpha = ex2_approx(st[nt].m - mx);  // st.m == -inf -> 0
             st[nt].l *= alpha;
             st[nt].z *= alpha;
@@ -1251,6 +1255,9 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS) __maxnreg_
     c_begin = 0;
     c_end = fk ? (n_tok + C::CF - 1) / C::CF : 0;
   }
+  // diagnostics (profiles/attn_micro.py): 4 = the fp tail CTAs skip their chunks, 8 = the main ones do
+  if ((P.dbg & 4) && split >= n_main) c_end = c_begin;
+  if ((P.dbg & 8) && split < n_main) c_end = c_begin;
 
   uint32_t tacc = 0;  // this consumer warp's parked accumulators (TMEM lane quarter + column block)
   if constexpr (C::PARK) {

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--r", type=int, default=1, help="query heads per KV head (GQA: 4)")
     ap.add_argument("--batch", type=int, default=1, help="sequences per launch")
+    ap.add_argument("--graph", type=int, default=0, help="1: replay the launches from a CUDA graph")
     a = ap.parse_args()
     import torch
 
@@ -72,9 +73,19 @@ def main():
                     _lib.check(_lib.load().qs_attn_decode(args, mode, s))
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                if a.graph:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        for _ in range(a.iters):
+                            _lib.check(_lib.load().qs_attn_decode(args, mode, _lib.stream_ptr()))
+                    g.replay()
+                    torch.cuda.synchronize()
                 e0.record()
-                for _ in range(a.iters):
-                    _lib.check(_lib.load().qs_attn_decode(args, mode, s))
+                if a.graph:
+                    g.replay()
+                else:
+                    for _ in range(a.iters):
+                        _lib.check(_lib.load().qs_attn_decode(args, mode, s))
                 e1.record()
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) / a.iters * 1e3

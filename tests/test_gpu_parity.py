@@ -231,10 +231,10 @@ def _attn_setup(H, hd, G, n_prompt, extra, seed=0, r=1):
     return cache, orc, rows_k, rows_v, rng
 
 
-def _run_attention(cache, q, view, T, row_offset=0, r=1):
+def _run_attention(cache, q, view, T, row_offset=0, r=1, splits=None):
     lay = cache.layout
     geo = Geometry(1, lay.num_heads * lay.head_dim, lay.num_heads, lay.kv_heads, lay.head_dim, 16, 16, 1 << 20)
-    run = Runner(geo, cache, max_cols=16)
+    run = Runner(geo, cache, max_cols=32, attn_splits=splits)
     run.q[:T] = torch.from_numpy(q.reshape(T, -1)).cuda()
     run._attention(0, view, T, row_offset, _lib.stream_ptr())
     torch.cuda.synchronize()
@@ -294,19 +294,23 @@ def test_attention_gqa_vs_oracle(view, T):
         assert err <= 2e-3 * vmax, (t, err)
 
 
-def test_attention_batch_invariance_bit_exact():
-    """Row t of a T-row launch == the same row launched alone at its position."""
+@pytest.mark.parametrize("r,splits", [(1, None), (1, 1), (4, None), (4, 1)])
+def test_attention_batch_invariance_bit_exact(r, splits):
+    """Row t of a T-row launch == the same row launched alone at its position -- also when one CTA
+    streams many chunks (splits=1: the lazy softmax reference must be decided per query, not per
+    warp) and for GQA, where the T-row verify parks its accumulators in TMEM (r*T = 20 queries)
+    while a single row keeps them in registers."""
     H, hd, G = 4, 128, 128
-    cache, orc, rk, rv, rng = _attn_setup(H, hd, G, 3 * 128 + 17, 5, seed=11)
+    cache, orc, rk, rv, rng = _attn_setup(H, hd, G, 9 * 128 + 17, 5, seed=11, r=r)
     base = cache.fp2_len
     for t in range(5):
         cache.fp_k[0, 0, 1, :, base + t] = torch.from_numpy(rk[t]).cuda().half().reshape(H, hd)
         cache.fp_v[0, 0, 1, :, base + t] = torch.from_numpy(rv[t]).cuda().half().reshape(H, hd)
-    q = (rng.standard_normal((5, H, hd)) * 2.0).astype(np.float32)
+    q = (rng.standard_normal((5, H * r, hd)) * 2.0).astype(np.float32)
     for view in (_lib.VIEW_DRAFT, _lib.VIEW_TARGET):
-        full = _run_attention(cache, q, view, 5)
+        full = _run_attention(cache, q, view, 5, r=r, splits=splits)
         for t in range(5):
-            one = _run_attention(cache, q[t : t + 1], view, 1, row_offset=t)
+            one = _run_attention(cache, q[t : t + 1], view, 1, row_offset=t, r=r, splits=splits)
             assert np.array_equal(one[0], full[t]), (view, t)
 
 
