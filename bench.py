@@ -660,12 +660,17 @@ def reference_arm(args):
 
 
 def lib_digest() -> str:
+    """md5 over the CUDA sources and build flags of libqsb200.so (stable across rebuilds of the same
+    sources, unlike the .so's own bytes), so a traffic capture is tied to the code it measured."""
+    import glob
     import hashlib
 
-    from paper_2502_10424_b200 import _lib
-
-    with open(_lib.lib_path(), "rb") as f:
-        return hashlib.md5(f.read()).hexdigest()
+    h = hashlib.md5()
+    pkg = os.path.join(ROOT, "paper_2502_10424_b200")
+    for p in sorted(glob.glob(os.path.join(pkg, "csrc", "*"))) + [os.path.join(pkg, "_build.py")]:
+        with open(p, "rb") as f:
+            h.update(os.path.basename(p).encode() + b"\0" + f.read())
+    return h.hexdigest()
 
 
 def measured_traffic():

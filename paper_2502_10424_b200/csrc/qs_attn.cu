@@ -380,9 +380,12 @@ __device__ __forceinline__ void fp16_region(uint8_t* region, uint32_t* bqf, cons
 // into ring stage i % NSTAGE; completion is counted on tma_b[stage].  Reads only
 // blocks below n_blocks, which no kernel of a decode forward modifies, so the
 // first NSTAGE chunks are issued before the grid dependency resolves (PDL).
+#ifndef QS_ATTN_L2PF
+#define QS_ATTN_L2PF 0  // A/B: L2 bulk prefetch this many ring depths ahead of the TMA ring (0: off)
+#endif
 template <typename C, int HD, int MODE>
 __device__ __forceinline__ void quant_issue(const AttnParams& P, uint8_t* region, uint64_t* tma_b, int seq, int head,
-                                            int n_blocks, int c_begin, int i) {
+                                            int n_blocks, int c_begin, int i, int nchunk) {
   constexpr bool TGT = MODE == MODE_QTARGET;
   const int G = P.G;
   const int bpc = QS_CHUNK_Q >> (31 - __clz(G));  // G is a power of two: no integer division per issue
@@ -412,6 +415,22 @@ __device__ __forceinline__ void quant_issue(const AttnParams& P, uint8_t* region
   if constexpr (TGT) {
     bulk_g2s(sp + 2 * C::PLANE_CHUNK, P.kl + ph + b0 * plane_blk, pbytes, &tma_b[s]);
     bulk_g2s(sp + 3 * C::PLANE_CHUNK, P.vl + ph + b0 * plane_blk, pbytes, &tma_b[s]);
+  }
+  if constexpr (QS_ATTN_L2PF > 0) {
+    // the chunk one ring depth further on goes to L2 now: twice the ring's bytes in flight to DRAM
+    const int ip = i + C::NSTAGE * QS_ATTN_L2PF;
+    if (ip < nchunk) {
+      const int pb0 = (c_begin + ip) * bpc, pnb = min(bpc, n_blocks - pb0);
+      const uint32_t pby = (uint32_t)(pnb * plane_blk);
+      bulk_prefetch_l2(kp + (size_t)pb0 * HD, (uint32_t)(pnb * HD * 8));
+      bulk_prefetch_l2(vp + (size_t)pb0 * G, (uint32_t)(pnb * G * 8));
+      bulk_prefetch_l2(P.ku + ph + pb0 * plane_blk, pby);
+      bulk_prefetch_l2(P.vu + ph + pb0 * plane_blk, pby);
+      if constexpr (TGT) {
+        bulk_prefetch_l2(P.kl + ph + pb0 * plane_blk, pby);
+        bulk_prefetch_l2(P.vl + ph + pb0 * plane_blk, pby);
+      }
+    }
   }
 }
 
@@ -634,7 +653,7 @@ __device__ __forceinline__ void quant_region(uint8_t* region, uint64_t* bars, co
 
   if (warp >= C::NCW) {
     // ======================= producer warps (NPW) =======================
-    auto issue = [&](int i) { quant_issue<C, HD, MODE>(P, region, tma_b, seq, head, n_blocks, c_begin, i); };
+    auto issue = [&](int i) { quant_issue<C, HD, MODE>(P, region, tma_b, seq, head, n_blocks, c_begin, i, nchunk); };
     const int pwid = warp - C::NCW;
     // Producer warp p folds whole chunks j = p (mod NPW) on its own (no inter-warp
     // synchronisation: the per-chunk fold is a latency chain, so independent warps
@@ -1281,7 +1300,7 @@ __global__ void __launch_bounds__(AttnCfg<HD, NT, MODE, QR>::THREADS) __maxnreg_
     // PDL: the first ring stages of packed planes stream in before the grid dependency resolves
     if (region_kind == 0 && warp == NCW && lane == 0)
       for (int i = 0; i < C::NSTAGE && i < c_end - c_begin; ++i)
-        quant_issue<C, HD, MODE>(P, region, bars, seq, head, P.n_blocks[seq], c_begin, i);
+        quant_issue<C, HD, MODE>(P, region, bars, seq, head, P.n_blocks[seq], c_begin, i, c_end - c_begin);
   }
   pdl_wait();
   pdl_trigger();

@@ -251,6 +251,9 @@ __device__ __forceinline__ void act_prep_row(const float* __restrict__ xr, const
 #ifndef QS_I4_KCH1
 #define QS_I4_KCH1 128  // A/B builds: k-steps per stage of the single-row INT4 config
 #endif
+#ifndef QS_I4_L2PF
+#define QS_I4_L2PF 0  // A/B: L2 bulk prefetch this many ring depths ahead of the TMA ring (0: off)
+#endif
 template <int NTC, int GKS, int CW>
 struct I4Cfg {
   static constexpr int KP = 8;                                    // k-parts: warps per tile
@@ -498,6 +501,18 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS, I4Cfg<NTC, GKS, 
       bulk_g2s(sp, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)tp * (ks_pad / 4) + ks0 / 4) * 1024, wb, &full_b[s]);
       bulk_g2s(sp + C::OFF_P, reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)tp * gpr + ks0 * 16 / WG) * 256,
                pb, &full_b[s]);
+      if constexpr (QS_I4_L2PF > 0) {
+        // stage q + NSTAGE * L2PF to L2 now: the DRAM requests in flight are not capped by the ring
+        const int qp = q + C::NSTAGE * QS_I4_L2PF;
+        if (qp < total) {
+          const int tpp = blockIdx.x + (qp / nst) * gridDim.x, up = qp % nst;
+          const int pks0 = up * KCH, pnks = min(KCH, KS - pks0);
+          bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(P.w) + ((size_t)tpp * (ks_pad / 4) + pks0 / 4) * 1024,
+                           (uint32_t)((pnks + 3) / 4) * 1024);
+          bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(P.wparams) + ((size_t)tpp * gpr + pks0 * 16 / WG) * 256,
+                           (uint32_t)((pnks * 16 + WG - 1) / WG) * 256);
+        }
+      }
     };
     auto issue_act = [&](int q) {
       const int s = q % C::NSTAGE, u = q % nst;
@@ -607,6 +622,9 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS, I4Cfg<NTC, GKS, 
 // The schedule (grid = min(pairs, SMs), 8 k-parts per tile, fixed summation order) does not
 // depend on the number of activation rows, so a T-row verify equals T one-row steps bit for bit.
 // ---------------------------------------------------------------------------
+#ifndef QS_F16_L2PF
+#define QS_F16_L2PF 0  // A/B: L2 bulk prefetch this many ring depths ahead of the TMA ring (0: off)
+#endif
 template <int NTC>
 struct F16Cfg {
   static constexpr int KP = 8;
@@ -672,6 +690,14 @@ __global__ void __launch_bounds__(F16Cfg<NTC>::THREADS) linear_f16p_kernel(const
       const uint32_t wb = (uint32_t)nks * 1024, bb = (uint32_t)nks * 32;
       mbar_arrive_expect_tx(&full_b[s], wb + (act_in ? 0u : ncols * bb));
       bulk_g2s(sm + s * C::STAGE, reinterpret_cast<const uint8_t*>(P.w) + ((size_t)tp * KS + ks0) * 1024, wb, &full_b[s]);
+      if constexpr (QS_F16_L2PF > 0) {
+        const int qp = q + C::NSTAGE * QS_F16_L2PF;
+        if (qp < total) {
+          const int tpp = blockIdx.x + (qp / nst) * gridDim.x, up = qp % nst;
+          const int pks0 = up * KCH, pnks = min(KCH, KS - pks0);
+          bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(P.w) + ((size_t)tpp * KS + pks0) * 1024, (uint32_t)pnks * 1024);
+        }
+      }
     };
     auto issue_act = [&](int q) {
       const int s = q % C::NSTAGE, u = q % nst;

@@ -1,7 +1,7 @@
 #!/bin/bash
 # ncu DRAM bytes of the draft-attention launch that bench.py times (the 4th attn_kernel launch of
-# `bench.py --profile-kernels`), recorded with the md5 of the libqsb200.so it measured; bench.py
-# reports roofline.traffic only when the md5 matches the build it runs.   usage (under gpurun):
+# `bench.py --profile-kernels`), recorded with the md5 of the CUDA sources it measured (bench.lib_digest); bench.py
+# reports roofline.traffic only when the md5 matches the sources it runs.   usage (under gpurun):
 #   bash profiles/collect_traffic.sh [extra bench args]
 set -e
 mkdir -p gpurun_out
@@ -17,7 +17,7 @@ m = {r[iN]: float(r[iV].replace(",", "")) for r in rows[1:]}
 unit = {r[iN]: r[hdr.index("Metric Unit")] for r in rows[1:]}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 b = sum(m[k] * scale[unit[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-md5 = hashlib.md5(open("paper_2502_10424_b200/libqsb200.so", "rb").read()).hexdigest()
+import sys; sys.path.insert(0, "."); import bench; md5 = bench.lib_digest()
 out = {"attn_draft_bytes_per_launch": b, "lib_md5": md5, "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
        "kernel_us": m.get("gpu__time_duration.sum"), "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum, 4th attn_kernel launch of bench.py --profile-kernels"}
 json.dump(out, open("profiles/traffic.json", "w"), indent=1)
