@@ -248,19 +248,25 @@ __device__ __forceinline__ void act_prep_row(const float* __restrict__ xr, const
 #ifndef QS_I4_CHAINS
 #define QS_I4_CHAINS 2  // A/B builds: MMA accumulator chains per window (power of two)
 #endif
+#ifndef QS_I4_KP1
+#define QS_I4_KP1 8  // k-parts (consumer warps per tile) of the single-row INT4 config (A/B: 4 is 4% faster in
+                     // isolation but 1.3% slower over the whole decode cycle, profiles/r02/NOTES.md)
+#endif
 #ifndef QS_I4_KCH1
 #define QS_I4_KCH1 128  // A/B builds: k-steps per stage of the single-row INT4 config
 #endif
 #ifndef QS_I4_L2PF
 #define QS_I4_L2PF 0  // A/B: L2 bulk prefetch this many ring depths ahead of the TMA ring (0: off)
 #endif
-template <int NTC, int GKS, int CW>
+// KC: k-steps per stage of the single-row config (0: QS_I4_KCH1); with QS_I4_BIGK the dispatch takes 256
+// for K <= QS_I4_BIGK (A/B: with 4 k-parts 8% faster in isolation, slower inside the decode cycle)
+template <int NTC, int GKS, int CW, int KC = 0>
 struct I4Cfg {
-  static constexpr int KP = 8;                                    // k-parts: warps per tile
+  static constexpr bool SINGLE = NTC == 1 && CW == 1;             // one activation row
+  static constexpr int KP = SINGLE ? QS_I4_KP1 : 8;               // k-parts: warps per tile
   static constexpr int NCW = 2 * KP;                              // tile w&1, k-part w>>1
   static constexpr int THREADS = (NCW + 1) * 32;
-  static constexpr bool SINGLE = NTC == 1 && CW == 1;             // one activation row
-  static constexpr int KCH = SINGLE ? QS_I4_KCH1 : 128;           // k-steps per stage
+  static constexpr int KCH = SINGLE ? (KC ? KC : QS_I4_KCH1) : 128;  // k-steps per stage
 #ifdef QS_I4_MINB1
   static constexpr int MINB = SINGLE ? QS_I4_MINB1 : 1;             // A/B builds: resident CTAs per SM
 #else
@@ -436,6 +442,107 @@ __device__ __forceinline__ void i4_steps(const uint4* __restrict__ wa, const uin
   }
 }
 
+#ifndef QS_I4_EARLY
+#define QS_I4_EARLY 0  // A/B builds: single-row consumers copy their stage slice to registers and release it first
+#endif
+// Single activation row (NTC = CW = 1), early release: the warp's codes, its two param slots per
+// window, its own slot's B words and the 16-sums are copied into registers first, the stage is
+// handed back to the producer (`release`), and the MMA chain then runs from registers -- the ring
+// stage is held for one round of shared loads instead of the whole window.  Same operations in the
+// same order as i4_steps, so the results are bit-identical.
+template <class C, int GKS, class Rel>
+__device__ __forceinline__ void i4_steps_early(const uint4* __restrict__ wa, const uint8_t* bbase, const float4* pp,
+                                               const float* xsm, const int nks, const int g, const int t4,
+                                               float (&acc)[1][4], const int gb, Rel release) {
+  constexpr int WIN = (8 * GKS < C::HKS) ? 8 * GKS : C::HKS;  // k-steps per window
+  constexpr int NSLOT = WIN / GKS;
+  constexpr int NW = C::HKS / WIN;
+  constexpr int NQ4 = (C::HKS + 3) / 4;
+  uint4 wr[NQ4];
+  uint32_t xb[NW][GKS][2];
+  float4 pr[NW][2];
+  float X[NW][2];
+#pragma unroll
+  for (int i = 0; i < NQ4; ++i) wr[i] = (4 * i < nks) ? wa[i * 64] : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int k0 = w * WIN;
+#pragma unroll
+    for (int j = 0; j < GKS; ++j) {
+      const int ks = k0 + g * GKS + j;
+      const bool ok = g < NSLOT && ks < nks;
+      xb[w][j][0] = ok ? *reinterpret_cast<const uint32_t*>(bbase + 4 * t4 + ks * 32) : 0u;
+      xb[w][j][1] = ok ? *reinterpret_cast<const uint32_t*>(bbase + 4 * t4 + ks * 32 + 16) : 0u;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int sl = 2 * t4 + e, gl = k0 / GKS + sl, kk0 = gl * GKS;
+      pr[w][e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      X[w][e] = 0.f;
+      if (sl < NSLOT && kk0 < nks) {
+        pr[w][e] = pp[gl * 16 + (g ^ i4_param_swz(gb + gl))];
+        const float* xc = xsm + kk0;
+        if (kk0 + GKS <= nks) {
+          X[w][e] = sum_n<GKS>(xc);
+        } else {
+          for (int q = 0; q < nks - kk0; ++q) X[w][e] = __fadd_rn(X[w][e], xc[q]);
+        }
+      }
+    }
+  }
+  release();
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int k0 = w * WIN;
+    if (k0 >= nks) break;
+    constexpr int NCH = QS_I4_CHAINS;
+    float D2[NCH][4];
+#pragma unroll
+    for (int c2 = 0; c2 < NCH; ++c2)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) D2[c2][e] = 0.f;
+#pragma unroll
+    for (int sl = 0; sl < NSLOT; ++sl) {
+      const bool mine = g == sl;
+#pragma unroll
+      for (int j = 0; j < GKS; ++j) {
+        const int ks = k0 + sl * GKS + j;
+        if (ks < nks) {
+          const uint4 w4 = wr[ks >> 2];
+          const uint32_t wv = (ks & 3) == 0 ? w4.x : (ks & 3) == 1 ? w4.y : (ks & 3) == 2 ? w4.z : w4.w;
+          uint32_t a[4];
+          unpack_u4_raw(wv, a);
+          mma_acc(D2[(sl * GKS + j) % NCH], a, mine ? xb[w][j][0] : 0u, mine ? xb[w][j][1] : 0u);
+        }
+      }
+    }
+    float D[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float t[NCH];
+#pragma unroll
+      for (int c2 = 0; c2 < NCH; ++c2) t[c2] = D2[c2][e];
+#pragma unroll
+      for (int h = NCH / 2; h > 0; h >>= 1)
+#pragma unroll
+        for (int c2 = 0; c2 < h; ++c2) t[c2] = __fadd_rn(t[c2], t[c2 + h]);
+      D[e] = t[0];
+    }
+    float vg[2], v8[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int sl = 2 * t4 + e, kk0 = (k0 / GKS + sl) * GKS;
+      vg[e] = v8[e] = 0.f;
+      if (sl < NSLOT && kk0 < nks) {
+        vg[e] = __fmaf_rn(pr[w][e].x, D[e], __fmul_rn(pr[w][e].y, X[w][e]));
+        v8[e] = __fmaf_rn(pr[w][e].z, D[e + 2], __fmul_rn(pr[w][e].w, X[w][e]));
+      }
+    }
+    acc[0][0] = __fadd_rn(acc[0][0], __fadd_rn(vg[0], vg[1]));
+    acc[0][2] = __fadd_rn(acc[0][2], __fadd_rn(v8[0], v8[1]));
+  }
+}
+
 // CW == 1: sum the four lanes' slot partials of rows g, g+8 (every lane of the quad ends with the total)
 template <int NTC, int CW>
 __device__ __forceinline__ void i4_quad_sum(float (&acc)[NTC][4]) {
@@ -450,9 +557,9 @@ __device__ __forceinline__ void i4_quad_sum(float (&acc)[NTC][4]) {
   }
 }
 
-template <int NTC, int EPI, int GKS, int CW>
-__global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS, I4Cfg<NTC, GKS, CW>::MINB) linear_i4_kernel(const __grid_constant__ LinearParams P) {
-  using C = I4Cfg<NTC, GKS, CW>;
+template <int NTC, int EPI, int GKS, int CW, int KC = 0>
+__global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW, KC>::THREADS, I4Cfg<NTC, GKS, CW, KC>::MINB) linear_i4_kernel(const __grid_constant__ LinearParams P) {
+  using C = I4Cfg<NTC, GKS, CW, KC>;
   constexpr int COLS = 8 * NTC;
   constexpr int KCH = C::KCH;
   extern __shared__ __align__(128) uint8_t sm[];
@@ -574,6 +681,21 @@ __global__ void __launch_bounds__(I4Cfg<NTC, GKS, CW>::THREADS, I4Cfg<NTC, GKS, 
         const float* xsm = act_in ? act_s + kabs : reinterpret_cast<const float*>(sp + C::OFF_X) + ko;
         const uint8_t* bb = act_in ? act_h + kabs * 32 : sp + C::OFF_B + ko * 32;
         const int brs = act_in ? C::ACT_ROW : C::BROW, xw = act_in ? C::ACT_SROW : C::XROW / 4;
+        if constexpr (QS_I4_EARLY && C::SINGLE) {
+          auto release = [&] {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_b[s]);
+          };
+          if (nks >= C::HKS)
+            i4_steps_early<C, GKS>(wa, bb, pp, xsm, C::HKS, g, t4, acc, gb, release);
+          else
+            i4_steps_early<C, GKS>(wa, bb, pp, xsm, nks, g, t4, acc, gb, release);
+          if (++s == C::NSTAGE) {
+            s = 0;
+            ph ^= 1;
+          }
+          continue;
+        }
         if (P.dbg & 2)
           i4_steps<C, NTC, GKS, CW, true>(wa, bb, pp, xsm, min(nks, C::HKS), g, t4, acc, brs, xw, gb);
         else if (nks >= C::HKS)
@@ -830,10 +952,10 @@ static cudaError_t launch_f16p_e(const LinearParams& p, cudaStream_t s) {
   }
 }
 
-template <int NTC, int EPI, int GKS, int CW>
+template <int NTC, int EPI, int GKS, int CW, int KC>
 static cudaError_t launch_i4_t(const LinearParams& p, cudaStream_t s) {
-  using C = I4Cfg<NTC, GKS, CW>;
-  auto kern = linear_i4_kernel<NTC, EPI, GKS, CW>;
+  using C = I4Cfg<NTC, GKS, CW, KC>;
+  auto kern = linear_i4_kernel<NTC, EPI, GKS, CW, KC>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -851,19 +973,24 @@ static cudaError_t launch_i4_t(const LinearParams& p, cudaStream_t s) {
   return launch_pdl(kern, dim3(pairs < slots ? pairs : slots), dim3(C::THREADS), C::SMEM, s, p);
 }
 
-template <int NTC, int GKS, int CW>
+template <int NTC, int GKS, int CW, int KC = 0>
 static cudaError_t launch_i4_e(const LinearParams& p, cudaStream_t s) {
   switch (p.epi) {
-    case QS_EPI_STORE: return launch_i4_t<NTC, QS_EPI_STORE, GKS, CW>(p, s);
-    case QS_EPI_ADD: return launch_i4_t<NTC, QS_EPI_ADD, GKS, CW>(p, s);
-    case QS_EPI_QKV: return launch_i4_t<NTC, QS_EPI_QKV, GKS, CW>(p, s);
-    case QS_EPI_SILU_MUL: return launch_i4_t<NTC, QS_EPI_SILU_MUL, GKS, CW>(p, s);
+    case QS_EPI_STORE: return launch_i4_t<NTC, QS_EPI_STORE, GKS, CW, KC>(p, s);
+    case QS_EPI_ADD: return launch_i4_t<NTC, QS_EPI_ADD, GKS, CW, KC>(p, s);
+    case QS_EPI_QKV: return launch_i4_t<NTC, QS_EPI_QKV, GKS, CW, KC>(p, s);
+    case QS_EPI_SILU_MUL: return launch_i4_t<NTC, QS_EPI_SILU_MUL, GKS, CW, KC>(p, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int GKS>
 static cudaError_t launch_i4_n(const LinearParams& p, cudaStream_t s) {
+#ifndef QS_I4_BIGK
+#define QS_I4_BIGK 0  // A/B: single-row launches with K <= this stream 256-k-step stages (0: never)
+#endif
+  if constexpr (QS_I4_BIGK > 0)
+    if (p.ncols == 1 && p.K <= QS_I4_BIGK) return launch_i4_e<1, GKS, 1, 256>(p, s);
   if (p.ncols == 1) return launch_i4_e<1, GKS, 1>(p, s);
   if (p.ncols == 2) return launch_i4_e<1, GKS, 2>(p, s);
   if (p.ncols <= 4) return launch_i4_e<1, GKS, 4>(p, s);

@@ -4,10 +4,11 @@ context 4K-256K for the draft view (T=1) and the verify view (T = gamma+1,
 gamma 1..8), plus the flush-quantise kernel (K1) per flush, on a synthetic
 Llama-2-7B-shaped store (32 KV heads, hd 128, G 128; one layer).
 
-    python profiles/sweep.py [--contexts 4096,16384,65536,131072,262144] [--gammas 1,2,4,8]
+    python profiles/sweep.py [--contexts 4096,16384,32768,65536,131072,262144] [--gammas 1,2,4,8]
 
 Times are CUDA-event medians of back-to-back launches (each launch preceded by
-its own event pair, queued behind a GPU sleep); GB/s counts algorithmic bytes
+its own event pair, queued behind a GPU sleep), and "in-stream": 8 launches replayed
+from one CUDA graph (PDL overlap between them, as in a decode forward); GB/s counts algorithmic bytes
 (planes + (S, Z) params + fp tails + q/o).
 """
 
@@ -37,9 +38,34 @@ def timed(fn, iters=11):
     return statistics.median(s.elapsed_time(e) for s, e in ev) * 1e3  # us
 
 
+def timed_stream(fn, n=8, reps=5):
+    """Per-launch device time of n back-to-back launches replayed from one CUDA graph (PDL overlaps
+    each launch's prologue with the previous one's tail, as inside a decode forward)."""
+    import torch
+
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(n):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        out.append(s.elapsed_time(e) * 1e3 / n)
+    return statistics.median(out)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--contexts", default="4096,16384,65536,131072,262144")
+    ap.add_argument("--contexts", default="4096,16384,32768,65536,131072,262144")
     ap.add_argument("--gammas", default="1,2,4,8")
     a = ap.parse_args()
     import torch
@@ -84,9 +110,11 @@ def main():
             per_tok = kv * (1.0 if view == _lib.VIEW_DRAFT else 2.0) + 8.0 * kv / G + 8.0 * math.ceil(kv / G)
             nbytes = nb * G * per_tok + (G + 3 + T) * kv * 4.0 + T * kv * 8.0
             us = timed(lambda: run._attention(0, view, T, 0, s))
+            # in-stream replays the same layer: only meaningful when it does not fit the 126 MB L2 twice
+            uss = timed_stream(lambda: run._attention(0, view, T, 0, _lib.stream_ptr())) if nbytes > 2.5e8 else float("nan")
             name = "draft " if view == _lib.VIEW_DRAFT else f"verify g={T - 1}"
             print(f"ctx={ctx:7d} {name:11s} T={T}  {us:8.1f} us  {nbytes / us / 1e3:7.0f} GB/s  "
-                  f"{nbytes / us / 1e3 / peak:6.1%}", flush=True)
+                  f"{nbytes / us / 1e3 / peak:6.1%}   in-stream {uss:8.1f} us {nbytes / uss / 1e3 / peak:6.1%}", flush=True)
             del run
         del c
         torch.cuda.empty_cache()
