@@ -1,0 +1,13 @@
+#!/bin/bash
+# End-to-end A/B of runtime settings on the decode cycle (interleaved repetitions on one box).
+#   usage (under gpurun): bash profiles/ab_env_bench.sh OUT "VAR=a" "VAR=b" ...
+OUT=$1; shift
+mkdir -p gpurun_out
+for r in 1 2; do
+  for E in "$@"; do
+    echo "== $E rep=$r" >> gpurun_out/$OUT
+    env $E QS_BENCH_NO_KERNELS=1 python bench.py --modes ${AB_MODES:-both,kv_only,fp16_ar} --steps 32 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1])
+print({k:(round(v.get('tok_s'),2), v.get('acceptance'), round(v.get('ms_per_step'),3)) for k,v in d['modes'].items()}, d['clocks'])" >> gpurun_out/$OUT
+  done
+done
