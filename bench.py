@@ -526,9 +526,10 @@ def measure_spec(geo, fw, dw, cache, first, gamma, steps, warmup, use_graphs, *,
             a_all += sum(r.metrics.accepted_tokens for r in r2)
             cyc += 16
         out["acceptance_long"] = {"rate": a_all / max(1, d_all), "drafted": d_all, "ci95": _binom_ci(a_all, d_all)}
-        a = a_all / max(1, d_all)
-        tpc = (1 - a ** (gamma + 1)) / (1 - a) if a < 1 else gamma + 1.0
-        # the same cycle time at the long-run acceptance (expected tokens per cycle E = (1 - a^(g+1)) / (1 - a))
+        # the same cycle time at the long-run acceptance: every cycle emits its accepted drafts + one
+        # target token per sequence, so tokens per cycle per sequence = 1 + accepted / (cycles * B)
+        tpc = 1.0 + a_all / max(1, (steps + cyc) * B)
+        out["tokens_per_cycle_long"] = tpc
         out["tok_s_at_long_acceptance"] = B * tpc / (dt / steps)
     return out
 

@@ -383,14 +383,15 @@ def _run_linear(pl, x, ncols, *, epi=None, y=None, yh=None, xf=None, gain=None, 
     return y
 
 
-@pytest.mark.parametrize("K,N,ncols", [(64, 48 * 4, 1), (4096, 4096, 1), (176, 64, 5), (4096, 11008 * 2, 9),
-                                       (11008, 4096, 5), (4096, 32000, 16), (1024, 576, 2), (176, 64, 3),
-                                       (11008, 128, 4), (272, 4096, 1), (4096, 6144, 24), (1024, 512, 40),
-                                       (4096, 4096, 48), (4096, 1024, 33)])
-@pytest.mark.parametrize("mode", ["f16", "int4"])
+_LIN_SHAPES = [(64, 48 * 4, 1), (4096, 4096, 1), (176, 64, 5), (4096, 11008 * 2, 9), (11008, 4096, 5),
+               (4096, 32000, 16), (1024, 576, 2), (176, 64, 3), (11008, 128, 4), (272, 4096, 1), (4096, 6144, 24),
+               (1024, 512, 40), (4096, 4096, 48), (4096, 1024, 33)]
+
+
+# INT4 weights are draft-only: one row per sequence, at most 16 sequences per launch
+@pytest.mark.parametrize("K,N,ncols,mode", [(*s, m) for m in ("f16", "int4") for s in _LIN_SHAPES
+                                            if m == "f16" or s[2] <= 16])
 def test_linear_vs_torch(K, N, ncols, mode):
-    if mode == "int4" and ncols > 16:
-        pytest.skip("INT4 weights are draft-only: one row per sequence, at most 16 sequences")
     from paper_2502_10424_b200.runtime import PackedLinear
 
     g = torch.Generator(device="cuda").manual_seed(K + N)
