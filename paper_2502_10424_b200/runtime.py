@@ -209,6 +209,10 @@ def plan_attention_splits(n_heads_total: int, max_chunks: int, ctas_per_sm: int 
     best, best_eff = 1, -1.0
     for waves in (1, 2):  # each extra wave pays one more pipeline fill
         n = max(1, (waves * slots) // heads)
+        if waves > 1 and max_chunks < 64 * n:
+            # short contexts: CTAs of < 64 chunks cannot amortise a second wave's ring fill + merge
+            # (verify at 32K: 4 splits 57.9 us vs 9 splits 62.6 us; 16K 34.3 vs 41.8; 128K keeps 9)
+            break
         eff = (n * heads) / (math.ceil(n * heads / slots) * slots)
         if eff > best_eff + 0.05:
             best, best_eff = n, eff

@@ -19,7 +19,7 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 b = sum(m[k] * scale[unit[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
 import sys; sys.path.insert(0, "."); import bench; md5 = bench.lib_digest()
 out = {"attn_draft_bytes_per_launch": b, "lib_md5": md5, "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
-       "kernel_us": m.get("gpu__time_duration.sum"), "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum, 4th attn_kernel launch of bench.py --profile-kernels"}
+       "kernel_us": m.get("gpu__time_duration.sum", 0) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit.get("gpu__time_duration.sum"), 1.0), "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum, 4th attn_kernel launch of bench.py --profile-kernels"}
 json.dump(out, open("profiles/traffic.json", "w"), indent=1)
 json.dump(out, open("gpurun_out/traffic.json", "w"), indent=1)
 print(out)
