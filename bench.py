@@ -684,7 +684,7 @@ def measured_traffic():
         return None, "no ncu capture (profiles/traffic.json)"
     if t.get("lib_md5") != lib_digest():
         return None, f"ncu capture is of build {t.get('lib_md5')}, not this build"
-    return t.get("attn_draft_bytes_per_launch"), f"ncu --set full capture of this build ({t.get('when', '')})"
+    return t.get("attn_draft_bytes_per_launch"), f"ncu DRAM-bytes capture of these CUDA sources ({t.get('when', '')})"
 
 
 def main():
