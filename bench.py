@@ -425,6 +425,8 @@ def kernel_roofline(geo, fw, qw, hcache, peak, shard=None):
                      ("gemv_int4_down", [lw["down"] for lw in qw.layers]),
                      ("gemv_int4_qkv", [lw["qkv"] for lw in qw.layers]),
                      ("gemv_int4_gate_up", [lw["gu"] for lw in qw.layers]),
+                     ("gemv_int4_o", [lw["o"] for lw in qw.layers]),
+                     ("gemv_draft_lm_head", [qw.lm_head]),
                      ("gemv_f16_lm_head", [fw.lm_head])):  # lm_head: one matrix, isolated
         w = ws[0]
         src = (run.hh, run.hs) if w.K == geo.mlp_hidden else (run.xh, run.xs)
@@ -444,6 +446,22 @@ def kernel_roofline(geo, fw, qw, hcache, peak, shard=None):
         out[name] = {"us": dt * 1e6, "us_isolated": dt_iso * 1e6, "bytes": algo, "gbs": algo / dt / 1e9,
                      "frac": algo / dt / 1e9 / peak, "frac_isolated": algo / dt_iso / 1e9 / peak,
                      "timing": f"graph of {len(fns)} launches (layers' own matrices)" if len(fns) > 1 else "isolated"}
+    if not shard and not ISO_ONLY:
+        # one whole draft forward (INT4 weights, T = 1 per sequence) replayed from a graph, against the
+        # sum of its kernels' in-forward times: what the kernel boundaries cost inside a forward
+        fwd = time_graph([lambda: run.forward(qw, 1, _lib.VIEW_DRAFT)])
+        ksum = L * sum(out[k]["us"] for k in ("attn_draft", "gemv_int4_qkv", "gemv_int4_o", "gemv_int4_gate_up",
+                                              "gemv_int4_down")) + out["gemv_draft_lm_head"]["us"]
+        launches = 1 + 5 * L + 1  # embed, per layer QKV / attention / O / gate-up / down, lm_head
+        out["forward_draft"] = {"us": fwd * 1e6, "kernels_in_forward_us": ksum, "launches": launches,
+                                "boundary_us_per_launch": (fwd * 1e6 - ksum) / launches,
+                                "timing": "graph of one draft forward vs the sum of the kernels' in-forward times"}
+        # the other forwards of the cycles, whole (the cycle time minus gamma draft forwards and one verify
+        # forward is what accept / flush / argmax / the per-cycle host round trip cost)
+        out["forward_draft_f16"] = {"us": time_graph([lambda: run.forward(fw, 1, _lib.VIEW_DRAFT)]) * 1e6,
+                                    "timing": "graph of one kv_only draft forward (fp16 weights, T = 1)"}
+        out["forward_verify"] = {"us": time_graph([lambda: run.forward(fw, 5, _lib.VIEW_TARGET)]) * 1e6,
+                                 "timing": "graph of one verify forward (fp16 weights, T = 5 per sequence)"}
     torch.cuda.synchronize()
     return out
 
@@ -531,6 +549,17 @@ def measure_spec(geo, fw, dw, cache, first, gamma, steps, warmup, use_graphs, *,
         tpc = 1.0 + a_all / max(1, (steps + cyc) * B)
         out["tokens_per_cycle_long"] = tpc
         out["tok_s_at_long_acceptance"] = B * tpc / (dt / steps)
+    # device span of the cycle graph alone (events right around the replay, untimed continuation):
+    # ms_per_step minus this is the GPU's idle time per cycle while the host turns the cycle around
+    spans = []
+    for _ in range(8):
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        eng.cycle(sync=False)
+        eb.record()
+        eng.finish()
+        spans.append(ea.elapsed_time(eb))
+    out["cycle_graph_ms"] = sorted(spans)[len(spans) // 2]
     return out
 
 
