@@ -462,6 +462,11 @@ def kernel_roofline(geo, fw, qw, hcache, peak, shard=None):
                                     "timing": "graph of one kv_only draft forward (fp16 weights, T = 1)"}
         out["forward_verify"] = {"us": time_graph([lambda: run.forward(fw, 5, _lib.VIEW_TARGET)]) * 1e6,
                                  "timing": "graph of one verify forward (fp16 weights, T = 5 per sequence)"}
+        # the cycle's five forwards back to back in one graph, without argmax / accept / flush / copies
+        five = [(lambda i=i: run.forward(qw, 1, _lib.VIEW_DRAFT, row_offset=i, tok_col=i)) for i in range(4)]
+        five.append(lambda: run.forward(fw, 5, _lib.VIEW_TARGET))
+        out["forwards_of_a_cycle"] = {"us": time_graph(five) * 5 * 1e6,
+                                      "timing": "graph of 4 INT4 draft forwards + 1 verify forward (no argmax/accept/copies)"}
     torch.cuda.synchronize()
     return out
 
